@@ -1,0 +1,477 @@
+/*
+ * disttrain_b200.h — C-ABI drop-in boundary for the DistTrain (arXiv 2408.04275)
+ * data-reordering and orchestration-search hot path, implemented with sm_100a
+ * kernels (libdisttrain_b200.so).
+ *
+ * Every entry point replaces one function of the reference C++ planner
+ * `mmplan` (read-only at /root/reference/proj/core).  The citation on each
+ * declaration is the reference interface it stands in for
+ * (`include/` = proj/core/include/mmplan/, `src/` = proj/core/src/).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types cross the boundary.
+ *  - Functions without a `_dev` suffix take HOST buffers (the call stages
+ *    them through device memory and synchronises before returning).
+ *    `_dev` functions take DEVICE pointers and a cudaStream_t passed as
+ *    `void*`; they enqueue work and return without synchronising.
+ *  - Every function returns a dtb_status.  Status codes map 1:1 onto the
+ *    reference exception classes (include/errors.hpp:22-84); the message text
+ *    of the last failure on the calling thread is `dtb_last_error()`.
+ *  - Inputs are validated on the host before any launch, in the same order
+ *    the reference validates them, so the same bad input raises the same
+ *    error class with the same message.
+ *  - The same ABI (with prefixes `mmref_` / `mmport_`) is exported by the
+ *    test oracles under oracle/ so the parity tests can call all three
+ *    implementations through one binding.
+ */
+#ifndef DISTTRAIN_B200_H
+#define DISTTRAIN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DTB_ABI_VERSION 1
+
+/* ---------------------------------------------------------------- status */
+
+/* 1:1 with include/errors.hpp:22-84 (plus two ABI-level codes). */
+typedef enum dtb_status {
+  DTB_OK = 0,
+  DTB_ERR_INTERNAL = 1,            /* InternalError        errors.hpp:52   */
+  DTB_ERR_K_TOO_LARGE = 2,         /* KTooLargeError       errors.hpp:58   */
+  DTB_ERR_INDIVISIBLE_VPP = 3,     /* IndivisibleVppError  errors.hpp:72   */
+  DTB_ERR_BATCH_SIZE_MISMATCH = 4, /* BatchSizeMismatchError errors.hpp:78 */
+  DTB_ERR_CONFIG = 5,              /* ConfigError          errors.hpp:22   */
+  DTB_ERR_EMPTY_PROFILE = 6,       /* EmptyProfileError    errors.hpp:28   */
+  DTB_ERR_INFEASIBLE = 7,          /* InfeasibleError      errors.hpp:46   */
+  DTB_ERR_CAP_EXCEEDED = 8,        /* CapExceededError     errors.hpp:64   */
+  DTB_ERR_INVALID_ARGUMENT = 100,  /* null pointer / ABI limit exceeded    */
+  DTB_ERR_CUDA = 101               /* device failure (no reference analogue) */
+} dtb_status;
+
+/* Message of the last non-OK status returned on this thread. */
+const char* dtb_last_error(void);
+int dtb_abi_version(void);
+
+/* ----------------------------------------------------------- domain PODs */
+
+enum { DTB_ENCODER = 0, DTB_BACKBONE = 1, DTB_GENERATOR = 2 }; /* core.hpp:27 */
+enum { DTB_ASCENDING = 0, DTB_DESCENDING = 1 };                 /* reorder.hpp:29 */
+enum { DTB_FORWARD = 0, DTB_BACKWARD = 1 };                     /* core.hpp:195 */
+
+/* ArchDesc (include/core.hpp:36-50). */
+typedef struct dtb_arch {
+  int32_t layers;
+  int32_t heads;
+  int32_t groups;
+  int32_t reserved;
+  int64_t hidden;
+  int64_t ffn_hidden;
+} dtb_arch;
+
+/* ModuleMemory (include/core.hpp:57-61), bytes. */
+typedef struct dtb_module_memory {
+  double param_grad_bytes;
+  double optimizer_bytes;
+  double activation_bytes_per_mb;
+} dtb_module_memory;
+
+/* ModuleSpec (include/core.hpp:63-67). */
+typedef struct dtb_module_spec {
+  dtb_arch arch;
+  dtb_module_memory mem;
+  int32_t frozen;
+  int32_t reserved;
+} dtb_module_spec;
+
+/* ModelSpec (include/core.hpp:69-88); unit[] indexed by DTB_ENCODER.. */
+typedef struct dtb_model_spec {
+  dtb_module_spec unit[3];
+  int64_t seq_len;
+  double frozen_backward_factor;
+  double dp_sync_seconds;
+} dtb_model_spec;
+
+/* ClusterSpec (include/core.hpp:90-97). */
+typedef struct dtb_cluster_spec {
+  int32_t total_gpus;
+  int32_t gpus_per_node;
+  double peak_flops;
+  double gpu_mem_bytes;
+  double intra_node_bw;
+  double inter_node_bw;
+} dtb_cluster_spec;
+
+/* One CostProfile::add_row call (include/cost_model.hpp:44-45).  Rows are
+ * applied in array order with add_row semantics (sorted insert, last row
+ * wins on a duplicate token load, src/cost_model.cpp:37-60). */
+typedef struct dtb_profile_row {
+  int32_t module;
+  int32_t tp;
+  int32_t has_bwd;
+  int32_t reserved;
+  double token_load;
+  double fwd_s;
+  double bwd_s;
+} dtb_profile_row;
+
+/* CostBook (include/cost_model.hpp:72-83). */
+typedef struct dtb_costbook {
+  const dtb_profile_row* rows;
+  int64_t n_rows;
+  double analytic_efficiency;    /* AnalyticCoeffs::efficiency, default 0.45 */
+  double analytic_bwd_fwd_ratio; /* AnalyticCoeffs::bwd_fwd_ratio, default 2 */
+} dtb_costbook;
+
+/* ParallelismChoice (include/core.hpp:103-110). */
+typedef struct dtb_parallelism {
+  int32_t tp;
+  int32_t dp;
+  int32_t pp;
+} dtb_parallelism;
+
+/* Plan (include/core.hpp:115-150). */
+typedef struct dtb_plan {
+  dtb_parallelism unit[3];
+  int32_t vpp;
+  int64_t global_batch;
+} dtb_plan;
+
+/* WorkloadStats (include/cost_model.hpp:88-92). */
+typedef struct dtb_workload_stats {
+  int64_t seq_len;
+  double mean_encoder_tokens;
+  double mean_generator_tokens;
+} dtb_workload_stats;
+
+/* A span of Samples (include/core.hpp:155-170) in CSR form.  Sample i owns
+ * image_tokens[image_offsets[i] .. image_offsets[i+1]) and likewise audio.
+ * Offsets are absolute int32 indices (ABI limit: < 2^31 subsequences per
+ * call); text_tokens may be NULL (the reorder path never reads it). */
+typedef struct dtb_samples {
+  int64_t n;
+  const int32_t* text_tokens;
+  const int32_t* image_offsets;
+  const int32_t* image_tokens;
+  const int32_t* audio_offsets;
+  const int32_t* audio_tokens;
+} dtb_samples;
+
+/* A span of Microbatches (include/core.hpp:175-193) by their cached keys. */
+typedef struct dtb_microbatches {
+  int64_t n;
+  const int64_t* encoder_tokens;
+  const int64_t* generator_tokens;
+  const int32_t* sample_count;
+} dtb_microbatches;
+
+/* ReorderMode (include/reorder.hpp:86-90). */
+typedef struct dtb_reorder_mode {
+  int32_t intra;
+  int32_t inter;
+  int32_t sort_order;
+} dtb_reorder_mode;
+
+/* ParallelismTuple (include/orchestrator.hpp:41-48). */
+typedef struct dtb_tuple {
+  int32_t tp_me, dp_me;
+  int32_t tp_lm, dp_lm;
+  int32_t tp_mg, dp_mg;
+} dtb_tuple;
+
+/* PredictedTimes (include/orchestrator.hpp:26-30). */
+typedef struct dtb_predicted_times {
+  double t_warm;
+  double t_steady;
+  double t_iter;
+} dtb_predicted_times;
+
+/* CandidateResult (include/orchestrator.hpp:57-67); the reason string is an
+ * enum (text: dtb_infeasible_reason_text). */
+enum {
+  DTB_REASON_NONE = 0,
+  DTB_REASON_DP_NOT_DIVIDING = 1,         /* src/orchestrator.cpp:72    */
+  DTB_REASON_ACTIVATION_ENCODER = 2,      /* src/orchestrator.cpp:96-98 */
+  DTB_REASON_ACTIVATION_BACKBONE = 3,
+  DTB_REASON_ACTIVATION_GENERATOR = 4,
+  DTB_REASON_MEMORY_FLOOR = 5,            /* src/orchestrator.cpp:108,172 */
+  DTB_REASON_NO_INTEGER_SPLIT = 6         /* src/orchestrator.cpp:372   */
+};
+typedef struct dtb_candidate {
+  dtb_tuple tuple;
+  int32_t feasible;
+  int32_t reason;
+  dtb_plan plan;
+  dtb_predicted_times times;
+  double cont_x, cont_y, cont_z, cont_t_iter;
+} dtb_candidate;
+const char* dtb_infeasible_reason_text(int32_t reason);
+
+/* OrchestrationResult (include/orchestrator.hpp:83-89). */
+typedef struct dtb_orchestration_result {
+  dtb_plan best;
+  dtb_predicted_times times;
+  int64_t candidates_evaluated;
+  double solve_seconds;
+} dtb_orchestration_result;
+
+/* MemoryReport (include/cost_model.hpp:98-109). */
+typedef struct dtb_memory_report {
+  double bytes_per_gpu[3];
+  int32_t fits[3];
+  int32_t pass;
+  double capacity_bytes;
+} dtb_memory_report;
+
+/* Per-call outputs of disaggregated_reorder (ReorderReport,
+ * include/reorder.hpp:92-98) for one global batch; arrays caller-owned:
+ * output_order[global_batch], group_load_before/after[backbone.dp]. */
+typedef struct dtb_reorder_report {
+  int32_t* output_order;
+  double* group_load_before;
+  double* group_load_after;
+  double t_iter_before;
+  double t_iter_after;
+} dtb_reorder_report;
+
+/* --------------------------------------------------------------- handles */
+
+typedef struct dtb_context dtb_context;       /* device, stream, scratch */
+typedef struct dtb_cost_model dtb_cost_model; /* CostModel (cost_model.hpp:152) */
+
+dtb_status dtb_context_create(int32_t device, dtb_context** out);
+dtb_status dtb_context_destroy(dtb_context* ctx);
+
+/* CostModel(model, cluster, book) — include/cost_model.hpp:154. Applies
+ * add_row to every row (ConfigError on a bad row, cost_model.cpp:39-48) and
+ * uploads the flattened book to the device. */
+dtb_status dtb_cost_model_create(dtb_context* ctx, const dtb_model_spec* model,
+                                 const dtb_cluster_spec* cluster,
+                                 const dtb_costbook* book,
+                                 dtb_cost_model** out);
+dtb_status dtb_cost_model_destroy(dtb_cost_model* cm);
+
+/* ----------------------------------------------------- L1: cost model (a1-a7) */
+
+/* Sample::cost_size for every sample (include/core.hpp:160-167,
+ * src/core.cpp:90-95). out[n]. */
+dtb_status dtb_cost_sizes(dtb_context* ctx, const dtb_samples* samples,
+                          int64_t* out);
+
+/* CostModel::unit_forward_time / unit_backward_time
+ * (src/cost_model.cpp:255-278) at n token loads; either output may be NULL. */
+dtb_status dtb_unit_times(dtb_context* ctx, const dtb_cost_model* cm,
+                          int32_t module, int32_t tp, int64_t n,
+                          const double* token_loads, double* fwd_out,
+                          double* bwd_out);
+
+/* memory_check (src/cost_model.cpp:167-189), one plan. */
+dtb_status dtb_memory_check(dtb_context* ctx, const dtb_cost_model* cm,
+                            const dtb_plan* plan, dtb_memory_report* out);
+
+/* CostModel::build_stage_times (src/cost_model.cpp:334-362).
+ * fwd/bwd: [mbs->n * virtual_stages] row-major. */
+dtb_status dtb_build_stage_times(dtb_context* ctx, const dtb_cost_model* cm,
+                                 const dtb_plan* plan,
+                                 const dtb_microbatches* mbs, double* fwd,
+                                 double* bwd);
+
+/* microbatch_fwd_keys (src/reorder.cpp:300-317). keys[mbs->n]. */
+dtb_status dtb_microbatch_fwd_keys(dtb_context* ctx, const dtb_cost_model* cm,
+                                   const dtb_plan* plan,
+                                   const dtb_microbatches* mbs, double* keys);
+
+/* compute_stats (src/workload.cpp:206-220). */
+dtb_status dtb_compute_stats(dtb_context* ctx, const dtb_samples* samples,
+                             int64_t seq_len, dtb_workload_stats* out);
+
+/* ------------------------------------------- L3: intra reorder (a10-a14) */
+
+/* intra_partition (src/reorder.cpp:70-90) + IntraPartition::flat
+ * (src/reorder.cpp:46-52).  flat_out[n]: group 0's members in assignment
+ * order, then group 1's, ...; group_offsets_out[m+1] delimits the groups. */
+dtb_status dtb_intra_partition(dtb_context* ctx, const double* sizes,
+                               int64_t n, int32_t m, int32_t sort_order,
+                               int32_t equal_counts, int32_t* flat_out,
+                               int64_t* group_offsets_out);
+
+/* block_group_loads (src/reorder.cpp:111-119). loads_out[m]. */
+dtb_status dtb_block_group_loads(dtb_context* ctx, const double* sizes,
+                                 const int32_t* order, int64_t n, int32_t m,
+                                 double* loads_out);
+
+/* select_min / select_closest (src/reorder.cpp:121-175). out[k]. */
+dtb_status dtb_select_min(dtb_context* ctx, const double* keys, int64_t n_keys,
+                          const int32_t* pending, int64_t n_pending, int32_t k,
+                          int32_t* out);
+dtb_status dtb_select_closest(dtb_context* ctx, const double* keys,
+                              int64_t n_keys, const int32_t* pending,
+                              int64_t n_pending, int32_t k, double target,
+                              int32_t* out);
+
+/* ---------------------------------------- L2: pipeline simulator (a15-a17) */
+
+/* schedule_1f1b (vpp == 1) / schedule_interleaved (src/pipeline_sim.cpp:
+ * 232-254).  fwd/bwd: [l*p].  Event arrays have 2*l*p entries, sorted as
+ * Timeline::events (src/pipeline_sim.cpp:172-178); any event array may be
+ * NULL.  device_busy[p/vpp] may be NULL. */
+dtb_status dtb_schedule(dtb_context* ctx, const double* fwd, const double* bwd,
+                        int32_t l, int32_t p, int32_t vpp, int32_t* ev_device,
+                        int32_t* ev_microbatch, int32_t* ev_stage,
+                        int32_t* ev_phase, double* ev_start, double* ev_end,
+                        double* iteration_time, double* device_busy);
+
+/* get_intervals (src/pipeline_sim.cpp:264-289) over an explicit event list
+ * (any Timeline).  Outputs: n_intervals, starts/ends[n_intervals],
+ * fill_offsets[n_intervals+1], fill_microbatch[fill_offsets[n]]; capacity of
+ * every output array = n_events (+1 for offsets). */
+dtb_status dtb_get_intervals(dtb_context* ctx, int64_t n_events,
+                             const int32_t* ev_device,
+                             const int32_t* ev_microbatch,
+                             const int32_t* ev_stage, const int32_t* ev_phase,
+                             const double* ev_start, const double* ev_end,
+                             int64_t* n_intervals, double* starts,
+                             double* ends, int64_t* fill_offsets,
+                             int32_t* fill_microbatch);
+
+/* interval_windows (src/pipeline_sim.cpp:291-298). volumes[l]. */
+dtb_status dtb_interval_windows(dtb_context* ctx, const double* fwd,
+                                const double* bwd, int32_t l, int32_t p,
+                                double* volumes);
+
+/* Batched makespans: iteration_time[b] of problem b (fwd/bwd [B*l*p]);
+ * device_busy[B * p/vpp] may be NULL.  Same values as dtb_schedule. */
+dtb_status dtb_schedule_batch(dtb_context* ctx, int64_t batch, const double* fwd,
+                              const double* bwd, int32_t l, int32_t p,
+                              int32_t vpp, double* iteration_time,
+                              double* device_busy);
+dtb_status dtb_schedule_batch_dev(dtb_context* ctx, int64_t batch,
+                                  const double* fwd, const double* bwd,
+                                  int32_t l, int32_t p, int32_t vpp,
+                                  double* iteration_time, double* device_busy,
+                                  void* stream);
+
+/* simulate_iteration (src/simulate.cpp:23-48) over n_groups coupled groups;
+ * group g owns microbatches [group_offsets[g], group_offsets[g+1]).
+ * group_times[n_groups] may be NULL. */
+dtb_status dtb_simulate_iteration(dtb_context* ctx, const dtb_cost_model* cm,
+                                  const dtb_plan* plan, int32_t n_groups,
+                                  const int64_t* group_offsets,
+                                  const dtb_microbatches* mbs, double* t_iter,
+                                  double* group_times, int32_t* slowest_group,
+                                  double* slowest_group_time,
+                                  double* mean_bubble_fraction);
+
+/* ------------------------------------------- L3: inter reorder (a18-a19) */
+
+/* inter_reorder (src/reorder.cpp:238-298). order_out[l]. */
+dtb_status dtb_inter_reorder(dtb_context* ctx, const double* fwd,
+                             const double* bwd, int32_t l, int32_t p,
+                             const double* fwd_key, int32_t vpp,
+                             int32_t* order_out);
+
+/* Batched inter_reorder over independent problems (fwd/bwd [B*l*p],
+ * keys [B*l], orders [B*l]). */
+dtb_status dtb_inter_reorder_batch(dtb_context* ctx, int64_t batch,
+                                   const double* fwd, const double* bwd,
+                                   int32_t l, int32_t p, const double* fwd_key,
+                                   int32_t vpp, int32_t* orders);
+dtb_status dtb_inter_reorder_batch_dev(dtb_context* ctx, int64_t batch,
+                                       const double* fwd, const double* bwd,
+                                       int32_t l, int32_t p,
+                                       const double* fwd_key, int32_t vpp,
+                                       int32_t* orders, void* stream);
+
+/* ------------------------------------- L3: disaggregated reorder (a20-a21) */
+
+/* disaggregated_reorder (src/reorder.cpp:319-396) for ONE global batch of
+ * batch->n samples.  The reordered microbatch groups of DisaggregatedResult
+ * are assemble_microbatches(batch[output_order], plan). */
+dtb_status dtb_disaggregated_reorder(dtb_context* ctx, const dtb_cost_model* cm,
+                                     const dtb_plan* plan,
+                                     const dtb_reorder_mode* mode,
+                                     const dtb_samples* batch,
+                                     dtb_reorder_report* report);
+
+/* disaggregated_reorder over a stream of n_batches consecutive global
+ * batches (samples->n == n_batches * plan->global_batch).  Outputs:
+ * output_order[n] (batch-local indices), load_before/after[n_batches*dp_lm],
+ * t_iter_before/after[n_batches]; greedy_kept[n_batches] (1 when the greedy
+ * split won the fallback check, src/reorder.cpp:350-353) may be NULL.
+ * Host variant pipelines host->device copies with compute. */
+dtb_status dtb_reorder_stream(dtb_context* ctx, const dtb_cost_model* cm,
+                              const dtb_plan* plan,
+                              const dtb_reorder_mode* mode,
+                              const dtb_samples* samples, int64_t n_batches,
+                              int32_t* output_order, double* load_before,
+                              double* load_after, double* t_iter_before,
+                              double* t_iter_after, uint8_t* greedy_kept);
+dtb_status dtb_reorder_stream_dev(dtb_context* ctx, const dtb_cost_model* cm,
+                                  const dtb_plan* plan,
+                                  const dtb_reorder_mode* mode,
+                                  const dtb_samples* samples,
+                                  int64_t n_batches, int32_t* output_order,
+                                  double* load_before, double* load_after,
+                                  double* t_iter_before, double* t_iter_after,
+                                  uint8_t* greedy_kept, void* stream);
+
+/* ------------------------------------------ L3: orchestration (a22-a29) */
+
+/* predict_times (src/orchestrator.cpp:237-266) for n plans. */
+dtb_status dtb_predict_times(dtb_context* ctx, const dtb_cost_model* cm,
+                             const dtb_workload_stats* stats,
+                             const dtb_plan* plans, int64_t n,
+                             dtb_predicted_times* out);
+
+/* enumerate_parallelism (src/orchestrator.cpp:268-301).  Writes the count;
+ * with tuples != NULL also writes min(count, capacity) tuples in the
+ * reference's sorted order. */
+dtb_status dtb_enumerate_parallelism(dtb_context* ctx,
+                                     const dtb_cluster_spec* cluster,
+                                     int64_t global_batch, int64_t* count,
+                                     dtb_tuple* tuples, int64_t capacity);
+
+/* solve_subproblem (src/orchestrator.cpp:303-378) for n tuples. */
+dtb_status dtb_solve_subproblem(dtb_context* ctx, const dtb_cost_model* cm,
+                                const dtb_workload_stats* stats,
+                                const dtb_tuple* tuples, int64_t n,
+                                int64_t global_batch, int32_t vpp,
+                                dtb_candidate* out);
+
+/* model_orchestration (src/orchestrator.cpp:380-405).  With candidates !=
+ * NULL the per-tuple table (OrchestrationOptions::keep_candidates) is
+ * written in tuple order, up to `capacity` rows. */
+dtb_status dtb_model_orchestration(dtb_context* ctx, const dtb_cost_model* cm,
+                                   const dtb_workload_stats* stats,
+                                   int64_t global_batch, int32_t vpp,
+                                   dtb_orchestration_result* result,
+                                   dtb_candidate* candidates,
+                                   int64_t capacity);
+
+/* One shard of the search for multi-GPU runs: evaluates the tuples whose
+ * sorted index i satisfies i % shard_count == shard_index and writes the
+ * shard's BestTracker winner (feasible == 0 when none) to *best_dev, a
+ * DEVICE pointer; *evaluated_dev (device int64) gets the tuple count.
+ * dtb_best_reduce_dev folds n such records (device array) into one with the
+ * reference's tie-break (src/orchestrator.cpp:211-233). */
+dtb_status dtb_orchestration_shard_dev(dtb_context* ctx,
+                                       const dtb_cost_model* cm,
+                                       const dtb_workload_stats* stats,
+                                       int64_t global_batch, int32_t vpp,
+                                       int64_t shard_index,
+                                       int64_t shard_count,
+                                       dtb_candidate* best_dev,
+                                       int64_t* evaluated_dev, void* stream);
+dtb_status dtb_best_reduce_dev(dtb_context* ctx, const dtb_candidate* records,
+                               int64_t n, dtb_candidate* best_dev,
+                               void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* DISTTRAIN_B200_H */

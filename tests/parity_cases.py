@@ -1,0 +1,288 @@
+"""Parity cases shared by the oracle pinning tests (port vs compiled
+reference, CPU) and the GPU parity tests (CUDA path vs oracle).
+
+Every `check_*(impl, oracle, ...)` feeds identical inputs to both planners
+and asserts BIT-EXACT equality: orders, assignments and plans are integers,
+and every floating value is produced by the same IEEE operation sequence
+(the north_star's 1e-6 relative slack is not needed and not used)."""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2408_04275_b200.api import ASCENDING, DESCENDING, SampleBatch, stats_to_c
+from paper_2408_04275_b200.workload import synth_stream
+
+import helpers as H
+
+
+def assert_same(a, b, what=""):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, f"{what}: shape {a.shape} vs {b.shape}"
+    if a.dtype.kind == "f":
+        same = (a == b) | (np.isnan(a) & np.isnan(b))
+        if not same.all():
+            i = np.flatnonzero(~same.ravel())[0]
+            raise AssertionError(f"{what}: first mismatch at {i}: {a.ravel()[i]!r} vs {b.ravel()[i]!r}"
+                                 f" ({(~same).sum()} of {same.size})")
+    else:
+        if not np.array_equal(a, b):
+            i = np.flatnonzero((a != b).ravel())[0]
+            raise AssertionError(f"{what}: first mismatch at {i}: {a.ravel()[i]} vs {b.ravel()[i]}"
+                                 f" ({(a != b).sum()} of {a.size})")
+
+
+# ------------------------------------------------------------------ intra
+def intra_size_sets(rng):
+    yield np.array([1, 3, 2, 4.0]), 2
+    yield np.array([2, 3, 4, 5.0]), 2
+    yield np.full(12, 3.0), 4
+    yield np.zeros(10), 3
+    yield np.array([0.0, -0.0, 0.0, 5.0, -0.0]), 2
+    for _ in range(20):
+        n = int(rng.integers(1, 300))
+        m = int(rng.integers(1, 20))
+        kind = rng.integers(0, 4)
+        if kind == 0:
+            s = rng.lognormal(4.0, 0.8, n)
+        elif kind == 1:
+            s = 2.0 * rng.integers(0, 50, n)
+        elif kind == 2:
+            s = np.where(rng.random(n) < 0.35, 0.0, 2.0 * rng.integers(1, 4000, n))
+        else:
+            s = rng.integers(0, 3, n).astype(float)
+        yield s.astype(float), m
+    for n, m in ((512, 8), (2048, 64), (4096, 128)):
+        yield 2.0 * synth_stream(n, int(rng.integers(1, 1 << 30)), "skewed").modality(), m
+
+
+def check_intra(impl, oracle, rng):
+    for sizes, m in intra_size_sets(rng):
+        for order in (ASCENDING, DESCENDING):
+            for eq in (False, True):
+                a = impl.intra_partition(sizes, m, order, eq)
+                b = oracle.intra_partition(sizes, m, order, eq)
+                assert a.groups == b.groups, (len(sizes), m, order, eq)
+        flat = oracle.intra_partition(sizes, m, ASCENDING, True).flat()
+        if len(sizes) >= m:
+            assert_same(impl.block_group_loads(sizes, flat, m),
+                        oracle.block_group_loads(sizes, flat, m), "block loads")
+
+
+def check_select(impl, oracle, rng):
+    for _ in range(50):
+        n = int(rng.integers(1, 40))
+        keys = np.round(rng.lognormal(0, 0.7, n), int(rng.integers(0, 3)))
+        pending = np.sort(rng.choice(n, int(rng.integers(1, n + 1)), replace=False))
+        k = int(rng.integers(0, len(pending) + 1))
+        assert impl.select_min(keys, pending, k) == oracle.select_min(keys, pending, k)
+        target = float(rng.uniform(0, keys.sum()))
+        assert (impl.select_closest(keys, pending, k, target)
+                == oracle.select_closest(keys, pending, k, target))
+
+
+# ---------------------------------------------------------------- schedule
+def schedule_cases(rng):
+    for p in range(1, 7):
+        for l in range(1, 7):
+            yield np.full((l, p), 0.7), np.full((l, p), 1.3), 1
+    for _ in range(40):
+        l = int(rng.integers(1, 40))
+        p = int(rng.integers(1, 9))
+        f, b = H.random_times(rng, l, p)
+        yield f, b, 1
+    for _ in range(20):
+        vpp = int(rng.integers(2, 4))
+        d = int(rng.integers(1, 4))
+        p = d * vpp
+        l = d * int(rng.integers(1, 6))
+        f, b = H.random_times(rng, l, p)
+        yield f, b, vpp
+
+
+def check_schedule(impl, oracle, rng):
+    for f, b, vpp in schedule_cases(rng):
+        ta = impl.schedule(f, b, vpp)
+        tb = oracle.schedule(f, b, vpp)
+        assert ta.iteration_time == tb.iteration_time
+        for fld in ("device", "microbatch", "stage", "phase", "start", "end", "device_busy"):
+            assert_same(getattr(ta, fld), getattr(tb, fld), fld)
+        ia, ib = impl.get_intervals(ta), oracle.get_intervals(tb)
+        assert [(i.start, i.end, i.filled_by) for i in ia] == [(i.start, i.end, i.filled_by) for i in ib]
+        if vpp == 1:
+            assert_same(impl.interval_windows(f, b), oracle.interval_windows(f, b), "windows")
+    # batched makespans
+    for vpp, (l, p) in ((1, (32, 4)), (1, (7, 3)), (2, (8, 4))):
+        f = rng.uniform(0.1, 2.0, (17, l, p))
+        b = rng.uniform(0.1, 2.0, (17, l, p))
+        ia, ba = impl.schedule_batch(f, b, vpp, with_busy=True)
+        ib, bb = oracle.schedule_batch(f, b, vpp, with_busy=True)
+        assert_same(ia, ib, "batch makespan")
+        assert_same(ba, bb, "batch busy")
+
+
+# ------------------------------------------------------------------- inter
+def inter_cases(rng):
+    for _ in range(30):
+        l = int(rng.integers(1, 14))
+        p = int(rng.integers(1, 6))
+        enc = rng.lognormal(0, 0.6, l)
+        f, b = H.skewed_times(enc, p, 0.3)
+        yield f, b, f[:, 0].copy(), 1
+    for _ in range(20):
+        l = int(rng.integers(2, 40))
+        p = int(rng.integers(2, 7))
+        f, b = H.random_times(rng, l, p)
+        yield f, b, rng.lognormal(0, 0.5, l), 1
+    for _ in range(4):  # tie-heavy keys
+        l, p = 24, 4
+        f, b = H.random_times(rng, l, p)
+        yield f, b, np.round(rng.uniform(0, 3, l)), 1
+    for _ in range(12):
+        vpp = int(rng.integers(2, 4))
+        d = int(rng.integers(2, 4))
+        l = d * int(rng.integers(1, 5))
+        f, b = H.skewed_times(rng.lognormal(0, 0.5, l), d * vpp, 0.4)
+        yield f, b, f[:, 0].copy(), vpp
+    f, b = H.skewed_times(np.full(8, 0.7), 4, 0.4)
+    yield f, b, np.full(8, 0.7), 2
+
+
+def check_inter(impl, oracle, rng):
+    for f, b, keys, vpp in inter_cases(rng):
+        assert (impl.inter_reorder(f, b, keys, vpp)
+                == oracle.inter_reorder(f, b, keys, vpp)), (f.shape, vpp)
+    f = rng.uniform(0.1, 2.0, (9, 32, 4))
+    b = 2.0 * f
+    keys = f[:, :, 0].copy()
+    assert_same(impl.inter_reorder_batch(f, b, keys, 1),
+                oracle.inter_reorder_batch(f, b, keys, 1), "inter batch")
+
+
+# -------------------------------------------------------------- cost model
+def cost_models(impl, oracle):
+    """(name, impl handle, oracle handle, plans) over several books."""
+    cases = [
+        ("desk", H.desk_model(), H.desk_cluster(64), H.desk_book()),
+        ("toy-flat", H.toy_model(), H.toy_cluster(16), H.flat_book(0.4, 1.0, 0.4)),
+        ("analytic", H.toy_model(), H.toy_cluster(16), H.Book(analytic_efficiency=0.5)),
+        ("llava", H.llava_model(), H.a800_cluster(64), H.llava_book()),
+    ]
+    for name, model, cluster, book in cases:
+        yield name, impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
+
+
+PLANS = [
+    H.plan((1, 2, 1), (1, 2, 2), (1, 2, 1), 8),
+    H.plan((1, 8, 1), (1, 8, 2), (1, 8, 1), 512),
+    H.plan((2, 4, 1), (2, 8, 2), (1, 8, 1), 64),
+    H.plan((1, 2, 1), (1, 4, 2), (1, 4, 1), 48, vpp=2),
+    H.plan((1, 1, 1), (1, 2, 1), (1, 1, 1), 8),
+]
+
+
+def check_cost(impl, oracle, rng):
+    for name, ci, co in cost_models(impl, oracle):
+        for mod in range(3):
+            for tp in (1, 2, 4, 8):
+                loads = np.concatenate([[0.0, 8192.0, 9000.0, 1.5], rng.uniform(0, 10000, 20)])
+                fa, ba = impl.unit_times(ci, mod, tp, loads)
+                fb, bb = oracle.unit_times(co, mod, tp, loads)
+                assert_same(fa, fb, f"{name} fwd")
+                assert_same(ba, bb, f"{name} bwd")
+        for pl in PLANS:
+            l = 12
+            enc = rng.integers(0, 20000, l)
+            cnt = np.full(l, max(1, pl.samples_per_microbatch()))
+            fa, ba = impl.build_stage_times(ci, pl, enc, enc, cnt)
+            fb, bb = oracle.build_stage_times(co, pl, enc, enc, cnt)
+            assert_same(fa, fb, f"{name} stage fwd")
+            assert_same(ba, bb, f"{name} stage bwd")
+            assert_same(impl.microbatch_fwd_keys(ci, pl, enc, enc, cnt),
+                        oracle.microbatch_fwd_keys(co, pl, enc, enc, cnt), f"{name} keys")
+            ma, mb = impl.memory_check(ci, pl), oracle.memory_check(co, pl)
+            assert list(ma.bytes_per_gpu) == list(mb.bytes_per_gpu) and ma.pass_ == mb.pass_
+
+
+# ------------------------------------------------------- disaggregated path
+def disagg_cases(rng):
+    yield H.plan((1, 8, 1), (1, 8, 2), (1, 8, 1), 512), "skewed"
+    yield H.plan((1, 2, 1), (1, 8, 2), (1, 4, 1), 256), "mixed"
+    yield H.plan((1, 2, 1), (1, 2, 2), (1, 2, 1), 8), "skewed"
+    yield H.plan((1, 1, 1), (1, 2, 1), (1, 1, 1), 8), "skewed"
+    yield H.plan((1, 2, 1), (1, 4, 2), (1, 4, 1), 64, vpp=2), "mixed"
+    yield H.plan((1, 4, 1), (1, 4, 2), (1, 4, 1), 90), "mixed"  # n % m != 0 blocks
+
+
+def check_disaggregated(impl, oracle, rng, modes=None):
+    modes = modes or [dict(intra=True, inter=True), dict(intra=True, inter=False),
+                      dict(intra=True, inter=True, sort_order=DESCENDING),
+                      dict(intra=False, inter=True)]
+    model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
+    ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
+    for pl, fam in disagg_cases(rng):
+        batch = synth_stream(pl.global_batch, int(rng.integers(1, 1 << 30)), fam)
+        for md in modes:
+            ra = impl.disaggregated_reorder(ci, pl, batch, **md)
+            rb = oracle.disaggregated_reorder(co, pl, batch, **md)
+            tag = f"{pl} {md}"
+            assert_same(ra.output_order, rb.output_order, tag + " order")
+            assert_same(ra.group_load_before, rb.group_load_before, tag + " lb")
+            assert_same(ra.group_load_after, rb.group_load_after, tag + " la")
+            assert ra.t_iter_before == rb.t_iter_before, tag
+            assert ra.t_iter_after == rb.t_iter_after, tag
+
+
+def check_stream(impl, oracle, rng, n_batches=3, bs=512, dp=8, inter=True):
+    model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
+    ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
+    pl = H.plan((1, dp, 1), (1, dp, 2), (1, dp, 1), bs)
+    s = synth_stream(n_batches * bs, int(rng.integers(1, 1 << 30)), "mixed")
+    ra = impl.reorder_stream(ci, pl, s, n_batches, inter=inter)
+    rb = oracle.reorder_stream(co, pl, s, n_batches, inter=inter)
+    for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
+        assert_same(ra[k], rb[k], k)
+
+
+def check_simulate(impl, oracle, rng):
+    model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
+    ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
+    for pl in PLANS:
+        groups = []
+        for g in range(int(rng.integers(1, 5))):
+            l = pl.microbatch_count() if pl.vpp > 1 else int(rng.integers(1, 20))
+            enc = rng.integers(0, 9000, l)
+            groups.append((enc, enc, np.full(l, max(1, pl.samples_per_microbatch()))))
+        a = impl.simulate_iteration(ci, pl, groups)
+        b = oracle.simulate_iteration(co, pl, groups)
+        for k in a:
+            assert_same(a[k], b[k], k)
+
+
+# ------------------------------------------------------------ orchestration
+def orch_cases():
+    yield H.toy_model(), H.quiet_cluster(12), H.flat_book(1.0, 1.0, 1.0), 8, 1
+    yield H.toy_model(), H.quiet_cluster(16), H.tp_scaled_book(0.3, 1.7, 0.9), 4, 1
+    yield H.toy_model(), H.quiet_cluster(24), H.tp_scaled_book(0.4, 2.0, 0.6), 8, 2
+    yield H.desk_model(), H.desk_cluster(64), H.desk_book(), 64, 1
+    yield H.mllm72b_model(), H.a800_cluster(112), H.mllm72b_book(), 240, 1
+
+
+def check_orchestration(impl, oracle, rng):
+    for model, cluster, book, bs, vpp in orch_cases():
+        ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
+        stats = stats_to_c(model.seq_len, 1000.0, 1000.0)
+        ta = impl.enumerate_parallelism(cluster, bs)
+        tb = oracle.enumerate_parallelism(cluster, bs)
+        assert ta == tb
+        sub = [tb[i] for i in sorted(set(rng.integers(0, len(tb), 200).tolist()))]
+        ca = impl.solve_subproblem(ci, stats, sub, bs, vpp)
+        cb = oracle.solve_subproblem(co, stats, sub, bs, vpp)
+        for x, y in zip(ca, cb):
+            assert x == y, (x, y)
+        ra = impl.model_orchestration(ci, stats, bs, vpp)
+        rb = oracle.model_orchestration(co, stats, bs, vpp)
+        assert ra["best"] == rb["best"] and ra["times"] == rb["times"]
+        assert ra["candidates_evaluated"] == rb["candidates_evaluated"]
+        plans = [c.plan for c in cb if c.feasible][:50]
+        if plans:
+            assert impl.predict_times(ci, stats, plans) == oracle.predict_times(co, stats, plans)
