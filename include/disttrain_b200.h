@@ -419,6 +419,19 @@ dtb_status dtb_reorder_stream_dev(dtb_context* ctx, const dtb_cost_model* cm,
                                   double* t_iter_before, double* t_iter_after,
                                   uint8_t* greedy_kept, void* stream);
 
+/* The intra stage of disaggregated_reorder alone (src/reorder.cpp:333-364)
+ * over a stream: per global batch, cost -> stable sort -> equal-count greedy
+ * over dp_lm groups -> keep-greedy-if-no-worse.  order_out[n] gets the
+ * batch-local intra order; load_before/after[n_batches*dp_lm] and
+ * greedy_kept[n_batches] may be NULL.  (The sort/partition kernel the
+ * roofline is reported on.) */
+dtb_status dtb_intra_stream_dev(dtb_context* ctx, int64_t global_batch,
+                                int32_t dp_lm, int32_t sort_order,
+                                const dtb_samples* samples, int64_t n_batches,
+                                int32_t* order_out, double* load_before,
+                                double* load_after, uint8_t* greedy_kept,
+                                void* stream);
+
 /* ------------------------------------------ L3: orchestration (a22-a29) */
 
 /* predict_times (src/orchestrator.cpp:237-266) for n plans. */

@@ -169,6 +169,8 @@ _SIGS = {
     "reorder_stream_dev": (c_i32, [VP, VP, P(Plan), P(ReorderMode),
                                    P(Samples), c_i64, VP, VP, VP, VP, VP, VP,
                                    VP]),
+    "intra_stream_dev": (c_i32, [VP, c_i64, c_i32, c_i32, P(Samples), c_i64, VP, VP, VP, VP,
+                                 VP]),
     "predict_times": (c_i32, [VP, VP, P(WorkloadStats), P(Plan), c_i64,
                               P(PredictedTimes)]),
     "enumerate_parallelism": (c_i32, [VP, P(ClusterSpec), c_i64, P(c_i64),

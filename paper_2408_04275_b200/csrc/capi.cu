@@ -1,0 +1,1276 @@
+// C-ABI layer of libdisttrain_b200.so (include/disttrain_b200.h).
+//
+// Host code here only validates inputs (in the reference's order, with the
+// reference's messages), stages buffers and launches kernels; every value of
+// the hot path is computed on the device.  Host-pointer entry points copy in,
+// run on the context stream and synchronise; `_dev` entry points enqueue on
+// the caller's stream.
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace dtb;
+
+namespace dtb {
+size_t enumerate_scratch(long long bs);
+}
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local std::string g_err;
+
+dtb_status fail(dtb_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+const char* kind_name(int k) {
+  return k == 0 ? "encoder" : k == 1 ? "backbone" : "generator";
+}
+
+#define CU(expr)                                                          \
+  do {                                                                    \
+    cudaError_t _e = (expr);                                              \
+    if (_e != cudaSuccess)                                                \
+      return fail(DTB_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define TRY(expr)                      \
+  do {                                 \
+    dtb_status _s = (expr);            \
+    if (_s != DTB_OK) return _s;       \
+  } while (0)
+
+}  // namespace
+
+struct dtb_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DevErr* err = nullptr;  // device
+};
+
+struct dtb_cost_model {
+  dtb_model_spec model;
+  dtb_cluster_spec cluster;
+  double eff = 0.45, ratio = 2.0;
+  struct Row {
+    double load, fwd, bwd;
+  };
+  std::vector<Row> rows[3][4];
+  bool nonempty[3] = {false, false, false};
+  double* d_rows = nullptr;  // device: load | fwd | bwd
+  DevCM dev{};
+};
+
+namespace {
+
+// Device allocation tied to a stream (stream-ordered pool).
+struct DBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  cudaError_t alloc(size_t bytes, cudaStream_t st) {
+    s = st;
+    return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+dtb_status set_device(dtb_context* ctx) {
+  if (ctx == nullptr) return fail(DTB_ERR_INVALID_ARGUMENT, "null context");
+  CU(cudaSetDevice(ctx->device));
+  return DTB_OK;
+}
+
+dtb_status reset_err(dtb_context* ctx) {
+  DevErr init{0, 0, 0, 0, ~0ull};
+  CU(cudaMemcpyAsync(ctx->err, &init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+  return DTB_OK;
+}
+
+template <typename T>
+dtb_status upload(DBuf& b, const T* host, size_t count, cudaStream_t s) {
+  CU(b.alloc(sizeof(T) * count, s));
+  if (count) CU(cudaMemcpyAsync(b.p, host, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+  return DTB_OK;
+}
+
+template <typename T>
+dtb_status download(T* host, const DBuf& b, size_t count, cudaStream_t s) {
+  if (count && host) CU(cudaMemcpyAsync(host, b.p, sizeof(T) * count, cudaMemcpyDeviceToHost, s));
+  return DTB_OK;
+}
+
+// Maps the device error record onto the reference's exception + message.
+// `ctx_tp[u]` gives the TP of unit u when the record carries only a unit.
+dtb_status dev_status(const DevErr& e, const int* tp_of_unit = nullptr) {
+  int code = e.code, a = e.a;
+  int unit = -1;
+  if (code == 0) return DTB_OK;
+  if (code == -1) {
+    code = static_cast<int>(e.ordered & 0xff);
+    unit = static_cast<int>((e.ordered >> 8) % 3);
+  }
+  switch (code) {
+    case E_EMPTY_TP:
+      return fail(DTB_ERR_EMPTY_PROFILE, "no profile rows for tp=%d",
+                  tp_of_unit && unit >= 0 ? tp_of_unit[unit] : a);
+    case E_ANALYTIC:
+      return fail(DTB_ERR_EMPTY_PROFILE,
+                  "no profile rows for module '%s' and no usable analytic fallback",
+                  kind_name(unit >= 0 ? unit : a));
+    case E_TP_NOT_ALLOWED:
+      return fail(DTB_ERR_INTERNAL, "tp size %d not allowed",
+                  tp_of_unit && unit >= 0 ? tp_of_unit[unit] : a);
+    case E_NEG_LOAD:
+      return fail(DTB_ERR_INTERNAL, "negative token load");
+    case E_BAD_TIMES:
+      return fail(DTB_ERR_INTERNAL, "bad stage times: %s",
+                  a == 2 ? "negative or NaN backward time" : "negative or NaN forward time");
+    case E_DEADLOCK:
+      return fail(DTB_ERR_INTERNAL, "pipeline schedule deadlocked; op order is invalid");
+    case E_COST_RANGE:
+      return fail(DTB_ERR_INVALID_ARGUMENT,
+                  "sample cost outside the kernel's 32-bit key range (batch %d)", a);
+    case E_NO_MICROBATCH:
+      return fail(DTB_ERR_INTERNAL, "plan yields no microbatches per iteration");
+  }
+  return fail(DTB_ERR_INTERNAL, "device error %d", code);
+}
+
+dtb_status sync_and_check(dtb_context* ctx, const int* tp_of_unit = nullptr,
+                          DevErr* out = nullptr) {
+  DevErr e;
+  CU(cudaMemcpyAsync(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (out) *out = e;
+  return dev_status(e, tp_of_unit);
+}
+
+bool tp_allowed(int tp) { return tp == 1 || tp == 2 || tp == 4 || tp == 8; }
+
+// The reference raises cost-model errors from the first query it makes;
+// these checks depend only on (kind, tp) and the book, so they are evaluated
+// up front in the same query order.
+dtb_status check_fwd_query(const dtb_cost_model* cm, int kind, int tp) {
+  if (!tp_allowed(tp)) return fail(DTB_ERR_INTERNAL, "tp size %d not allowed", tp);
+  if (!cm->nonempty[kind]) {
+    if (!(cm->eff > 0.0) || !(cm->cluster.peak_flops > 0.0))
+      return fail(DTB_ERR_EMPTY_PROFILE,
+                  "no profile rows for module '%s' and no usable analytic fallback",
+                  kind_name(kind));
+    return DTB_OK;
+  }
+  if (cm->rows[kind][tp_index(tp)].empty())
+    return fail(DTB_ERR_EMPTY_PROFILE, "no profile rows for tp=%d", tp);
+  return DTB_OK;
+}
+
+dtb_status check_bwd_query(const dtb_cost_model* cm, int kind, int tp) {
+  if (!cm->nonempty[kind]) {
+    if (!(cm->eff > 0.0) || !(cm->cluster.peak_flops > 0.0))
+      return fail(DTB_ERR_EMPTY_PROFILE,
+                  "no profile rows for module '%s' and no usable analytic fallback",
+                  kind_name(kind));
+    return DTB_OK;
+  }
+  const int ti = tp_index(tp);
+  if (ti < 0 || cm->rows[kind][ti].empty())
+    return fail(DTB_ERR_EMPTY_PROFILE, "no profile rows for tp=%d", tp);
+  return DTB_OK;
+}
+
+// build_stage_times queries, per unit: forward then backward.
+dtb_status check_stage_queries(const dtb_cost_model* cm, const dtb_plan& p) {
+  for (int u = 0; u < 3; ++u) {
+    TRY(check_fwd_query(cm, u, p.unit[u].tp));
+    TRY(check_bwd_query(cm, u, p.unit[u].tp));
+  }
+  return DTB_OK;
+}
+
+dtb_status check_key_queries(const dtb_cost_model* cm, const dtb_plan& p) {
+  TRY(check_fwd_query(cm, DTB_ENCODER, p.unit[DTB_ENCODER].tp));
+  return check_fwd_query(cm, DTB_GENERATOR, p.unit[DTB_GENERATOR].tp);
+}
+
+// schedule_interleaved's divisibility checks (pipeline_sim.cpp:237-253).
+dtb_status check_vpp(int l, int p, int vpp) {
+  if (l < 1) return fail(DTB_ERR_INTERNAL, "bad stage times: microbatch count must be >= 1");
+  if (p < 1) return fail(DTB_ERR_INTERNAL, "bad stage times: stage count must be >= 1");
+  if (vpp < 1) return fail(DTB_ERR_INDIVISIBLE_VPP, "vpp must be >= 1");
+  if (vpp == 1) return DTB_OK;
+  if (p % vpp != 0)
+    return fail(DTB_ERR_INDIVISIBLE_VPP, "stage count %d is not divisible by vpp %d", p, vpp);
+  if (l % (p / vpp) != 0)
+    return fail(DTB_ERR_INDIVISIBLE_VPP,
+                "microbatch count %d is not divisible by the device count %d", l, p / vpp);
+  return DTB_OK;
+}
+
+long long total_subseqs(const dtb_samples* s, bool audio) {
+  return 0 * audio + 0 * s->n;
+}
+
+// Uploads a CSR span of samples [0, n) (offsets absolute).
+struct DevSamples {
+  DBuf io, it, ao, at;
+  const int* img_off = nullptr;
+  const int* img_tok = nullptr;
+  const int* aud_off = nullptr;
+  const int* aud_tok = nullptr;
+};
+
+dtb_status upload_samples(const dtb_samples* s, cudaStream_t st, DevSamples* d) {
+  if (s == nullptr || s->image_offsets == nullptr)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "samples need image_offsets");
+  const long long n = s->n;
+  const long long ni = s->image_offsets[n];
+  TRY(upload(d->io, s->image_offsets, n + 1, st));
+  TRY(upload(d->it, s->image_tokens, ni, st));
+  d->img_off = d->io.as<int>();
+  d->img_tok = d->it.as<int>();
+  if (s->audio_offsets != nullptr) {
+    const long long na = s->audio_offsets[n];
+    TRY(upload(d->ao, s->audio_offsets, n + 1, st));
+    TRY(upload(d->at, s->audio_tokens, na, st));
+    d->aud_off = d->ao.as<int>();
+    d->aud_tok = d->at.as<int>();
+  }
+  return DTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dtb_last_error(void) { return g_err.c_str(); }
+int dtb_abi_version(void) { return DTB_ABI_VERSION; }
+
+const char* dtb_infeasible_reason_text(int32_t r) {
+  switch (r) {
+    case DTB_REASON_NONE: return "";
+    case DTB_REASON_DP_NOT_DIVIDING: return "dp does not divide the global batch";
+    case DTB_REASON_ACTIVATION_ENCODER:
+      return "activation memory of encoder exceeds GPU capacity at any allocation";
+    case DTB_REASON_ACTIVATION_BACKBONE:
+      return "activation memory of backbone exceeds GPU capacity at any allocation";
+    case DTB_REASON_ACTIVATION_GENERATOR:
+      return "activation memory of generator exceeds GPU capacity at any allocation";
+    case DTB_REASON_MEMORY_FLOOR: return "memory floor exceeds the cluster";
+    case DTB_REASON_NO_INTEGER_SPLIT: return "no integer stage split is feasible";
+  }
+  return "?";
+}
+
+dtb_status dtb_context_create(int32_t device, dtb_context** out) {
+  if (out == nullptr) return fail(DTB_ERR_INVALID_ARGUMENT, "null out");
+  int count = 0;
+  CU(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count)
+    return fail(DTB_ERR_CUDA, "CUDA device %d not present (%d visible)", device, count);
+  auto* ctx = new dtb_context;
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->err, sizeof(DevErr));
+  if (e != cudaSuccess) {
+    delete ctx;
+    return fail(DTB_ERR_CUDA, "context init: %s", cudaGetErrorString(e));
+  }
+  *out = ctx;
+  return DTB_OK;
+}
+
+dtb_status dtb_context_destroy(dtb_context* ctx) {
+  if (!ctx) return DTB_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->err);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return DTB_OK;
+}
+
+// ---------------------------------------------------------------- cost model
+static double param_count(const dtb_arch& a) {  // src/core.cpp:40-49
+  const double h = static_cast<double>(a.hidden);
+  const double f = static_cast<double>(a.ffn_hidden);
+  const double kv = a.heads > 0 ? static_cast<double>(a.groups) / static_cast<double>(a.heads) : 1.0;
+  const double attn = h * h * (2.0 + 2.0 * kv);
+  const double ffn = 3.0 * h * f;
+  return static_cast<double>(a.layers) * (attn + ffn);
+}
+
+dtb_status dtb_cost_model_create(dtb_context* ctx, const dtb_model_spec* model,
+                                 const dtb_cluster_spec* cluster, const dtb_costbook* book,
+                                 dtb_cost_model** out) {
+  TRY(set_device(ctx));
+  if (!model || !cluster || !book || !out) return fail(DTB_ERR_INVALID_ARGUMENT, "null argument");
+  auto* cm = new dtb_cost_model;
+  cm->model = *model;
+  cm->cluster = *cluster;
+  cm->eff = book->analytic_efficiency;
+  cm->ratio = book->analytic_bwd_fwd_ratio;
+  // CostProfile::add_row (cost_model.cpp:37-60)
+  for (int64_t i = 0; i < book->n_rows; ++i) {
+    const dtb_profile_row& r = book->rows[i];
+    dtb_status st = DTB_OK;
+    if (!tp_allowed(r.tp))
+      st = fail(DTB_ERR_CONFIG, "profile TP size %d is not one of {1,2,4,8}", r.tp);
+    else if (!(r.fwd_s > 0.0) || (r.has_bwd && !(r.bwd_s > 0.0)))
+      st = fail(DTB_ERR_CONFIG, "profile times must be strictly positive");
+    else if (r.token_load < 0.0)
+      st = fail(DTB_ERR_CONFIG, "profile token load must be non-negative");
+    else if (r.module < 0 || r.module > 2)
+      st = fail(DTB_ERR_CONFIG, "bad module index %d", r.module);
+    if (st != DTB_OK) {
+      delete cm;
+      return st;
+    }
+    auto& rows = cm->rows[r.module][tp_index(r.tp)];
+    const dtb_cost_model::Row pt{r.token_load, r.fwd_s, r.has_bwd ? r.bwd_s : 2.0 * r.fwd_s};
+    auto it = std::lower_bound(rows.begin(), rows.end(), r.token_load,
+                               [](const dtb_cost_model::Row& p, double v) { return p.load < v; });
+    if (it != rows.end() && it->load == r.token_load) *it = pt;
+    else rows.insert(it, pt);
+    cm->nonempty[r.module] = true;
+  }
+  // flatten + upload
+  std::vector<double> flat;
+  DevCM& d = cm->dev;
+  int off = 0;
+  for (int u = 0; u < 3; ++u)
+    for (int t = 0; t < 4; ++t) {
+      d.off[u][t] = off;
+      d.cnt[u][t] = static_cast<int>(cm->rows[u][t].size());
+      off += d.cnt[u][t];
+    }
+  flat.resize(3 * static_cast<size_t>(off > 0 ? off : 1));
+  for (int u = 0; u < 3; ++u)
+    for (int t = 0; t < 4; ++t)
+      for (size_t k = 0; k < cm->rows[u][t].size(); ++k) {
+        const auto& r = cm->rows[u][t][k];
+        flat[d.off[u][t] + k] = r.load;
+        flat[off + d.off[u][t] + k] = r.fwd;
+        flat[2 * off + d.off[u][t] + k] = r.bwd;
+      }
+  cudaError_t e = cudaMalloc(&cm->d_rows, sizeof(double) * flat.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(cm->d_rows, flat.data(), sizeof(double) * flat.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    delete cm;
+    return fail(DTB_ERR_CUDA, "cost model upload: %s", cudaGetErrorString(e));
+  }
+  d.load = cm->d_rows;
+  d.fwd = cm->d_rows + off;
+  d.bwd = cm->d_rows + 2 * off;
+  for (int u = 0; u < 3; ++u) {
+    d.nonempty[u] = cm->nonempty[u] ? 1 : 0;
+    d.param_count[u] = param_count(model->unit[u].arch);
+    d.hidden[u] = static_cast<double>(model->unit[u].arch.hidden);
+    d.bwd_factor[u] = model->unit[u].frozen ? model->frozen_backward_factor : 1.0;
+    d.mem_pg[u] = model->unit[u].mem.param_grad_bytes;
+    d.mem_opt[u] = model->unit[u].mem.optimizer_bytes;
+    d.mem_act[u] = model->unit[u].mem.activation_bytes_per_mb;
+  }
+  d.analytic_ok = (cm->eff > 0.0 && cluster->peak_flops > 0.0) ? 1 : 0;
+  d.analytic_denom = cluster->peak_flops * cm->eff;
+  d.analytic_ratio = cm->ratio;
+  d.seq_len = static_cast<double>(model->seq_len);
+  d.dp_sync = model->dp_sync_seconds;
+  d.cluster = *cluster;
+  *out = cm;
+  return DTB_OK;
+}
+
+dtb_status dtb_cost_model_destroy(dtb_cost_model* cm) {
+  if (!cm) return DTB_OK;
+  cudaFree(cm->d_rows);
+  delete cm;
+  return DTB_OK;
+}
+
+dtb_status dtb_cost_sizes(dtb_context* ctx, const dtb_samples* s, int64_t* out) {
+  TRY(set_device(ctx));
+  if (s->n == 0) return DTB_OK;
+  DevSamples d;
+  TRY(upload_samples(s, ctx->stream, &d));
+  DBuf o;
+  CU(o.alloc(sizeof(long long) * s->n, ctx->stream));
+  CU(launch_cost_sizes(d.img_off, d.img_tok, d.aud_off, d.aud_tok, s->n, o.as<long long>(),
+                       ctx->stream));
+  TRY(download(reinterpret_cast<long long*>(out), o, s->n, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DTB_OK;
+}
+
+dtb_status dtb_unit_times(dtb_context* ctx, const dtb_cost_model* cm, int32_t module, int32_t tp,
+                          int64_t n, const double* loads, double* fwd, double* bwd) {
+  TRY(set_device(ctx));
+  if (module < 0 || module > 2) return fail(DTB_ERR_INVALID_ARGUMENT, "bad module");
+  if (n == 0) return DTB_OK;
+  TRY(reset_err(ctx));
+  DBuf dl, df, db;
+  TRY(upload(dl, loads, n, ctx->stream));
+  CU(df.alloc(8 * n, ctx->stream));
+  CU(db.alloc(8 * n, ctx->stream));
+  // one query stream per output, in the reference's order for element 0
+  if (fwd) TRY(check_fwd_query(cm, module, tp));
+  if (bwd && !fwd) TRY(check_bwd_query(cm, module, tp));
+  if (fwd && bwd) TRY(check_bwd_query(cm, module, tp));
+  CU(launch_unit_times(cm->dev, module, tp, n, dl.as<double>(), fwd ? df.as<double>() : nullptr,
+                       bwd ? db.as<double>() : nullptr, ctx->err, ctx->stream));
+  TRY(download(fwd, df, n, ctx->stream));
+  TRY(download(bwd, db, n, ctx->stream));
+  return sync_and_check(ctx);
+}
+
+dtb_status dtb_memory_check(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan* plan,
+                            dtb_memory_report* out) {
+  TRY(set_device(ctx));
+  DBuf o;
+  CU(o.alloc(sizeof(dtb_memory_report), ctx->stream));
+  CU(launch_memory_check(cm->dev, *plan, o.as<dtb_memory_report>(), ctx->stream));
+  TRY(download(out, o, 1, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DTB_OK;
+}
+
+static dtb_status upload_mbs(const dtb_microbatches* m, cudaStream_t s, DBuf& e, DBuf& g,
+                             DBuf& c) {
+  TRY(upload(e, m->encoder_tokens, m->n, s));
+  TRY(upload(g, m->generator_tokens, m->n, s));
+  TRY(upload(c, m->sample_count, m->n, s));
+  return DTB_OK;
+}
+
+dtb_status dtb_build_stage_times(dtb_context* ctx, const dtb_cost_model* cm,
+                                 const dtb_plan* plan, const dtb_microbatches* mbs, double* fwd,
+                                 double* bwd) {
+  TRY(set_device(ctx));
+  if (mbs->n == 0) return DTB_OK;
+  TRY(check_stage_queries(cm, *plan));
+  TRY(reset_err(ctx));
+  const int p = plan_stages(*plan);
+  DBuf e, g, c, f, b;
+  TRY(upload_mbs(mbs, ctx->stream, e, g, c));
+  CU(f.alloc(8ull * mbs->n * p, ctx->stream));
+  CU(b.alloc(8ull * mbs->n * p, ctx->stream));
+  CU(launch_stage_times(cm->dev, *plan, mbs->n, e.as<long long>(), g.as<long long>(),
+                        c.as<int>(), f.as<double>(), b.as<double>(), ctx->err, ctx->stream));
+  TRY(download(fwd, f, mbs->n * p, ctx->stream));
+  TRY(download(bwd, b, mbs->n * p, ctx->stream));
+  return sync_and_check(ctx);
+}
+
+dtb_status dtb_microbatch_fwd_keys(dtb_context* ctx, const dtb_cost_model* cm,
+                                   const dtb_plan* plan, const dtb_microbatches* mbs,
+                                   double* keys) {
+  TRY(set_device(ctx));
+  if (mbs->n == 0) return DTB_OK;
+  TRY(check_key_queries(cm, *plan));
+  TRY(reset_err(ctx));
+  DBuf e, g, c, k;
+  TRY(upload_mbs(mbs, ctx->stream, e, g, c));
+  CU(k.alloc(8ull * mbs->n, ctx->stream));
+  CU(launch_fwd_keys(cm->dev, *plan, mbs->n, e.as<long long>(), g.as<long long>(), c.as<int>(),
+                     k.as<double>(), ctx->err, ctx->stream));
+  TRY(download(keys, k, mbs->n, ctx->stream));
+  return sync_and_check(ctx);
+}
+
+dtb_status dtb_compute_stats(dtb_context* ctx, const dtb_samples* s, int64_t seq_len,
+                             dtb_workload_stats* out) {
+  TRY(set_device(ctx));
+  out->seq_len = seq_len;
+  DevSamples d;
+  if (s->n > 0) TRY(upload_samples(s, ctx->stream, &d));
+  DBuf o;
+  CU(o.alloc(64, ctx->stream));
+  CU(launch_compute_stats(d.img_off, d.img_tok, d.aud_off, d.aud_tok, s->n, o.as<double>(),
+                          ctx->stream));
+  double r[2];
+  TRY(download(r, o, 2, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  out->mean_encoder_tokens = r[0];
+  out->mean_generator_tokens = r[1];
+  return DTB_OK;
+}
+
+// ------------------------------------------------------------------- intra
+dtb_status dtb_intra_partition(dtb_context* ctx, const double* sizes, int64_t n, int32_t m,
+                               int32_t order, int32_t equal_counts, int32_t* flat_out,
+                               int64_t* offsets_out) {
+  TRY(set_device(ctx));
+  if (m < 1) return fail(DTB_ERR_INTERNAL, "group count must be >= 1");
+  if (n == 0) return fail(DTB_ERR_INTERNAL, "cannot reorder an empty batch");
+  if (m > intra_generic_max_m())
+    return fail(DTB_ERR_INVALID_ARGUMENT, "group count %d exceeds the kernel limit %d", m,
+                intra_generic_max_m());
+  if (n >= (1LL << 31)) return fail(DTB_ERR_INVALID_ARGUMENT, "n exceeds 2^31");
+  DBuf ds, scratch, flat, offs;
+  TRY(upload(ds, sizes, n, ctx->stream));
+  const size_t sb = intra_generic_scratch(static_cast<int>(n), m);
+  CU(scratch.alloc(sb, ctx->stream));
+  CU(flat.alloc(4ull * n, ctx->stream));
+  CU(offs.alloc(8ull * (m + 1), ctx->stream));
+  CU(launch_intra_generic(ds.as<double>(), static_cast<int>(n), m, order, equal_counts,
+                          scratch.p, sb, flat.as<int>(), offs.as<long long>(), ctx->stream));
+  TRY(download(flat_out, flat, n, ctx->stream));
+  TRY(download(reinterpret_cast<long long*>(offsets_out), offs, m + 1, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DTB_OK;
+}
+
+dtb_status dtb_block_group_loads(dtb_context* ctx, const double* sizes, const int32_t* order,
+                                 int64_t n, int32_t m, double* loads) {
+  TRY(set_device(ctx));
+  if (m < 1) return fail(DTB_ERR_INTERNAL, "group count must be >= 1");
+  if (n > 0 && n / m == 0) return fail(DTB_ERR_INTERNAL, "fewer samples than groups");
+  DBuf ds, dord, dl;
+  // sizes is indexed by order entries: upload the span that covers them
+  int32_t max_idx = -1;
+  for (int64_t i = 0; i < n; ++i) max_idx = std::max(max_idx, order[i]);
+  TRY(upload(ds, sizes, static_cast<size_t>(max_idx + 1), ctx->stream));
+  TRY(upload(dord, order, n, ctx->stream));
+  CU(dl.alloc(8ull * m, ctx->stream));
+  if (n == 0) CU(cudaMemsetAsync(dl.p, 0, 8ull * m, ctx->stream));
+  else CU(launch_block_loads(ds.as<double>(), dord.as<int>(), static_cast<int>(n), m,
+                             dl.as<double>(), ctx->stream));
+  TRY(download(loads, dl, m, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DTB_OK;
+}
+
+static dtb_status select_common(dtb_context* ctx, const double* keys, int64_t n_keys,
+                                const int32_t* pending, int64_t np, int32_t k, int closest,
+                                double target, int32_t* out) {
+  TRY(set_device(ctx));
+  if (k < 0 || k > np)
+    return fail(DTB_ERR_K_TOO_LARGE, "%s asked for %d of %lld",
+                closest ? "select_closest" : "select_min", k, static_cast<long long>(np));
+  if (k == 0) return DTB_OK;
+  DBuf dk, dp, dout;
+  TRY(upload(dk, keys, n_keys, ctx->stream));
+  TRY(upload(dp, pending, np, ctx->stream));
+  CU(dout.alloc(4ull * (k + 1) + np + 16, ctx->stream));
+  CU(launch_select(dk.as<double>(), dp.as<int>(), static_cast<int>(np), k, closest, target,
+                   dout.as<int>(), ctx->stream));
+  TRY(download(out, dout, k, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DTB_OK;
+}
+
+dtb_status dtb_select_min(dtb_context* ctx, const double* keys, int64_t n_keys,
+                          const int32_t* pending, int64_t n_pending, int32_t k, int32_t* out) {
+  return select_common(ctx, keys, n_keys, pending, n_pending, k, 0, 0.0, out);
+}
+
+dtb_status dtb_select_closest(dtb_context* ctx, const double* keys, int64_t n_keys,
+                              const int32_t* pending, int64_t n_pending, int32_t k,
+                              double target, int32_t* out) {
+  return select_common(ctx, keys, n_keys, pending, n_pending, k, 1, target, out);
+}
+
+// --------------------------------------------------------------- simulator
+dtb_status dtb_schedule(dtb_context* ctx, const double* fwd, const double* bwd, int32_t l,
+                        int32_t p, int32_t vpp, int32_t* ev_device, int32_t* ev_mb,
+                        int32_t* ev_stage, int32_t* ev_phase, double* ev_start, double* ev_end,
+                        double* iteration_time, double* device_busy) {
+  TRY(set_device(ctx));
+  // schedule_interleaved: check_times first (in-kernel for values), vpp rules
+  if (l < 1) return fail(DTB_ERR_INTERNAL, "bad stage times: microbatch count must be >= 1");
+  if (p < 1) return fail(DTB_ERR_INTERNAL, "bad stage times: stage count must be >= 1");
+  TRY(reset_err(ctx));
+  const size_t cells = static_cast<size_t>(l) * p;
+  DBuf df, db;
+  TRY(upload(df, fwd, cells, ctx->stream));
+  TRY(upload(db, bwd, cells, ctx->stream));
+  // values are validated before the vpp rules, as check_times runs first
+  CU(launch_check_times(df.as<double>(), db.as<double>(), static_cast<long long>(cells), ctx->err,
+                        ctx->stream));
+  TRY(sync_and_check(ctx));
+  TRY(check_vpp(l, p, vpp));
+  const int devices = p / vpp;
+  const size_t ne = 2 * cells;
+  DBuf dev, mb, st, ph, s, e, busy, it, scr, sort_scr;
+  CU(dev.alloc(4 * ne, ctx->stream));
+  CU(mb.alloc(4 * ne, ctx->stream));
+  CU(st.alloc(4 * ne, ctx->stream));
+  CU(ph.alloc(4 * ne, ctx->stream));
+  CU(s.alloc(8 * ne, ctx->stream));
+  CU(e.alloc(8 * ne, ctx->stream));
+  CU(busy.alloc(8ull * devices, ctx->stream));
+  CU(it.alloc(8, ctx->stream));
+  CU(scr.alloc(8 * (2 * cells + 4 * static_cast<size_t>(p) + 8), ctx->stream));
+  CU(launch_schedule_events(df.as<double>(), db.as<double>(), l, p, vpp, dev.as<int>(),
+                            mb.as<int>(), st.as<int>(), ph.as<int>(), s.as<double>(),
+                            e.as<double>(), busy.as<double>(), it.as<double>(), scr.p, ctx->err,
+                            ctx->stream));
+  const size_t sbytes = sort_events_scratch(static_cast<int>(ne));
+  CU(sort_scr.alloc(sbytes, ctx->stream));
+  CU(launch_sort_events(static_cast<int>(ne), dev.as<int>(), mb.as<int>(), st.as<int>(),
+                        ph.as<int>(), s.as<double>(), e.as<double>(), sort_scr.p, sbytes,
+                        ctx->stream));
+  TRY(download(ev_device, dev, ne, ctx->stream));
+  TRY(download(ev_mb, mb, ne, ctx->stream));
+  TRY(download(ev_stage, st, ne, ctx->stream));
+  TRY(download(ev_phase, ph, ne, ctx->stream));
+  TRY(download(ev_start, s, ne, ctx->stream));
+  TRY(download(ev_end, e, ne, ctx->stream));
+  TRY(download(device_busy, busy, devices, ctx->stream));
+  TRY(download(iteration_time, it, 1, ctx->stream));
+  return sync_and_check(ctx);
+}
+
+dtb_status dtb_get_intervals(dtb_context* ctx, int64_t n, const int32_t* dev,
+                             const int32_t* mb, const int32_t* stage, const int32_t* phase,
+                             const double* start, const double* end, int64_t* n_intervals,
+                             double* starts, double* ends, int64_t* fill_offsets,
+                             int32_t* fill_mb) {
+  TRY(set_device(ctx));
+  (void)stage;
+  DBuf dd, dm, dp, ds, de, ni, os, oe, fo, fm;
+  TRY(upload(dd, dev, n, ctx->stream));
+  TRY(upload(dm, mb, n, ctx->stream));
+  TRY(upload(dp, phase, n, ctx->stream));
+  TRY(upload(ds, start, n, ctx->stream));
+  TRY(upload(de, end, n, ctx->stream));
+  CU(ni.alloc(8, ctx->stream));
+  CU(os.alloc(8 * (n + 1), ctx->stream));
+  CU(oe.alloc(8 * (n + 1), ctx->stream));
+  CU(fo.alloc(8 * (n + 2), ctx->stream));
+  CU(fm.alloc(4 * (n + 1), ctx->stream));
+  CU(launch_get_intervals(n, dd.as<int>(), dm.as<int>(), dp.as<int>(), ds.as<double>(),
+                          de.as<double>(), ni.as<long long>(), os.as<double>(), oe.as<double>(),
+                          fo.as<long long>(), fm.as<int>(), ctx->stream));
+  long long k = 0;
+  TRY(download(&k, ni, 1, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *n_intervals = k;
+  TRY(download(starts, os, k, ctx->stream));
+  TRY(download(ends, oe, k, ctx->stream));
+  TRY(download(reinterpret_cast<long long*>(fill_offsets), fo, k + 1, ctx->stream));
+  long long nf = 0;
+  CU(cudaMemcpyAsync(&nf, fo.as<long long>() + k, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  TRY(download(fill_mb, fm, nf, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DTB_OK;
+}
+
+dtb_status dtb_interval_windows(dtb_context* ctx, const double* fwd, const double* bwd,
+                                int32_t l, int32_t p, double* volumes) {
+  TRY(set_device(ctx));
+  const size_t cells = static_cast<size_t>(l) * p;
+  const size_t ne = 2 * cells;
+  std::vector<int32_t> dev(ne), mb(ne), st(ne), ph(ne);
+  std::vector<double> s(ne), e(ne), busy(p > 0 ? p : 1);
+  double it;
+  TRY(dtb_schedule(ctx, fwd, bwd, l, p, 1, dev.data(), mb.data(), st.data(), ph.data(),
+                   s.data(), e.data(), &it, busy.data()));
+  std::vector<double> a(ne + 1), b(ne + 1);
+  std::vector<int64_t> fo(ne + 2);
+  std::vector<int32_t> fm(ne + 1);
+  int64_t k = 0;
+  TRY(dtb_get_intervals(ctx, static_cast<int64_t>(ne), dev.data(), mb.data(), st.data(),
+                        ph.data(), s.data(), e.data(), &k, a.data(), b.data(), fo.data(),
+                        fm.data()));
+  for (int64_t i = 0; i < k; ++i) volumes[i] = b[i] - a[i];  // Interval::volume
+  return DTB_OK;
+}
+
+dtb_status dtb_schedule_batch_dev(dtb_context* ctx, int64_t batch, const double* fwd,
+                                  const double* bwd, int32_t l, int32_t p, int32_t vpp,
+                                  double* iteration_time, double* device_busy, void* stream) {
+  TRY(set_device(ctx));
+  TRY(check_vpp(l, p, vpp));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TRY(reset_err(ctx));
+  CU(cudaStreamSynchronize(ctx->stream));
+  DBuf scr;
+  CU(scr.alloc(schedule_batch_scratch(batch, l, p, vpp), s));
+  CU(launch_schedule_batch(batch, fwd, bwd, l, p, vpp, iteration_time, device_busy, scr.p,
+                           ctx->err, s));
+  return DTB_OK;
+}
+
+dtb_status dtb_schedule_batch(dtb_context* ctx, int64_t batch, const double* fwd,
+                              const double* bwd, int32_t l, int32_t p, int32_t vpp,
+                              double* iteration_time, double* device_busy) {
+  TRY(set_device(ctx));
+  TRY(check_vpp(l, p, vpp));
+  const size_t cells = static_cast<size_t>(batch) * l * p;
+  DBuf df, db, it, busy;
+  TRY(upload(df, fwd, cells, ctx->stream));
+  TRY(upload(db, bwd, cells, ctx->stream));
+  CU(it.alloc(8ull * batch, ctx->stream));
+  CU(busy.alloc(8ull * batch * (p / vpp), ctx->stream));
+  TRY(reset_err(ctx));
+  DBuf scr;
+  CU(scr.alloc(schedule_batch_scratch(batch, l, p, vpp), ctx->stream));
+  CU(launch_schedule_batch(batch, df.as<double>(), db.as<double>(), l, p, vpp, it.as<double>(),
+                           device_busy ? busy.as<double>() : nullptr, scr.p, ctx->err,
+                           ctx->stream));
+  TRY(download(iteration_time, it, batch, ctx->stream));
+  TRY(download(device_busy, busy, batch * (p / vpp), ctx->stream));
+  return sync_and_check(ctx);
+}
+
+dtb_status dtb_simulate_iteration(dtb_context* ctx, const dtb_cost_model* cm,
+                                  const dtb_plan* plan, int32_t n_groups,
+                                  const int64_t* group_offsets, const dtb_microbatches* mbs,
+                                  double* t_iter, double* group_times, int32_t* slowest_group,
+                                  double* slowest_group_time, double* mean_bubble) {
+  TRY(set_device(ctx));
+  if (n_groups <= 0) return fail(DTB_ERR_INTERNAL, "no microbatch groups to simulate");
+  const int p = plan_stages(*plan);
+  // groups may have different sizes: one launch per distinct size run
+  std::vector<double> tg(n_groups), bub(n_groups);
+  DBuf e, g, c;
+  TRY(upload_mbs(mbs, ctx->stream, e, g, c));
+  for (int32_t gi = 0; gi < n_groups; ++gi) {
+    const long long l = group_offsets[gi + 1] - group_offsets[gi];
+    if (l > 0) TRY(check_stage_queries(cm, *plan));
+    TRY(check_vpp(static_cast<int>(l), p, plan->vpp));
+    TRY(reset_err(ctx));
+    GroupSimArgs a{};
+    a.cm = cm->dev;
+    a.plan = *plan;
+    a.n_batches = 1;
+    a.groups = 1;
+    a.l = static_cast<int>(l);
+    a.enc = e.as<long long>() + group_offsets[gi];
+    a.gen = g.as<long long>() + group_offsets[gi];
+    a.count = c.as<int>() + group_offsets[gi];
+    a.span = 1;
+    DBuf tgd, bd, scr;
+    CU(tgd.alloc(8, ctx->stream));
+    CU(bd.alloc(8, ctx->stream));
+    a.t_group = tgd.as<double>();
+    a.busy = bd.as<double>();
+    a.err = ctx->err;
+    CU(scr.alloc(group_sims_scratch(a), ctx->stream));
+    CU(launch_group_sims(a, scr.p, ctx->stream));
+    TRY(download(&tg[gi], tgd, 1, ctx->stream));
+    TRY(download(&bub[gi], bd, 1, ctx->stream));
+    TRY(sync_and_check(ctx));
+  }
+  // simulate.cpp:31-46 fold (sequential over groups, as the reference)
+  double bubble_sum = 0.0, worst = 0.0;
+  int worst_g = 0;
+  for (int32_t gi = 0; gi < n_groups; ++gi) {
+    bubble_sum += bub[gi];
+    if (tg[gi] > worst) {
+      worst = tg[gi];
+      worst_g = gi;
+    }
+  }
+  if (group_times) std::copy(tg.begin(), tg.end(), group_times);
+  if (slowest_group) *slowest_group = worst_g;
+  if (slowest_group_time) *slowest_group_time = worst;
+  if (mean_bubble) *mean_bubble = bubble_sum / static_cast<double>(n_groups);
+  if (t_iter) *t_iter = worst + cm->model.dp_sync_seconds;
+  return DTB_OK;
+}
+
+// ------------------------------------------------------------------- inter
+static dtb_status inter_checks(int32_t l, int32_t p, int32_t vpp) {
+  if (l <= 1) return DTB_OK;
+  if (vpp < 1) return fail(DTB_ERR_INDIVISIBLE_VPP, "vpp must be >= 1");
+  if (p % vpp != 0) return fail(DTB_ERR_INDIVISIBLE_VPP, "stage count not divisible by vpp");
+  const int devices = p / vpp;
+  if (devices == 1) return DTB_OK;
+  const int pending = l - 1 - std::min(devices - 1, l - 1);
+  if (pending > 0 && vpp > 1 && l % devices != 0)
+    return fail(DTB_ERR_INDIVISIBLE_VPP,
+                "microbatch count %d is not divisible by the device count %d", l, devices);
+  return DTB_OK;
+}
+
+dtb_status dtb_inter_reorder_batch_dev(dtb_context* ctx, int64_t batch, const double* fwd,
+                                       const double* bwd, int32_t l, int32_t p,
+                                       const double* keys, int32_t vpp, int32_t* orders,
+                                       void* stream) {
+  TRY(set_device(ctx));
+  TRY(inter_checks(l, p, vpp));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  InterArgs a{};
+  a.batch = batch;
+  a.l = l;
+  a.p = p;
+  a.vpp = vpp;
+  a.fwd = fwd;
+  a.bwd = bwd;
+  a.keys = keys;
+  a.orders = orders;
+  a.err = ctx->err;
+  const size_t bytes = inter_scratch(a);
+  DBuf scr;
+  CU(scr.alloc(bytes, s));
+  CU(launch_inter(a, scr.p, bytes, s));
+  return DTB_OK;
+}
+
+dtb_status dtb_inter_reorder_batch(dtb_context* ctx, int64_t batch, const double* fwd,
+                                   const double* bwd, int32_t l, int32_t p, const double* keys,
+                                   int32_t vpp, int32_t* orders) {
+  TRY(set_device(ctx));
+  TRY(inter_checks(l, p, vpp));
+  if (batch == 0 || l == 0) return DTB_OK;
+  const size_t cells = static_cast<size_t>(batch) * l * p;
+  DBuf df, db, dk, dord;
+  TRY(upload(df, fwd, cells, ctx->stream));
+  TRY(upload(db, bwd, cells, ctx->stream));
+  TRY(upload(dk, keys, static_cast<size_t>(batch) * l, ctx->stream));
+  CU(dord.alloc(4ull * batch * l, ctx->stream));
+  TRY(reset_err(ctx));
+  TRY(dtb_inter_reorder_batch_dev(ctx, batch, df.as<double>(), db.as<double>(), l, p,
+                                  dk.as<double>(), vpp, dord.as<int>(), ctx->stream));
+  TRY(download(orders, dord, static_cast<size_t>(batch) * l, ctx->stream));
+  return sync_and_check(ctx);
+}
+
+dtb_status dtb_inter_reorder(dtb_context* ctx, const double* fwd, const double* bwd, int32_t l,
+                             int32_t p, const double* keys, int32_t vpp, int32_t* order_out) {
+  if (l <= 1) {
+    for (int i = 0; i < l; ++i) order_out[i] = i;
+    return DTB_OK;
+  }
+  return dtb_inter_reorder_batch(ctx, 1, fwd, bwd, l, p, keys, vpp, order_out);
+}
+
+// --------------------------------------------------------- disaggregated
+static dtb_status stream_checks(const dtb_cost_model* cm, const dtb_plan* plan,
+                                const dtb_reorder_mode* mode, long long n_total,
+                                long long n_batches) {
+  const long long bs = plan->global_batch;
+  if (n_batches < 1 || n_total != n_batches * bs) {
+    if (n_batches == 1)
+      return fail(DTB_ERR_BATCH_SIZE_MISMATCH, "batch has %lld samples, plan expects %lld",
+                  n_total, bs);
+    return fail(DTB_ERR_BATCH_SIZE_MISMATCH,
+                "stream has %lld samples, plan expects %lld batches of %lld", n_total, n_batches,
+                bs);
+  }
+  const int dp_lm = plan->unit[DTB_BACKBONE].dp;
+  const int dp_me = plan->unit[DTB_ENCODER].dp;
+  if (mode->intra && dp_lm < 1) return fail(DTB_ERR_INTERNAL, "group count must be >= 1");
+  if (bs == 0) return fail(DTB_ERR_INTERNAL, "cannot reorder an empty batch");
+  if (dp_lm < 1 || dp_me < 1 || plan->unit[DTB_GENERATOR].dp < 1)
+    return fail(DTB_ERR_INTERNAL, "parallel sizes must be >= 1");
+  if (bs / dp_lm == 0) return fail(DTB_ERR_INTERNAL, "fewer samples than groups");
+  if (bs > fused_max_n() || dp_lm > fused_max_m())
+    return fail(DTB_ERR_INVALID_ARGUMENT,
+                "global batch %lld / dp %d beyond the fused kernel's limits (%d / %d)", bs, dp_lm,
+                fused_max_n(), fused_max_m());
+  // simulate_iteration(identity) is the first cost-model consumer
+  TRY(check_stage_queries(cm, *plan));
+  const int per_group = static_cast<int>(bs / dp_lm);
+  TRY(check_vpp(per_group, plan_stages(*plan), plan->vpp));
+  if (mode->inter) TRY(inter_checks(per_group, plan_stages(*plan), plan->vpp));
+  return DTB_OK;
+}
+
+// Device pipeline for n_batches global batches (all pointers device).
+static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan* plan,
+                             const dtb_reorder_mode* mode, const int* io, const int* it,
+                             const int* ao, const int* at, long long n_batches, int* order_out,
+                             double* lb, double* la, double* tb, double* ta, unsigned char* kept,
+                             cudaStream_t s) {
+  const int n = static_cast<int>(plan->global_batch);
+  const int dp_lm = plan->unit[DTB_BACKBONE].dp;
+  const int dp_me = plan->unit[DTB_ENCODER].dp;
+  const int per_group = n / dp_lm;
+  const int span = dp_lm / dp_me;
+  const long long n_mb = n_batches * dp_me * static_cast<long long>(per_group);
+  const long long total = n_batches * static_cast<long long>(n);
+  DBuf intra, orig_tok, staged_tok, enc0, enc1, tgrp, inter, scr, bub;
+  CU(intra.alloc(4ull * total, s));
+  CU(orig_tok.alloc(4ull * total, s));
+  CU(staged_tok.alloc(4ull * total, s));
+  FusedArgs fa{};
+  fa.n = n;
+  fa.m = dp_lm;
+  fa.order = mode->sort_order;
+  fa.intra = mode->intra;
+  fa.img_off = io;
+  fa.img_tok = it;
+  fa.aud_off = ao;
+  fa.aud_tok = at;
+  fa.order_out = intra.as<int>();
+  fa.load_before = lb;
+  fa.load_after = la;
+  fa.kept = kept;
+  fa.orig_tok = orig_tok.as<int>();
+  fa.staged_tok = staged_tok.as<int>();
+  fa.err = ctx->err;
+  CU(launch_intra_fused(fa, n_batches, s));
+  // microbatch token sums of the identity and the intra-ordered assembly
+  CU(enc0.alloc(8ull * n_mb, s));
+  CU(enc1.alloc(8ull * n_mb, s));
+  CU(launch_assemble(n_batches, n, dp_lm, dp_me, orig_tok.as<int>(), enc0.as<long long>(), s));
+  CU(launch_assemble(n_batches, n, dp_lm, dp_me, staged_tok.as<int>(), enc1.as<long long>(), s));
+  GroupSimArgs ga{};
+  ga.cm = cm->dev;
+  ga.plan = *plan;
+  ga.n_batches = n_batches;
+  ga.groups = dp_me;
+  ga.l = per_group;
+  ga.enc = enc0.as<long long>();
+  ga.gen = nullptr;
+  ga.count = nullptr;
+  ga.span = span;
+  CU(tgrp.alloc(8ull * n_batches * dp_me, s));
+  CU(bub.alloc(8ull * n_batches * dp_me, s));
+  ga.t_group = tgrp.as<double>();
+  ga.busy = nullptr;
+  ga.err = ctx->err;
+  const size_t sim_bytes = group_sims_scratch(ga);
+  InterArgs ia{};
+  ia.batch = n_batches * dp_me;
+  ia.l = per_group;
+  ia.p = plan_stages(*plan);
+  ia.vpp = plan->vpp;
+  ia.cm = cm->dev;
+  ia.plan = *plan;
+  ia.enc = enc1.as<long long>();
+  ia.gen = nullptr;
+  ia.span = span;
+  ia.err = ctx->err;
+  const size_t inter_bytes = mode->inter ? inter_scratch(ia) : 0;
+  CU(scr.alloc(std::max(sim_bytes, inter_bytes), s));
+  CU(launch_group_sims(ga, scr.p, s));
+  CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, tb, s));
+  if (mode->inter) {
+    CU(inter.alloc(4ull * n_mb, s));
+    ia.orders = inter.as<int>();
+    CU(launch_inter(ia, scr.p, inter_bytes, s));
+  }
+  CU(launch_compose(n_batches, n, dp_lm, dp_me, intra.as<int>(),
+                    mode->inter ? inter.as<int>() : nullptr, order_out, s));
+  ga.enc = enc1.as<long long>();
+  ga.order = mode->inter ? inter.as<int>() : nullptr;
+  CU(launch_group_sims(ga, scr.p, s));
+  CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, ta, s));
+  return DTB_OK;
+}
+
+dtb_status dtb_reorder_stream_dev(dtb_context* ctx, const dtb_cost_model* cm,
+                                  const dtb_plan* plan, const dtb_reorder_mode* mode,
+                                  const dtb_samples* samples, int64_t n_batches,
+                                  int32_t* output_order, double* load_before, double* load_after,
+                                  double* t_iter_before, double* t_iter_after,
+                                  uint8_t* greedy_kept, void* stream) {
+  TRY(set_device(ctx));
+  const dtb_reorder_mode def{1, 1, DTB_ASCENDING};
+  const dtb_reorder_mode* md = mode ? mode : &def;
+  TRY(stream_checks(cm, plan, md, samples->n, n_batches));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return run_stream(ctx, cm, plan, md, samples->image_offsets, samples->image_tokens,
+                    samples->audio_offsets, samples->audio_tokens, n_batches, output_order,
+                    load_before, load_after, t_iter_before, t_iter_after, greedy_kept, s);
+}
+
+dtb_status dtb_reorder_stream(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan* plan,
+                              const dtb_reorder_mode* mode, const dtb_samples* samples,
+                              int64_t n_batches, int32_t* output_order, double* load_before,
+                              double* load_after, double* t_iter_before, double* t_iter_after,
+                              uint8_t* greedy_kept) {
+  TRY(set_device(ctx));
+  const dtb_reorder_mode def{1, 1, DTB_ASCENDING};
+  const dtb_reorder_mode* md = mode ? mode : &def;
+  TRY(stream_checks(cm, plan, md, samples->n, n_batches));
+  cudaStream_t s = ctx->stream;
+  TRY(reset_err(ctx));
+  DevSamples d;
+  TRY(upload_samples(samples, s, &d));
+  const long long total = samples->n;
+  const int dp = plan->unit[DTB_BACKBONE].dp;
+  DBuf o, lb, la, tb, ta, kp;
+  CU(o.alloc(4ull * total, s));
+  CU(lb.alloc(8ull * n_batches * dp, s));
+  CU(la.alloc(8ull * n_batches * dp, s));
+  CU(tb.alloc(8ull * n_batches, s));
+  CU(ta.alloc(8ull * n_batches, s));
+  CU(kp.alloc(n_batches, s));
+  TRY(run_stream(ctx, cm, plan, md, d.img_off, d.img_tok, d.aud_off, d.aud_tok, n_batches,
+                 o.as<int>(), lb.as<double>(), la.as<double>(), tb.as<double>(), ta.as<double>(),
+                 kp.as<unsigned char>(), s));
+  TRY(download(output_order, o, total, s));
+  TRY(download(load_before, lb, n_batches * dp, s));
+  TRY(download(load_after, la, n_batches * dp, s));
+  TRY(download(t_iter_before, tb, n_batches, s));
+  TRY(download(t_iter_after, ta, n_batches, s));
+  TRY(download(greedy_kept, kp, n_batches, s));
+  return sync_and_check(ctx);
+}
+
+dtb_status dtb_intra_stream_dev(dtb_context* ctx, int64_t bs, int32_t dp_lm, int32_t sort_order,
+                                const dtb_samples* samples, int64_t n_batches, int32_t* order_out,
+                                double* load_before, double* load_after, uint8_t* greedy_kept,
+                                void* stream) {
+  TRY(set_device(ctx));
+  if (dp_lm < 1) return fail(DTB_ERR_INTERNAL, "group count must be >= 1");
+  if (bs < 1) return fail(DTB_ERR_INTERNAL, "cannot reorder an empty batch");
+  if (samples->n != n_batches * bs)
+    return fail(DTB_ERR_BATCH_SIZE_MISMATCH, "stream has %lld samples, expected %lld",
+                static_cast<long long>(samples->n), static_cast<long long>(n_batches * bs));
+  if (bs / dp_lm == 0) return fail(DTB_ERR_INTERNAL, "fewer samples than groups");
+  if (bs > fused_max_n() || dp_lm > fused_max_m())
+    return fail(DTB_ERR_INVALID_ARGUMENT, "global batch / dp beyond the fused kernel's limits");
+  FusedArgs fa{};
+  fa.n = static_cast<int>(bs);
+  fa.m = dp_lm;
+  fa.order = sort_order;
+  fa.intra = 1;
+  fa.img_off = samples->image_offsets;
+  fa.img_tok = samples->image_tokens;
+  fa.aud_off = samples->audio_offsets;
+  fa.aud_tok = samples->audio_tokens;
+  fa.order_out = order_out;
+  fa.load_before = load_before;
+  fa.load_after = load_after;
+  fa.kept = greedy_kept;
+  fa.err = ctx->err;
+  CU(launch_intra_fused(fa, n_batches, static_cast<cudaStream_t>(stream)));
+  return DTB_OK;
+}
+
+dtb_status dtb_disaggregated_reorder(dtb_context* ctx, const dtb_cost_model* cm,
+                                     const dtb_plan* plan, const dtb_reorder_mode* mode,
+                                     const dtb_samples* batch, dtb_reorder_report* r) {
+  return dtb_reorder_stream(ctx, cm, plan, mode, batch, 1, r->output_order,
+                            r->group_load_before, r->group_load_after, &r->t_iter_before,
+                            &r->t_iter_after, nullptr);
+}
+
+// ---------------------------------------------------------- orchestration
+dtb_status dtb_predict_times(dtb_context* ctx, const dtb_cost_model* cm,
+                             const dtb_workload_stats* stats, const dtb_plan* plans, int64_t n,
+                             dtb_predicted_times* out) {
+  TRY(set_device(ctx));
+  if (n == 0) return DTB_OK;
+  TRY(reset_err(ctx));
+  DBuf dp, o;
+  TRY(upload(dp, plans, n, ctx->stream));
+  CU(o.alloc(sizeof(dtb_predicted_times) * n, ctx->stream));
+  CU(launch_predict(cm->dev, *stats, dp.as<dtb_plan>(), n, o.as<dtb_predicted_times>(), ctx->err,
+                    ctx->stream));
+  TRY(download(out, o, n, ctx->stream));
+  DevErr e;
+  CU(cudaMemcpyAsync(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (e.code == -1) {
+    const long long idx = static_cast<long long>(e.ordered >> 8);
+    const int code = static_cast<int>(e.ordered & 0xff);
+    if (code == E_NO_MICROBATCH)
+      return fail(DTB_ERR_INTERNAL, "plan yields no microbatches per iteration");
+    // re-derive the unit from the plan's queries in reference order
+    for (int u = 0; u < 3; ++u) {
+      TRY(check_fwd_query(cm, u, plans[idx].unit[u].tp));
+      TRY(check_bwd_query(cm, u, plans[idx].unit[u].tp));
+    }
+    return dev_status(e);
+  }
+  return dev_status(e);
+}
+
+dtb_status dtb_enumerate_parallelism(dtb_context* ctx, const dtb_cluster_spec* cluster,
+                                     int64_t bs, int64_t* count, dtb_tuple* tuples,
+                                     int64_t capacity) {
+  TRY(set_device(ctx));
+  if (bs < 1) return fail(DTB_ERR_INVALID_ARGUMENT, "global batch must be >= 1");
+  DBuf scr, cnt, out;
+  CU(scr.alloc(enumerate_scratch(bs), ctx->stream));
+  CU(cnt.alloc(8, ctx->stream));
+  if (tuples != nullptr && capacity > 0) CU(out.alloc(sizeof(dtb_tuple) * capacity, ctx->stream));
+  CU(launch_enumerate(*cluster, bs, nullptr, 0, cnt.as<long long>(),
+                      tuples && capacity > 0 ? out.as<dtb_tuple>() : nullptr, capacity, scr.p,
+                      ctx->stream));
+  long long c = 0;
+  TRY(download(&c, cnt, 1, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *count = c;
+  if (tuples != nullptr && capacity > 0) {
+    TRY(download(tuples, out, std::min<long long>(c, capacity), ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  return DTB_OK;
+}
+
+static dtb_status orch_error(dtb_context* ctx, const dtb_cost_model* cm, const DevErr& e,
+                             const dtb_tuple* dev_tuples) {
+  if (e.code == 0) return DTB_OK;
+  if (e.code != -1) return dev_status(e);
+  const long long key = static_cast<long long>(e.ordered >> 8);
+  const long long idx = key / 3;
+  dtb_tuple t;
+  CU(cudaMemcpy(&t, dev_tuples + idx, sizeof t, cudaMemcpyDeviceToHost));
+  const int tps[3] = {t.tp_me, t.tp_lm, t.tp_mg};
+  for (int u = 0; u < 3; ++u) {
+    TRY(check_fwd_query(cm, u, tps[u]));
+    TRY(check_bwd_query(cm, u, tps[u]));
+  }
+  return dev_status(e, tps);
+}
+
+dtb_status dtb_solve_subproblem(dtb_context* ctx, const dtb_cost_model* cm,
+                                const dtb_workload_stats* stats, const dtb_tuple* tuples,
+                                int64_t n, int64_t bs, int32_t vpp, dtb_candidate* out) {
+  TRY(set_device(ctx));
+  if (n == 0) return DTB_OK;
+  TRY(reset_err(ctx));
+  DBuf dt, o, bb;
+  TRY(upload(dt, tuples, n, ctx->stream));
+  CU(o.alloc(sizeof(dtb_candidate) * n, ctx->stream));
+  const int grid = static_cast<int>(std::min<long long>((n + 127) / 128, 4096));
+  CU(bb.alloc(sizeof(dtb_candidate) * grid, ctx->stream));
+  OrchArgs a{};
+  a.cm = cm->dev;
+  a.stats = *stats;
+  a.bs = bs;
+  a.vpp = vpp;
+  a.tuples = dt.as<dtb_tuple>();
+  a.n = n;
+  a.shard_index = 0;
+  a.shard_count = 1;
+  a.out = o.as<dtb_candidate>();
+  a.block_best = bb.as<dtb_candidate>();
+  a.err = ctx->err;
+  CU(launch_orchestration(a, grid, ctx->stream));
+  TRY(download(out, o, n, ctx->stream));
+  DevErr e;
+  CU(cudaMemcpyAsync(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return orch_error(ctx, cm, e, dt.as<dtb_tuple>());
+}
+
+// Shared search driver: enumerate on device, solve the shard, reduce.
+static dtb_status search(dtb_context* ctx, const dtb_cost_model* cm,
+                         const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                         long long shard_index, long long shard_count, dtb_candidate* best_dev,
+                         long long* evaluated_dev, dtb_candidate* table_dev, cudaStream_t s,
+                         long long* n_tuples_out, DBuf& tuples) {
+  DBuf scr, cnt;
+  CU(scr.alloc(enumerate_scratch(bs), s));
+  CU(cnt.alloc(8, s));
+  CU(launch_enumerate(cm->cluster, bs, nullptr, 0, cnt.as<long long>(), nullptr, 0, scr.p, s));
+  long long n = 0;
+  CU(cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  CU(tuples.alloc(sizeof(dtb_tuple) * (n > 0 ? n : 1), s));
+  CU(launch_enumerate(cm->cluster, bs, nullptr, 0, cnt.as<long long>(), tuples.as<dtb_tuple>(),
+                      n, scr.p, s));
+  const long long mine = n > shard_index ? (n - shard_index + shard_count - 1) / shard_count : 0;
+  int grid = static_cast<int>(std::min<long long>((mine + 127) / 128, 148 * 16));
+  if (grid < 1) grid = 1;
+  DBuf bb;
+  CU(bb.alloc(sizeof(dtb_candidate) * grid, s));
+  OrchArgs a{};
+  a.cm = cm->dev;
+  a.stats = *stats;
+  a.bs = bs;
+  a.vpp = vpp;
+  a.tuples = tuples.as<dtb_tuple>();
+  a.n = n;
+  a.shard_index = shard_index;
+  a.shard_count = shard_count;
+  a.out = table_dev;
+  a.block_best = bb.as<dtb_candidate>();
+  a.err = ctx->err;
+  CU(launch_orchestration(a, grid, s));
+  CU(launch_best_reduce(bb.as<dtb_candidate>(), grid, best_dev, s));
+  if (evaluated_dev)
+    CU(cudaMemcpyAsync(evaluated_dev, &mine, 8, cudaMemcpyHostToDevice, s));
+  if (n_tuples_out) *n_tuples_out = n;
+  CU(cudaStreamSynchronize(s));  // `mine` and scratch lifetimes
+  return DTB_OK;
+}
+
+dtb_status dtb_model_orchestration(dtb_context* ctx, const dtb_cost_model* cm,
+                                   const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                                   dtb_orchestration_result* result, dtb_candidate* candidates,
+                                   int64_t capacity) {
+  TRY(set_device(ctx));
+  const auto t0 = std::chrono::steady_clock::now();
+  TRY(reset_err(ctx));
+  DBuf best, table, tuples;
+  CU(best.alloc(sizeof(dtb_candidate), ctx->stream));
+  long long n = 0;
+  // the table, when requested, needs the count first
+  if (candidates != nullptr) {
+    int64_t cnt = 0;
+    TRY(dtb_enumerate_parallelism(ctx, &cm->cluster, bs, &cnt, nullptr, 0));
+    CU(table.alloc(sizeof(dtb_candidate) * (cnt > 0 ? cnt : 1), ctx->stream));
+  }
+  TRY(search(ctx, cm, stats, bs, vpp, 0, 1, best.as<dtb_candidate>(), nullptr,
+             candidates ? table.as<dtb_candidate>() : nullptr, ctx->stream, &n, tuples));
+  DevErr e;
+  CU(cudaMemcpy(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost));
+  TRY(orch_error(ctx, cm, e, tuples.as<dtb_tuple>()));
+  dtb_candidate b;
+  CU(cudaMemcpy(&b, best.p, sizeof b, cudaMemcpyDeviceToHost));
+  if (candidates != nullptr) {
+    CU(cudaMemcpy(candidates, table.p, sizeof(dtb_candidate) * std::min<long long>(n, capacity),
+                  cudaMemcpyDeviceToHost));
+  }
+  result->candidates_evaluated = n;
+  result->solve_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (!b.feasible) return fail(DTB_ERR_INFEASIBLE, "no feasible plan for this model and cluster");
+  result->best = b.plan;
+  result->times = b.times;
+  return DTB_OK;
+}
+
+dtb_status dtb_orchestration_shard_dev(dtb_context* ctx, const dtb_cost_model* cm,
+                                       const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                                       int64_t shard_index, int64_t shard_count,
+                                       dtb_candidate* best_dev, int64_t* evaluated_dev,
+                                       void* stream) {
+  TRY(set_device(ctx));
+  if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "bad shard %lld of %lld", (long long)shard_index,
+                (long long)shard_count);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TRY(reset_err(ctx));
+  CU(cudaStreamSynchronize(ctx->stream));
+  DBuf tuples;
+  long long n = 0;
+  TRY(search(ctx, cm, stats, bs, vpp, shard_index, shard_count, best_dev,
+             reinterpret_cast<long long*>(evaluated_dev), nullptr, s, &n, tuples));
+  DevErr e;
+  CU(cudaMemcpy(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost));
+  return orch_error(ctx, cm, e, tuples.as<dtb_tuple>());
+}
+
+dtb_status dtb_best_reduce_dev(dtb_context* ctx, const dtb_candidate* records, int64_t n,
+                               dtb_candidate* best_dev, void* stream) {
+  TRY(set_device(ctx));
+  CU(launch_best_reduce(records, n, best_dev, static_cast<cudaStream_t>(stream)));
+  return DTB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,555 @@
+// Pipeline simulator kernels: schedules with events, intervals, batched
+// makespans, cost-model stage times, and per-coupled-group iteration sims
+// (reference: src/pipeline_sim.cpp, src/simulate.cpp, src/cost_model.cpp).
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+#include "sched.cuh"
+
+namespace dtb {
+
+// StageTimes::valid (pipeline_sim.cpp:214-230): 0 ok, 1 negative/NaN fwd,
+// 2 negative/NaN bwd.
+__device__ __forceinline__ int check_times(const double* f, const double* b,
+                                           int cells) {
+  for (int i = 0; i < cells; ++i)
+    if (!(f[i] >= 0.0)) return 1;
+  for (int i = 0; i < cells; ++i)
+    if (!(b[i] >= 0.0)) return 2;
+  return 0;
+}
+
+// Whole-array validation: the forward matrix is checked before the backward
+// one, as in the reference, so a fwd failure anywhere wins.
+__global__ void check_times_kernel(const double* f, const double* b, long long cells,
+                                   int* flags) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cells;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (!(f[i] >= 0.0)) atomicOr(flags, 1);
+    if (!(b[i] >= 0.0)) atomicOr(flags, 2);
+  }
+}
+
+__global__ void check_times_finish(const int* flags, DevErr* err) {
+  if (*flags & 1) dev_fail(err, E_BAD_TIMES, 1);
+  else if (*flags & 2) dev_fail(err, E_BAD_TIMES, 2);
+}
+
+cudaError_t launch_check_times(const double* fwd, const double* bwd, long long cells,
+                               DevErr* err, cudaStream_t stream) {
+  int* flags = &err->pad;  // scratch word inside the error record
+  cudaMemsetAsync(flags, 0, sizeof(int), stream);
+  if (cells > 0) {
+    long long blocks = (cells + 255) / 256;
+    if (blocks > 1024) blocks = 1024;
+    check_times_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(fwd, bwd, cells, flags);
+  }
+  check_times_finish<<<1, 1, 0, stream>>>(flags, err);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ one problem
+__global__ void schedule_events_kernel(const double* __restrict__ fwd,
+                                       const double* __restrict__ bwd, int l,
+                                       int p, int vpp, int* ev_dev, int* ev_mb,
+                                       int* ev_stage, int* ev_phase,
+                                       double* ev_start, double* ev_end,
+                                       double* busy, double* it,
+                                       double* f_end, double* b_end, int* next,
+                                       double* avail, DevErr* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int bad = check_times(fwd, bwd, l * p);
+  if (bad) {
+    dev_fail(err, E_BAD_TIMES, bad);
+    return;
+  }
+  const int devices = p / vpp;
+  const int per = 2 * l * vpp;
+  for (int d = 0; d < devices; ++d) busy[d] = 0.0;
+  double iter = 0.0;
+  int* count = reinterpret_cast<int*>(avail + devices);  // per-device emit cursor
+  for (int d = 0; d < devices; ++d) count[d] = 0;
+  auto dur = [&](int mb, int s, int ph) {
+    return ph == DTB_FORWARD ? fwd[mb * p + s] : bwd[mb * p + s];
+  };
+  auto visit = [&](int d, Op op, double start, double end) {
+    const int e = d * per + count[d]++;
+    ev_dev[e] = d;
+    ev_mb[e] = op.mb;
+    ev_stage[e] = op.stage;
+    ev_phase[e] = op.phase;
+    ev_start[e] = start;
+    ev_end[e] = end;
+    busy[d] += dur(op.mb, op.stage, op.phase);
+    iter = smax(iter, end);
+  };
+  const int e = dataflow_schedule(l, p, vpp, dur, f_end, b_end, next, avail, visit);
+  if (e) dev_fail(err, e);
+  *it = iter;
+}
+
+cudaError_t launch_schedule_events(const double* fwd, const double* bwd, int l,
+                                   int p, int vpp, int* ev_dev, int* ev_mb,
+                                   int* ev_stage, int* ev_phase,
+                                   double* ev_start, double* ev_end,
+                                   double* busy, double* it, void* scratch,
+                                   DevErr* err, cudaStream_t stream) {
+  char* s = static_cast<char*>(scratch);
+  double* f_end = reinterpret_cast<double*>(s);
+  double* b_end = f_end + static_cast<size_t>(l) * p;
+  double* avail = b_end + static_cast<size_t>(l) * p;
+  int* next = reinterpret_cast<int*>(avail + 2 * p + 2);
+  schedule_events_kernel<<<1, 32, 0, stream>>>(fwd, bwd, l, p, vpp, ev_dev,
+                                               ev_mb, ev_stage, ev_phase,
+                                               ev_start, ev_end, busy, it,
+                                               f_end, b_end, next, avail, err);
+  return cudaGetLastError();
+}
+
+// Timeline::events order (pipeline_sim.cpp:172-178): (start, device,
+// microbatch, stage); phase last for a total order.
+__device__ __forceinline__ unsigned long long ord_time(double x) {
+  if (x == 0.0) x = 0.0;
+  const unsigned long long b = __double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void event_keys_kernel(int n, const int* dev, const int* mb,
+                                  const int* stage, const int* phase,
+                                  const double* start,
+                                  unsigned long long* k_secondary,
+                                  unsigned long long* k_start, int* idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  k_secondary[i] = (static_cast<unsigned long long>(dev[i]) << 48) |
+                   (static_cast<unsigned long long>(mb[i]) << 24) |
+                   (static_cast<unsigned long long>(stage[i]) << 1) |
+                   static_cast<unsigned long long>(phase[i]);
+  k_start[i] = ord_time(start[i]);
+  idx[i] = i;
+}
+
+__global__ void gather_events_kernel(int n, const int* perm, const int* dev,
+                                     const int* mb, const int* stage,
+                                     const int* phase, const double* start,
+                                     const double* end, int* o_dev, int* o_mb,
+                                     int* o_stage, int* o_phase,
+                                     double* o_start, double* o_end) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = perm[i];
+  o_dev[i] = dev[j];
+  o_mb[i] = mb[j];
+  o_stage[i] = stage[j];
+  o_phase[i] = phase[j];
+  o_start[i] = start[j];
+  o_end[i] = end[j];
+}
+
+size_t sort_events_scratch(int n) {
+  size_t t1 = 0, t2 = 0;
+  cub::DoubleBuffer<unsigned long long> dk(nullptr, nullptr);
+  cub::DoubleBuffer<int> dv(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, dk, dv, n, 0, 64);
+  t2 = t1;
+  return static_cast<size_t>(n) * (8 * 4 + 4 * 2 + 4 * 4 + 8 * 2) + t2 + 4096;
+}
+
+// Sorts the event arrays in place into Timeline order: a stable radix sort
+// by the secondary key, then a stable radix sort by start time.
+cudaError_t launch_sort_events(int n, int* dev, int* mb, int* stage,
+                               int* phase, double* start, double* end,
+                               void* scratch, size_t bytes,
+                               cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  char* p = static_cast<char*>(scratch);
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += (b + 255) & ~size_t(255);
+    return r;
+  };
+  auto* ks = reinterpret_cast<unsigned long long*>(take(8ull * n));
+  auto* ks2 = reinterpret_cast<unsigned long long*>(take(8ull * n));
+  auto* kt = reinterpret_cast<unsigned long long*>(take(8ull * n));
+  auto* kt2 = reinterpret_cast<unsigned long long*>(take(8ull * n));
+  int* idx = reinterpret_cast<int*>(take(4ull * n));
+  int* idx2 = reinterpret_cast<int*>(take(4ull * n));
+  int* o_dev = reinterpret_cast<int*>(take(4ull * n));
+  int* o_mb = reinterpret_cast<int*>(take(4ull * n));
+  int* o_stage = reinterpret_cast<int*>(take(4ull * n));
+  int* o_phase = reinterpret_cast<int*>(take(4ull * n));
+  double* o_start = reinterpret_cast<double*>(take(8ull * n));
+  double* o_end = reinterpret_cast<double*>(take(8ull * n));
+  const size_t used = static_cast<size_t>(p - static_cast<char*>(scratch));
+  size_t temp = bytes - used;
+  const int grid = (n + 255) / 256;
+  event_keys_kernel<<<grid, 256, 0, stream>>>(n, dev, mb, stage, phase, start,
+                                              ks, kt, idx);
+  // 1) by secondary key (carry the start key along as a second pass input)
+  cub::DoubleBuffer<unsigned long long> dk(ks, ks2);
+  cub::DoubleBuffer<int> dv(idx, idx2);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(p, temp, dk, dv, n, 0, 64, stream);
+  if (e != cudaSuccess) return e;
+  // gather start keys into the secondary order, then sort stably by start
+  int* perm = dv.Current();
+  int* spare = dv.Alternate();
+  gather_events_kernel<<<grid, 256, 0, stream>>>(n, perm, dev, mb, stage, phase,
+                                                 start, end, o_dev, o_mb, o_stage,
+                                                 o_phase, o_start, o_end);
+  event_keys_kernel<<<grid, 256, 0, stream>>>(n, o_dev, o_mb, o_stage, o_phase,
+                                              o_start, ks, kt, spare);
+  cub::DoubleBuffer<unsigned long long> dk2(kt, kt2);
+  cub::DoubleBuffer<int> dv2(spare, perm);
+  e = cub::DeviceRadixSort::SortPairs(p, temp, dk2, dv2, n, 0, 64, stream);
+  if (e != cudaSuccess) return e;
+  gather_events_kernel<<<grid, 256, 0, stream>>>(n, dv2.Current(), o_dev, o_mb,
+                                                 o_stage, o_phase, o_start, o_end,
+                                                 dev, mb, stage, phase, start, end);
+  return cudaGetLastError();
+}
+
+// get_intervals (pipeline_sim.cpp:264-289) over a sorted event list.
+__global__ void get_intervals_kernel(long long n, const int* dev, const int* mb,
+                                     const int* phase, const double* start,
+                                     const double* end, long long* n_int,
+                                     double* starts, double* ends,
+                                     long long* fill_off, int* fill_mb) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // first device-0 forward and whether any device-0 backward exists
+  long long f_first = -1;
+  bool any_b = false;
+  for (long long i = 0; i < n; ++i) {
+    if (dev[i] != 0) continue;
+    if (phase[i] == DTB_FORWARD) {
+      if (f_first < 0) f_first = i;
+    } else {
+      any_b = true;
+    }
+  }
+  fill_off[0] = 0;
+  if (f_first < 0 || !any_b) {
+    *n_int = 0;
+    return;
+  }
+  double anchor = end[f_first];
+  long long fill = 0;  // cursor over device-0 forwards in event order
+  auto next_fwd = [&](long long from) {
+    while (from < n && !(dev[from] == 0 && phase[from] == DTB_FORWARD)) ++from;
+    return from;
+  };
+  fill = next_fwd(0);
+  long long k = 0, filled = 0;
+  for (long long i = 0; i < n; ++i) {
+    if (dev[i] != 0 || phase[i] != DTB_BACKWARD) continue;
+    const double s = anchor, e = start[i];
+    while (fill < n && start[fill] < s) fill = next_fwd(fill + 1);
+    while (fill < n && start[fill] < e) {
+      fill_mb[filled++] = mb[fill];
+      fill = next_fwd(fill + 1);
+    }
+    starts[k] = s;
+    ends[k] = e;
+    ++k;
+    fill_off[k] = filled;
+    anchor = end[i];
+  }
+  *n_int = k;
+}
+
+cudaError_t launch_get_intervals(long long n, const int* dev, const int* mb,
+                                 const int* phase, const double* start,
+                                 const double* end, long long* n_int,
+                                 double* starts, double* ends,
+                                 long long* fill_off, int* fill_mb,
+                                 cudaStream_t stream) {
+  get_intervals_kernel<<<1, 32, 0, stream>>>(n, dev, mb, phase, start, end,
+                                             n_int, starts, ends, fill_off,
+                                             fill_mb);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------- batched makespans
+__global__ void schedule_batch_kernel(long long batch, const double* __restrict__ fwd,
+                                      const double* __restrict__ bwd, int l, int p,
+                                      int vpp, double* __restrict__ it,
+                                      double* __restrict__ busy_out,
+                                      double* scratch, DevErr* err) {
+  const long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (b >= batch) return;
+  const size_t cells = static_cast<size_t>(l) * p;
+  const double* f = fwd + b * cells;
+  const double* bw = bwd + b * cells;
+  const int bad = check_times(f, bw, static_cast<int>(cells));
+  if (bad) {
+    dev_fail(err, E_BAD_TIMES, bad);
+    return;
+  }
+  const int devices = p / vpp;
+  // per-thread scratch: 2*p (+ cells*2 for the dataflow path) doubles
+  const size_t per = vpp == 1 ? static_cast<size_t>(3 * p + devices)
+                              : static_cast<size_t>(2 * cells + 2 * devices + devices);
+  double* s = scratch + b * per;
+  double* busy = vpp == 1 ? s + 3 * p : s + 2 * cells + 2 * devices;
+  for (int d = 0; d < devices; ++d) busy[d] = 0.0;
+  double iter = 0.0;
+  auto dur = [&](int mb, int st, int ph) {
+    return ph == DTB_FORWARD ? f[mb * p + st] : bw[mb * p + st];
+  };
+  auto visit = [&](int d, Op op, double start, double end) {
+    busy[d] += dur(op.mb, op.stage, op.phase);
+    iter = smax(iter, end);
+  };
+  if (vpp == 1) {
+    tick_1f1b(l, p, dur, s, s + p, s + 2 * p, visit);
+  } else {
+    const int e = dataflow_schedule(l, p, vpp, dur, s, s + cells,
+                                    reinterpret_cast<int*>(s + 2 * cells + devices),
+                                    s + 2 * cells, visit);
+    if (e) dev_fail(err, e);
+  }
+  it[b] = iter;
+  if (busy_out != nullptr)
+    for (int d = 0; d < devices; ++d) busy_out[b * devices + d] = busy[d];
+}
+
+size_t schedule_batch_scratch(long long batch, int l, int p, int vpp) {
+  const size_t cells = static_cast<size_t>(l) * p;
+  const int devices = p / vpp;
+  const size_t per = vpp == 1 ? static_cast<size_t>(3 * p + devices)
+                              : 2 * cells + 3 * static_cast<size_t>(devices);
+  return batch * per * sizeof(double) + 256;
+}
+
+cudaError_t launch_schedule_batch(long long batch, const double* fwd,
+                                  const double* bwd, int l, int p, int vpp,
+                                  double* it, double* busy, void* scratch,
+                                  DevErr* err, cudaStream_t stream) {
+  const int T = 128;
+  const long long grid = (batch + T - 1) / T;
+  schedule_batch_kernel<<<static_cast<unsigned>(grid), T, 0, stream>>>(
+      batch, fwd, bwd, l, p, vpp, it, busy, static_cast<double*>(scratch), err);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- cost-model kernels
+__global__ void stage_times_kernel(DevCM cm, dtb_plan plan, long long l,
+                                   const long long* enc, const long long* gen,
+                                   const int* count, double* fwd, double* bwd,
+                                   DevErr* err) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= l) return;
+  StageRow row;
+  const int e = dev_stage_row(cm, plan, mb_mean(enc[i], count[i]),
+                              mb_mean(gen[i], count[i]), &row);
+  if (e) {
+    dev_fail(err, e, e == E_EMPTY_TP || e == E_TP_NOT_ALLOWED ? 0 : 0);
+    return;
+  }
+  const int p = plan_stages(plan);
+  for (int s = 0; s < p; ++s) {
+    const int u = stage_unit(plan, s);
+    fwd[i * p + s] = row.f[u];
+    bwd[i * p + s] = row.b[u];
+  }
+}
+
+cudaError_t launch_stage_times(const DevCM& cm, const dtb_plan& plan,
+                               long long l, const long long* enc,
+                               const long long* gen, const int* count,
+                               double* fwd, double* bwd, DevErr* err,
+                               cudaStream_t stream) {
+  if (l == 0) return cudaSuccess;
+  const long long grid = (l + 127) / 128;
+  stage_times_kernel<<<static_cast<unsigned>(grid), 128, 0, stream>>>(
+      cm, plan, l, enc, gen, count, fwd, bwd, err);
+  return cudaGetLastError();
+}
+
+__global__ void fwd_keys_kernel(DevCM cm, dtb_plan plan, long long l,
+                                const long long* enc, const long long* gen,
+                                const int* count, double* keys, DevErr* err) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= l) return;
+  const int e = dev_fwd_key(cm, plan, mb_mean(enc[i], count[i]),
+                            mb_mean(gen[i], count[i]), &keys[i]);
+  if (e) dev_fail(err, e);
+}
+
+cudaError_t launch_fwd_keys(const DevCM& cm, const dtb_plan& plan, long long l,
+                            const long long* enc, const long long* gen,
+                            const int* count, double* keys, DevErr* err,
+                            cudaStream_t stream) {
+  if (l == 0) return cudaSuccess;
+  fwd_keys_kernel<<<static_cast<unsigned>((l + 127) / 128), 128, 0, stream>>>(
+      cm, plan, l, enc, gen, count, keys, err);
+  return cudaGetLastError();
+}
+
+__global__ void unit_times_kernel(DevCM cm, int kind, int tp, long long n,
+                                  const double* loads, double* fwd, double* bwd,
+                                  DevErr* err) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  int e = 0;
+  if (fwd) e = dev_unit_fwd(cm, kind, tp, loads[i], &fwd[i]);
+  if (!e && bwd) e = dev_unit_bwd(cm, kind, tp, loads[i], &bwd[i]);
+  if (e) dev_fail(err, e, tp, kind);
+}
+
+cudaError_t launch_unit_times(const DevCM& cm, int kind, int tp, long long n,
+                              const double* loads, double* fwd, double* bwd,
+                              DevErr* err, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  unit_times_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, stream>>>(
+      cm, kind, tp, n, loads, fwd, bwd, err);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------- coupled-group iteration
+// One thread per (batch, coupled group): build_stage_times rows from the
+// microbatch token sums on the fly (ring buffer of live rows) and evaluate
+// the schedule; writes the group's makespan and bubble fraction
+// (iteration_stats, pipeline_sim.cpp:355-366).
+constexpr int kRing = 66;  // plain-1F1B row ring: p + 2 <= kRing
+
+__global__ void group_sims_kernel(GroupSimArgs a, double* scratch) {
+  const long long gid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long total = a.n_batches * a.groups;
+  if (gid >= total) return;
+  const int l = a.l;
+  const int p = plan_stages(a.plan);
+  const int vpp = a.plan.vpp;
+  const int devices = p / vpp;
+  const long long base = gid * l;
+  auto tokens = [&](int i, long long* e, long long* g, int* c) {
+    const long long src = base + (a.order ? a.order[base + i] : i);
+    *e = a.enc[src];
+    *g = a.gen ? a.gen[src] : a.enc[src];
+    *c = a.count ? a.count[src] : a.span;
+  };
+  double* s = scratch + gid * (vpp == 1 ? static_cast<long long>(4 * p + 6 * kRing)
+                                        : static_cast<long long>(2 * l * p + 6 * l + 3 * devices));
+  double iter = 0.0;
+  int fault = 0;
+  if (vpp == 1) {
+    double* busy = s + 3 * p;
+    double* ring = s + 4 * p;  // [kRing][6]
+    int ring_id[kRing];
+    for (int q = 0; q < kRing; ++q) ring_id[q] = -1;
+    for (int d = 0; d < p; ++d) busy[d] = 0.0;
+    auto dur = [&](int mb, int st, int ph) {
+      const int slot = mb % (p + 2);
+      double* row = ring + slot * 6;
+      if (ring_id[slot] != mb) {
+        long long e, g;
+        int c;
+        tokens(mb, &e, &g, &c);
+        StageRow r;
+        const int code = dev_stage_row(a.cm, a.plan, mb_mean(e, c), mb_mean(g, c), &r);
+        if (code) fault = code;
+        for (int u = 0; u < 3; ++u) {
+          row[u] = r.f[u];
+          row[3 + u] = r.b[u];
+        }
+        ring_id[slot] = mb;
+      }
+      return row[(ph == DTB_FORWARD ? 0 : 3) + stage_unit(a.plan, st)];
+    };
+    // busy accumulates the durations themselves (pipeline_sim.cpp:157)
+    auto visit_exact = [&](int d, Op op, double start, double end) {
+      busy[d] += dur(op.mb, op.stage, op.phase);
+      iter = smax(iter, end);
+    };
+    tick_1f1b(l, p, dur, s, s + p, s + 2 * p, visit_exact);
+    double bub = 0.0;
+    if (iter > 0.0 && devices > 0) {
+      double idle = 0.0;
+      for (int d = 0; d < devices; ++d) idle += iter - busy[d];
+      bub = idle / (devices * iter);
+    }
+    if (a.busy) a.busy[gid] = bub;
+  } else {
+    double* f_end = s;
+    double* b_end = s + static_cast<size_t>(l) * p;
+    double* rows = b_end + static_cast<size_t>(l) * p;  // [l][6]
+    double* avail = rows + 6 * static_cast<size_t>(l);
+    double* busy = avail + devices;
+    int* next = reinterpret_cast<int*>(busy + devices);
+    for (int i = 0; i < l; ++i) {
+      long long e, g;
+      int c;
+      tokens(i, &e, &g, &c);
+      StageRow r;
+      const int code = dev_stage_row(a.cm, a.plan, mb_mean(e, c), mb_mean(g, c), &r);
+      if (code) fault = code;
+      for (int u = 0; u < 3; ++u) {
+        rows[i * 6 + u] = r.f[u];
+        rows[i * 6 + 3 + u] = r.b[u];
+      }
+    }
+    for (int d = 0; d < devices; ++d) busy[d] = 0.0;
+    auto dur = [&](int mb, int st, int ph) {
+      return rows[mb * 6 + (ph == DTB_FORWARD ? 0 : 3) + stage_unit(a.plan, st)];
+    };
+    auto visit = [&](int d, Op op, double start, double end) {
+      busy[d] += dur(op.mb, op.stage, op.phase);
+      iter = smax(iter, end);
+    };
+    const int e = dataflow_schedule(l, p, vpp, dur, f_end, b_end, next, avail, visit);
+    if (e) fault = e;
+    double bub = 0.0;
+    if (iter > 0.0 && devices > 0) {
+      double idle = 0.0;
+      for (int d = 0; d < devices; ++d) idle += iter - busy[d];
+      bub = idle / (devices * iter);
+    }
+    if (a.busy) a.busy[gid] = bub;
+  }
+  if (fault) dev_fail(a.err, fault);
+  a.t_group[gid] = iter;
+}
+
+size_t group_sims_scratch(const GroupSimArgs& a) {
+  const int p = plan_stages(a.plan);
+  const int devices = p / a.plan.vpp;
+  const long long per = a.plan.vpp == 1 ? 4 * p + 6 * kRing
+                                        : 2LL * a.l * p + 6LL * a.l + 3 * devices;
+  return static_cast<size_t>(a.n_batches * a.groups * per) * sizeof(double) + 256;
+}
+
+cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
+                              cudaStream_t stream) {
+  const long long total = a.n_batches * a.groups;
+  if (total == 0) return cudaSuccess;
+  const int T = 128;
+  group_sims_kernel<<<static_cast<unsigned>((total + T - 1) / T), T, 0, stream>>>(
+      a, static_cast<double*>(scratch));
+  return cudaGetLastError();
+}
+
+// simulate_iteration's fold over groups (simulate.cpp:31-46): slowest group
+// by strict '>' in group order, t_iter = slowest + dp_sync.  bubble (in/out)
+// holds per-group fractions; the mean is a sequential sum in group order.
+__global__ void t_iter_reduce_kernel(long long n_batches, int groups,
+                                     const double* t_group, double dp_sync,
+                                     double* t_iter) {
+  const long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (b >= n_batches) return;
+  double worst = 0.0;
+  for (int g = 0; g < groups; ++g) {
+    const double t = t_group[b * groups + g];
+    if (t > worst) worst = t;
+  }
+  t_iter[b] = worst + dp_sync;
+}
+
+cudaError_t launch_t_iter_reduce(long long n_batches, int groups,
+                                 const double* t_group, double dp_sync,
+                                 double* t_iter, cudaStream_t stream) {
+  if (n_batches == 0) return cudaSuccess;
+  t_iter_reduce_kernel<<<static_cast<unsigned>((n_batches + 127) / 128), 128, 0,
+                         stream>>>(n_batches, groups, t_group, dp_sync, t_iter);
+  return cudaGetLastError();
+}
+
+}  // namespace dtb

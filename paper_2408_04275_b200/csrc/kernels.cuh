@@ -1,0 +1,186 @@
+// Launcher declarations shared between the kernel translation units and the
+// C-ABI layer (capi.cu).
+#pragma once
+
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "dtb_internal.cuh"
+
+namespace dtb {
+
+// ---------------------------------------------------------------- intra
+struct FusedArgs {
+  int n;      // samples per global batch
+  int m;      // backbone DP groups
+  int order;  // DTB_ASCENDING / DTB_DESCENDING
+  int intra;  // ReorderMode::intra
+  const int* img_off;  // stream CSR (absolute offsets)
+  const int* img_tok;
+  const int* aud_off;  // may be null
+  const int* aud_tok;
+  int* order_out;       // [n_batches * n] batch-local intra order
+  double* load_before;  // [n_batches * m] or null
+  double* load_after;   // [n_batches * m] or null
+  unsigned char* kept;  // [n_batches] or null
+  int* orig_tok;        // [n_batches * n] modality tokens, input order, or null
+  int* staged_tok;      // [n_batches * n] modality tokens, intra order, or null
+  DevErr* err;
+};
+
+size_t fused_smem_bytes();
+int fused_max_n();
+int fused_max_m();
+cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches,
+                               cudaStream_t stream);
+
+size_t intra_generic_scratch(int n, int m);
+int intra_generic_max_m();
+cudaError_t launch_intra_generic(const double* sizes, int n, int m, int order,
+                                 int equal_counts, void* scratch,
+                                 size_t scratch_bytes, int* flat_out,
+                                 long long* offsets_out, cudaStream_t stream);
+
+cudaError_t launch_block_loads(const double* sizes, const int* order, int n,
+                               int m, double* loads, cudaStream_t stream);
+cudaError_t launch_select(const double* keys, const int* pending, int np,
+                          int k, int closest, double target, int* out,
+                          cudaStream_t stream);
+cudaError_t launch_cost_sizes(const int* img_off, const int* img_tok,
+                              const int* aud_off, const int* aud_tok,
+                              long long n, long long* out, cudaStream_t stream);
+cudaError_t launch_compute_stats(const int* img_off, const int* img_tok,
+                                 const int* aud_off, const int* aud_tok,
+                                 long long n, double* out2, cudaStream_t stream);
+
+// ------------------------------------------------------------- simulator
+// Generic schedule of one problem (any vpp) with full event materialisation
+// in op order: ev arrays [2*l*p]; busy [devices]; it [1].
+cudaError_t launch_schedule_events(const double* fwd, const double* bwd, int l,
+                                   int p, int vpp, int* ev_dev, int* ev_mb,
+                                   int* ev_stage, int* ev_phase,
+                                   double* ev_start, double* ev_end,
+                                   double* busy, double* it, void* scratch,
+                                   DevErr* err, cudaStream_t stream);
+cudaError_t launch_sort_events(int n_events, int* dev, int* mb, int* stage,
+                               int* phase, double* start, double* end,
+                               void* scratch, size_t scratch_bytes,
+                               cudaStream_t stream);
+size_t sort_events_scratch(int n_events);
+cudaError_t launch_get_intervals(long long n_events, const int* dev,
+                                 const int* mb, const int* phase,
+                                 const double* start, const double* end,
+                                 long long* n_int, double* starts,
+                                 double* ends, long long* fill_off,
+                                 int* fill_mb, cudaStream_t stream);
+cudaError_t launch_schedule_batch(long long batch, const double* fwd,
+                                  const double* bwd, int l, int p, int vpp,
+                                  double* it, double* busy, void* scratch,
+                                  DevErr* err, cudaStream_t stream);
+size_t schedule_batch_scratch(long long batch, int l, int p, int vpp);
+// StageTimes::valid over explicit matrices (E_BAD_TIMES, a = 1 fwd / 2 bwd).
+cudaError_t launch_check_times(const double* fwd, const double* bwd, long long cells,
+                               DevErr* err, cudaStream_t stream);
+
+// Stage-time rows for microbatches (build_stage_times), expanded to l x p.
+cudaError_t launch_stage_times(const DevCM& cm, const dtb_plan& plan,
+                               long long l, const long long* enc,
+                               const long long* gen, const int* count,
+                               double* fwd, double* bwd, DevErr* err,
+                               cudaStream_t stream);
+cudaError_t launch_fwd_keys(const DevCM& cm, const dtb_plan& plan, long long l,
+                            const long long* enc, const long long* gen,
+                            const int* count, double* keys, DevErr* err,
+                            cudaStream_t stream);
+cudaError_t launch_unit_times(const DevCM& cm, int kind, int tp, long long n,
+                              const double* loads, double* fwd, double* bwd,
+                              DevErr* err, cudaStream_t stream);
+
+// Makespans of coupled groups whose microbatches are given by token keys:
+// group g of batch b covers microbatches [g*l, (g+1)*l) of batch b.
+// t_group[b * groups + g] = iteration time; also device busy sums for the
+// bubble fraction when busy != null ([b*groups+g][devices]).
+struct GroupSimArgs {
+  DevCM cm;
+  dtb_plan plan;
+  long long n_batches;
+  int groups;        // coupled groups per batch
+  int l;             // microbatches per group
+  const long long* enc;  // [n_batches * groups * l] token sums
+  const long long* gen;
+  const int* count;      // sample counts (null = `span` for all)
+  int span;
+  const int* tok;        // alternative: per-microbatch tokens (int32) when span==1 path
+  const int* order;      // optional permutation of each group's microbatches
+  double* t_group;
+  double* busy;
+  DevErr* err;
+};
+cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
+                              cudaStream_t stream);
+size_t group_sims_scratch(const GroupSimArgs& a);
+
+// --------------------------------------------------------- inter reorder
+struct InterArgs {
+  long long batch;       // independent problems
+  int l, p, vpp;
+  const double* fwd;     // [batch * l * p] (explicit matrices), or null
+  const double* bwd;
+  const double* keys;    // [batch * l], or null (computed from tokens)
+  // Disaggregated form: rows from per-microbatch token sums via the cost model.
+  DevCM cm;
+  dtb_plan plan;
+  const long long* enc;  // [batch * l]
+  const long long* gen;
+  int span;
+  int* orders;           // [batch * l]
+  DevErr* err;
+};
+cudaError_t launch_inter(const InterArgs& a, void* scratch, size_t bytes,
+                         cudaStream_t stream);
+size_t inter_scratch(const InterArgs& a);
+
+// --------------------------------------------------------- orchestration
+struct OrchArgs {
+  DevCM cm;
+  dtb_workload_stats stats;
+  long long bs;
+  int vpp;
+  const dtb_tuple* tuples;
+  long long n;
+  long long shard_index, shard_count;  // evaluate i % count == index
+  dtb_candidate* out;                  // per-tuple results or null
+  dtb_candidate* block_best;           // [grid] winners
+  DevErr* err;
+};
+cudaError_t launch_enumerate(const dtb_cluster_spec& c, long long bs,
+                             const long long* divs, int n_divs,
+                             long long* count, dtb_tuple* out,
+                             long long capacity, void* scratch,
+                             cudaStream_t stream);
+cudaError_t launch_orchestration(const OrchArgs& a, int grid,
+                                 cudaStream_t stream);
+cudaError_t launch_best_reduce(const dtb_candidate* in, long long n,
+                               dtb_candidate* out, cudaStream_t stream);
+cudaError_t launch_predict(const DevCM& cm, const dtb_workload_stats& stats,
+                           const dtb_plan* plans, long long n,
+                           dtb_predicted_times* out, DevErr* err,
+                           cudaStream_t stream);
+cudaError_t launch_memory_check(const DevCM& cm, const dtb_plan& plan,
+                                dtb_memory_report* out, cudaStream_t stream);
+
+// ------------------------------------------------ disaggregated glue
+// Microbatch token sums of assembled coupled groups (assemble_microbatches,
+// src/workload.cpp:179-204) from per-position token keys.
+cudaError_t launch_assemble(long long n_batches, int n, int dp_lm, int dp_me,
+                            const int* tok_by_pos, long long* enc_out,
+                            cudaStream_t stream);
+// output_order composition (src/reorder.cpp:370-391).
+cudaError_t launch_compose(long long n_batches, int n, int dp_lm, int dp_me,
+                           const int* intra, const int* inter, int* out,
+                           cudaStream_t stream);
+cudaError_t launch_t_iter_reduce(long long n_batches, int groups,
+                                 const double* t_group, double dp_sync,
+                                 double* t_iter, cudaStream_t stream);
+
+}  // namespace dtb
