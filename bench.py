@@ -160,7 +160,6 @@ def main():
     rank, world, local = dist_init(args.gpus)
     model, cluster, book, plan = workload()
     from paper_2408_04275_b200 import _capi as A
-    from paper_2408_04275_b200.api import ReorderMode
     from paper_2408_04275_b200.workload import synth_stream
 
     n_batches_total = args.samples // BS

@@ -906,10 +906,22 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   const int span = dp_lm / dp_me;
   const long long n_mb = n_batches * dp_me * static_cast<long long>(per_group);
   const long long total = n_batches * static_cast<long long>(n);
-  DBuf intra, orig_tok, staged_tok, enc0, enc1, tgrp, inter, scr, bub;
-  CU(intra.alloc(4ull * total, s));
-  CU(orig_tok.alloc(4ull * total, s));
-  CU(staged_tok.alloc(4ull * total, s));
+  const bool direct = span == 1;  // K1 writes microbatch keys itself
+  DBuf intra, orig_tok, staged_tok, mb0, mb1, tgrp, inter, scr;
+  // without inter the intra order is the output order whenever every
+  // position belongs to a microbatch
+  const bool compose_needed = mode->inter || dp_me * span * per_group != n;
+  int* intra_out = order_out;
+  if (compose_needed) {
+    CU(intra.alloc(4ull * total, s));
+    intra_out = intra.as<int>();
+  }
+  CU(mb0.alloc(4ull * n_mb, s));
+  CU(mb1.alloc(4ull * n_mb, s));
+  if (!direct) {
+    CU(orig_tok.alloc(4ull * total, s));
+    CU(staged_tok.alloc(4ull * total, s));
+  }
   FusedArgs fa{};
   fa.n = n;
   fa.m = dp_lm;
@@ -919,31 +931,31 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   fa.img_tok = it;
   fa.aud_off = ao;
   fa.aud_tok = at;
-  fa.order_out = intra.as<int>();
+  fa.order_out = intra_out;
   fa.load_before = lb;
   fa.load_after = la;
   fa.kept = kept;
-  fa.orig_tok = orig_tok.as<int>();
-  fa.staged_tok = staged_tok.as<int>();
+  fa.orig_tok = direct ? nullptr : orig_tok.as<int>();
+  fa.staged_tok = direct ? nullptr : staged_tok.as<int>();
+  fa.pg = per_group;
+  fa.dp_me = dp_me;
+  fa.mb_orig = direct ? mb0.as<int>() : nullptr;
+  fa.mb_staged = direct ? mb1.as<int>() : nullptr;
   fa.err = ctx->err;
   CU(launch_intra_fused(fa, n_batches, s));
-  // microbatch token sums of the identity and the intra-ordered assembly
-  CU(enc0.alloc(8ull * n_mb, s));
-  CU(enc1.alloc(8ull * n_mb, s));
-  CU(launch_assemble(n_batches, n, dp_lm, dp_me, orig_tok.as<int>(), enc0.as<long long>(), s));
-  CU(launch_assemble(n_batches, n, dp_lm, dp_me, staged_tok.as<int>(), enc1.as<long long>(), s));
+  if (!direct) {
+    CU(launch_assemble(n_batches, n, dp_lm, dp_me, orig_tok.as<int>(), mb0.as<int>(), s));
+    CU(launch_assemble(n_batches, n, dp_lm, dp_me, staged_tok.as<int>(), mb1.as<int>(), s));
+  }
   GroupSimArgs ga{};
   ga.cm = cm->dev;
   ga.plan = *plan;
   ga.n_batches = n_batches;
   ga.groups = dp_me;
   ga.l = per_group;
-  ga.enc = enc0.as<long long>();
-  ga.gen = nullptr;
-  ga.count = nullptr;
+  ga.mbtok = mb0.as<int>();
   ga.span = span;
   CU(tgrp.alloc(8ull * n_batches * dp_me, s));
-  CU(bub.alloc(8ull * n_batches * dp_me, s));
   ga.t_group = tgrp.as<double>();
   ga.busy = nullptr;
   ga.err = ctx->err;
@@ -955,8 +967,8 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ia.vpp = plan->vpp;
   ia.cm = cm->dev;
   ia.plan = *plan;
-  ia.enc = enc1.as<long long>();
-  ia.gen = nullptr;
+  ia.mbtok = mb1.as<int>();
+  ia.groups = dp_me;
   ia.span = span;
   ia.err = ctx->err;
   const size_t inter_bytes = mode->inter ? inter_scratch(ia) : 0;
@@ -968,9 +980,10 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
     ia.orders = inter.as<int>();
     CU(launch_inter(ia, scr.p, inter_bytes, s));
   }
-  CU(launch_compose(n_batches, n, dp_lm, dp_me, intra.as<int>(),
-                    mode->inter ? inter.as<int>() : nullptr, order_out, s));
-  ga.enc = enc1.as<long long>();
+  if (compose_needed)
+    CU(launch_compose(n_batches, n, dp_lm, dp_me, intra_out, mode->inter ? inter.as<int>() : nullptr,
+                      order_out, s));
+  ga.mbtok = mb1.as<int>();
   ga.order = mode->inter ? inter.as<int>() : nullptr;
   CU(launch_group_sims(ga, scr.p, s));
   CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, ta, s));

@@ -172,6 +172,27 @@ __device__ __forceinline__ double mb_load(const DevCM& cm, int unit,
                                  : cm.seq_len;
 }
 
+// The build_stage_times entries (cost_model.cpp:334-362) of ONE unit at a
+// token load: f = stage_time/vpp + comm, b likewise, where stage_time =
+// coupling * whole / pp (cost_model.cpp:308-320).
+__device__ __forceinline__ int dev_unit_stage(const DevCM& cm, const dtb_plan& p, int u,
+                                              double load, bool want_f, bool want_b,
+                                              double* f, double* b) {
+  const dtb_parallelism& pc = p.unit[u];
+  const double comm = dev_comm(cm, p, u, load);
+  const double coupling = coupling_of(p, u);
+  double wf = 0.0, wb = 0.0;
+  int e = dev_unit_fwd(cm, u, pc.tp, load, &wf);
+  if (e) return e;
+  if (want_b) {
+    e = dev_unit_bwd(cm, u, pc.tp, load, &wb);
+    if (e) return e;
+  }
+  if (want_f) *f = coupling * wf / static_cast<double>(pc.pp) / p.vpp + comm;
+  if (want_b) *b = coupling * wb / static_cast<double>(pc.pp) / p.vpp + comm;
+  return 0;
+}
+
 // One microbatch row of build_stage_times (cost_model.cpp:334-362): the
 // per-unit forward/backward entry shared by all of a unit's stages.
 struct StageRow {

@@ -381,10 +381,12 @@ __global__ void inter_kernel(InterArgs a, char* scratch, long long begin,
     e = inter_one(tm, a.keys + prob * l, l, p, vpp, sc, out);
   } else {
     // token form: build_stage_times rows and microbatch_fwd_keys per microbatch
+    const long long bb = prob / a.groups;
+    const int grp = static_cast<int>(prob % a.groups);
     for (int i = 0; i < l && !e; ++i) {
-      const long long src = prob * l + i;
-      const double me = mb_mean(a.enc[src], a.span);
-      const double mg = mb_mean(a.gen ? a.gen[src] : a.enc[src], a.span);
+      const long long v = a.mbtok[(bb * l + i) * a.groups + grp];
+      const double me = mb_mean(v, a.span);
+      const double mg = me;
       StageRow r;
       e = dev_stage_row(a.cm, a.plan, me, mg, &r);
       if (!e) e = dev_fwd_key(a.cm, a.plan, me, mg, &tkeys[i]);

@@ -145,6 +145,8 @@ intra_fused_kernel(FusedArgs a) {
     kor |= key;
     zeros += cost == 0;
     if (a.orig_tok != nullptr) a.orig_tok[first + i] = static_cast<int>(t);
+    if (a.mb_orig != nullptr && i < a.pg * a.dp_me)
+      a.mb_orig[(b * a.pg + i % a.pg) * a.dp_me + i / a.pg] = static_cast<int>(t);
   }
   const long long bmax = block_max_ll<kFusedT>(maxc, S.tmpll);
   if (bmax > 0xffffffffll) {
@@ -239,25 +241,23 @@ intra_fused_kernel(FusedArgs a) {
   }
 
   // ---- 5. the intra order (batch-local indices) and staged token keys
+  const int mb_span = a.pg * a.dp_me;
+  auto put_staged = [&](int pos, unsigned int key) {
+    const int tok = static_cast<int>((desc ? ~key : key) >> 1);  // cost_size / 2
+    if (a.staged_tok != nullptr) a.staged_tok[first + pos] = tok;
+    if (a.mb_staged != nullptr && pos < mb_span)
+      a.mb_staged[(b * a.pg + pos % a.pg) * a.dp_me + pos / a.pg] = tok;
+  };
   if (keep) {
     for (int k = tid; k < n; k += kFusedT) {
       const unsigned int as = S.asg[k];
       const int pos = S.off[as >> 16] + static_cast<int>(as & 0xffffu);
-      const int idx = S.vals[k];
-      a.order_out[first + pos] = idx;
-      if (a.staged_tok != nullptr) {
-        const unsigned int key = S.keys[k];
-        a.staged_tok[first + pos] = static_cast<int>((desc ? ~key : key) >> 1);
-      }
+      a.order_out[first + pos] = S.vals[k];
+      put_staged(pos, S.keys[k]);
     }
   } else {
     for (int i = tid; i < n; i += kFusedT) a.order_out[first + i] = i;
-    if (a.staged_tok != nullptr) {
-      for (int k = tid; k < n; k += kFusedT) {
-        const unsigned int key = S.keys[k];
-        a.staged_tok[first + S.vals[k]] = static_cast<int>((desc ? ~key : key) >> 1);
-      }
-    }
+    for (int k = tid; k < n; k += kFusedT) put_staged(S.vals[k], S.keys[k]);
   }
 }
 

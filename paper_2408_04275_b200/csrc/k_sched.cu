@@ -406,114 +406,178 @@ cudaError_t launch_unit_times(const DevCM& cm, int kind, int tp, long long n,
 }
 
 // ------------------------------------------------- coupled-group iteration
-// One thread per (batch, coupled group): build_stage_times rows from the
-// microbatch token sums on the fly (ring buffer of live rows) and evaluate
-// the schedule; writes the group's makespan and bubble fraction
-// (iteration_stats, pipeline_sim.cpp:355-366).
-constexpr int kRing = 66;  // plain-1F1B row ring: p + 2 <= kRing
+// Microbatch token keys of coupled group `gid`, position i (after the
+// group's optional reorder): stream layout [b][i][e] (int32, enc == gen,
+// count == span) or group-contiguous int64 enc/gen/count arrays.
+struct GroupTok {
+  const GroupSimArgs* a;
+  long long gid;
+  __device__ __forceinline__ void operator()(int i, long long* e, long long* g, int* c) const {
+    const int l = a->l;
+    const int src_i = a->order ? a->order[gid * l + i] : i;
+    if (a->mbtok) {
+      const long long b = gid / a->groups;
+      const int grp = static_cast<int>(gid % a->groups);
+      const long long v = a->mbtok[(b * l + src_i) * a->groups + grp];
+      *e = v;
+      *g = v;
+      *c = a->span;
+    } else {
+      const long long src = gid * l + src_i;
+      *e = a->enc[src];
+      *g = a->gen ? a->gen[src] : a->enc[src];
+      *c = a->count ? a->count[src] : a->span;
+    }
+  }
+};
 
-__global__ void group_sims_kernel(GroupSimArgs a, double* scratch) {
+// Fast path: plain 1F1B with P stages known at compile time.  Tick state
+// lives in registers; build_stage_times entries are evaluated on demand —
+// backbone entries are constants (their load is always seq_len) and every
+// encoder/generator cell needs its value exactly once, so no row cache.
+template <int P>
+__global__ void __launch_bounds__(128)
+group_sims_fast(GroupSimArgs a) {
   const long long gid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  const long long total = a.n_batches * a.groups;
-  if (gid >= total) return;
+  if (gid >= a.n_batches * a.groups) return;
+  const GroupTok tok{&a, gid};
   const int l = a.l;
-  const int p = plan_stages(a.plan);
-  const int vpp = a.plan.vpp;
-  const int devices = p / vpp;
-  const long long base = gid * l;
-  auto tokens = [&](int i, long long* e, long long* g, int* c) {
-    const long long src = base + (a.order ? a.order[base + i] : i);
-    *e = a.enc[src];
-    *g = a.gen ? a.gen[src] : a.enc[src];
-    *c = a.count ? a.count[src] : a.span;
-  };
-  double* s = scratch + gid * (vpp == 1 ? static_cast<long long>(4 * p + 6 * kRing)
-                                        : static_cast<long long>(2 * l * p + 6 * l + 3 * devices));
-  double iter = 0.0;
+  int unit[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) unit[s] = stage_unit(a.plan, s);
   int fault = 0;
-  if (vpp == 1) {
-    double* busy = s + 3 * p;
-    double* ring = s + 4 * p;  // [kRing][6]
-    int ring_id[kRing];
-    for (int q = 0; q < kRing; ++q) ring_id[q] = -1;
-    for (int d = 0; d < p; ++d) busy[d] = 0.0;
-    auto dur = [&](int mb, int st, int ph) {
-      const int slot = mb % (p + 2);
-      double* row = ring + slot * 6;
-      if (ring_id[slot] != mb) {
-        long long e, g;
-        int c;
-        tokens(mb, &e, &g, &c);
-        StageRow r;
-        const int code = dev_stage_row(a.cm, a.plan, mb_mean(e, c), mb_mean(g, c), &r);
-        if (code) fault = code;
-        for (int u = 0; u < 3; ++u) {
-          row[u] = r.f[u];
-          row[3 + u] = r.b[u];
-        }
-        ring_id[slot] = mb;
+  double fB = 0.0, bB = 0.0;
+  fault = dev_unit_stage(a.cm, a.plan, DTB_BACKBONE, a.cm.seq_len, true, true, &fB, &bB);
+  auto dur = [&](int i, int s, int ph) -> double {
+    const int u = unit[s];
+    if (u == DTB_BACKBONE) return ph == DTB_FORWARD ? fB : bB;
+    long long e, g;
+    int c;
+    tok(i, &e, &g, &c);
+    double f = 0.0, b = 0.0;
+    const int code = dev_unit_stage(a.cm, a.plan, u, mb_mean(u == DTB_ENCODER ? e : g, c),
+                                    ph == DTB_FORWARD, ph != DTB_FORWARD, &f, &b);
+    if (code) fault = code;
+    return ph == DTB_FORWARD ? f : b;
+  };
+  double avail[P], prev[P], cur[P], busy[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) avail[s] = prev[s] = cur[s] = busy[s] = 0.0;
+  double iter = 0.0;
+  const int last_tick = 2 * l + 2 * P - 3;
+  for (int t = 0; t <= last_tick; ++t) {
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int d = t - s;
+      if (d < 0) continue;
+      int mb, ph;
+      double dep;
+      if ((d & 1) == 0) {
+        mb = d >> 1;
+        if (mb >= l) continue;
+        ph = DTB_FORWARD;
+        dep = s > 0 ? prev[s - 1] : 0.0;
+      } else {
+        const int q = t - 2 * P + 1 + s;
+        if (q < 0) continue;
+        mb = q >> 1;
+        if (mb >= l) continue;
+        ph = DTB_BACKWARD;
+        dep = s + 1 < P ? prev[s + 1] : prev[s];
       }
-      return row[(ph == DTB_FORWARD ? 0 : 3) + stage_unit(a.plan, st)];
-    };
-    // busy accumulates the durations themselves (pipeline_sim.cpp:157)
-    auto visit_exact = [&](int d, Op op, double start, double end) {
-      busy[d] += dur(op.mb, op.stage, op.phase);
+      const double x = dur(mb, s, ph);
+      const double start = smax(avail[s], dep);
+      const double end = start + x;
+      avail[s] = end;
+      cur[s] = end;
+      busy[s] += x;
       iter = smax(iter, end);
-    };
-    tick_1f1b(l, p, dur, s, s + p, s + 2 * p, visit_exact);
+    }
+#pragma unroll
+    for (int s = 0; s < P; ++s) prev[s] = cur[s];
+  }
+  if (a.busy) {
     double bub = 0.0;
-    if (iter > 0.0 && devices > 0) {
+    if (iter > 0.0) {
       double idle = 0.0;
-      for (int d = 0; d < devices; ++d) idle += iter - busy[d];
-      bub = idle / (devices * iter);
+#pragma unroll
+      for (int s = 0; s < P; ++s) idle += iter - busy[s];
+      bub = idle / (P * iter);
     }
-    if (a.busy) a.busy[gid] = bub;
-  } else {
-    double* f_end = s;
-    double* b_end = s + static_cast<size_t>(l) * p;
-    double* rows = b_end + static_cast<size_t>(l) * p;  // [l][6]
-    double* avail = rows + 6 * static_cast<size_t>(l);
-    double* busy = avail + devices;
-    int* next = reinterpret_cast<int*>(busy + devices);
-    for (int i = 0; i < l; ++i) {
-      long long e, g;
-      int c;
-      tokens(i, &e, &g, &c);
-      StageRow r;
-      const int code = dev_stage_row(a.cm, a.plan, mb_mean(e, c), mb_mean(g, c), &r);
-      if (code) fault = code;
-      for (int u = 0; u < 3; ++u) {
-        rows[i * 6 + u] = r.f[u];
-        rows[i * 6 + 3 + u] = r.b[u];
-      }
-    }
-    for (int d = 0; d < devices; ++d) busy[d] = 0.0;
-    auto dur = [&](int mb, int st, int ph) {
-      return rows[mb * 6 + (ph == DTB_FORWARD ? 0 : 3) + stage_unit(a.plan, st)];
-    };
-    auto visit = [&](int d, Op op, double start, double end) {
-      busy[d] += dur(op.mb, op.stage, op.phase);
-      iter = smax(iter, end);
-    };
-    const int e = dataflow_schedule(l, p, vpp, dur, f_end, b_end, next, avail, visit);
-    if (e) fault = e;
-    double bub = 0.0;
-    if (iter > 0.0 && devices > 0) {
-      double idle = 0.0;
-      for (int d = 0; d < devices; ++d) idle += iter - busy[d];
-      bub = idle / (devices * iter);
-    }
-    if (a.busy) a.busy[gid] = bub;
+    a.busy[gid] = bub;
   }
   if (fault) dev_fail(a.err, fault);
   a.t_group[gid] = iter;
 }
 
+// General path (any stage count, interleaved schedules): rows of
+// build_stage_times materialised per group in scratch.
+__global__ void group_sims_kernel(GroupSimArgs a, double* scratch) {
+  const long long gid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long total = a.n_batches * a.groups;
+  if (gid >= total) return;
+  const GroupTok tok{&a, gid};
+  const int l = a.l;
+  const int p = plan_stages(a.plan);
+  const int vpp = a.plan.vpp;
+  const int devices = p / vpp;
+  double* s = scratch + gid * (2LL * l * p + 6LL * l + 3 * devices);
+  double* f_end = s;
+  double* b_end = s + static_cast<size_t>(l) * p;
+  double* rows = b_end + static_cast<size_t>(l) * p;  // [l][6]
+  double* avail = rows + 6 * static_cast<size_t>(l);
+  double* busy = avail + devices;
+  int* next = reinterpret_cast<int*>(busy + devices);
+  int fault = 0;
+  for (int i = 0; i < l; ++i) {
+    long long e, g;
+    int c;
+    tok(i, &e, &g, &c);
+    StageRow r;
+    const int code = dev_stage_row(a.cm, a.plan, mb_mean(e, c), mb_mean(g, c), &r);
+    if (code) fault = code;
+    for (int u = 0; u < 3; ++u) {
+      rows[i * 6 + u] = r.f[u];
+      rows[i * 6 + 3 + u] = r.b[u];
+    }
+  }
+  for (int d = 0; d < devices; ++d) busy[d] = 0.0;
+  double iter = 0.0;
+  auto dur = [&](int mb, int st, int ph) {
+    return rows[mb * 6 + (ph == DTB_FORWARD ? 0 : 3) + stage_unit(a.plan, st)];
+  };
+  // busy accumulates the durations themselves (pipeline_sim.cpp:157)
+  auto visit = [&](int d, Op op, double start, double end) {
+    busy[d] += dur(op.mb, op.stage, op.phase);
+    iter = smax(iter, end);
+  };
+  if (vpp == 1) {
+    tick_1f1b(l, p, dur, f_end, f_end + p, f_end + 2 * p, visit);
+  } else {
+    const int e = dataflow_schedule(l, p, vpp, dur, f_end, b_end, next, avail, visit);
+    if (e) fault = e;
+  }
+  double bub = 0.0;
+  if (iter > 0.0 && devices > 0) {
+    double idle = 0.0;
+    for (int d = 0; d < devices; ++d) idle += iter - busy[d];
+    bub = idle / (devices * iter);
+  }
+  if (a.busy) a.busy[gid] = bub;
+  if (fault) dev_fail(a.err, fault);
+  a.t_group[gid] = iter;
+}
+
+static bool fast_sims(const GroupSimArgs& a) {
+  const int p = plan_stages(a.plan);
+  return a.plan.vpp == 1 && p >= 2 && p <= 8;
+}
+
 size_t group_sims_scratch(const GroupSimArgs& a) {
+  if (fast_sims(a)) return 256;
   const int p = plan_stages(a.plan);
   const int devices = p / a.plan.vpp;
-  const long long per = a.plan.vpp == 1 ? 4 * p + 6 * kRing
-                                        : 2LL * a.l * p + 6LL * a.l + 3 * devices;
+  const long long per = 2LL * a.l * p + 6LL * a.l + 3 * devices;
   return static_cast<size_t>(a.n_batches * a.groups * per) * sizeof(double) + 256;
 }
 
@@ -522,8 +586,20 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
   const long long total = a.n_batches * a.groups;
   if (total == 0) return cudaSuccess;
   const int T = 128;
-  group_sims_kernel<<<static_cast<unsigned>((total + T - 1) / T), T, 0, stream>>>(
-      a, static_cast<double*>(scratch));
+  const unsigned grid = static_cast<unsigned>((total + T - 1) / T);
+  if (fast_sims(a)) {
+    switch (plan_stages(a.plan)) {
+      case 2: group_sims_fast<2><<<grid, T, 0, stream>>>(a); break;
+      case 3: group_sims_fast<3><<<grid, T, 0, stream>>>(a); break;
+      case 4: group_sims_fast<4><<<grid, T, 0, stream>>>(a); break;
+      case 5: group_sims_fast<5><<<grid, T, 0, stream>>>(a); break;
+      case 6: group_sims_fast<6><<<grid, T, 0, stream>>>(a); break;
+      case 7: group_sims_fast<7><<<grid, T, 0, stream>>>(a); break;
+      default: group_sims_fast<8><<<grid, T, 0, stream>>>(a); break;
+    }
+  } else {
+    group_sims_kernel<<<grid, T, 0, stream>>>(a, static_cast<double*>(scratch));
+  }
   return cudaGetLastError();
 }
 

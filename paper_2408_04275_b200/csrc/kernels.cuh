@@ -25,6 +25,13 @@ struct FusedArgs {
   unsigned char* kept;  // [n_batches] or null
   int* orig_tok;        // [n_batches * n] modality tokens, input order, or null
   int* staged_tok;      // [n_batches * n] modality tokens, intra order, or null
+  // span == 1 (DP_me == DP_lm): microbatch (e, i) is position e*pg + i, so the
+  // kernel writes the microbatch token keys directly in the stream layout
+  // [n_batches][pg][dp_me] consumed by the simulator / inter kernels.
+  int pg;               // samples per backbone group (global_batch / dp_lm)
+  int dp_me;
+  int* mb_orig;         // identity assembly, or null
+  int* mb_staged;       // intra-ordered assembly, or null
   DevErr* err;
 };
 
@@ -106,12 +113,15 @@ struct GroupSimArgs {
   long long n_batches;
   int groups;        // coupled groups per batch
   int l;             // microbatches per group
-  const long long* enc;  // [n_batches * groups * l] token sums
+  const long long* enc;  // [n_batches * groups * l] token sums (group-contiguous)
   const long long* gen;
   const int* count;      // sample counts (null = `span` for all)
   int span;
-  const int* tok;        // alternative: per-microbatch tokens (int32) when span==1 path
-  const int* order;      // optional permutation of each group's microbatches
+  // Stream layout instead of enc/gen/count: modality-token sums of the
+  // assembled microbatches, [n_batches][l][groups] (encoder == generator
+  // tokens, count == span), so a warp of groups reads one coalesced row.
+  const int* mbtok;
+  const int* order;      // optional [n_batches][groups][l] microbatch order
   double* t_group;
   double* busy;
   DevErr* err;
@@ -127,11 +137,12 @@ struct InterArgs {
   const double* fwd;     // [batch * l * p] (explicit matrices), or null
   const double* bwd;
   const double* keys;    // [batch * l], or null (computed from tokens)
-  // Disaggregated form: rows from per-microbatch token sums via the cost model.
+  // Disaggregated form: rows from per-microbatch token sums via the cost
+  // model, stream layout [batch / groups][l][groups] (problem = b*groups+e).
   DevCM cm;
   dtb_plan plan;
-  const long long* enc;  // [batch * l]
-  const long long* gen;
+  const int* mbtok;
+  int groups;
   int span;
   int* orders;           // [batch * l]
   DevErr* err;
@@ -171,9 +182,10 @@ cudaError_t launch_memory_check(const DevCM& cm, const dtb_plan& plan,
 
 // ------------------------------------------------ disaggregated glue
 // Microbatch token sums of assembled coupled groups (assemble_microbatches,
-// src/workload.cpp:179-204) from per-position token keys.
+// src/workload.cpp:179-204) from per-position token keys, written in the
+// stream layout [n_batches][pg][dp_me].
 cudaError_t launch_assemble(long long n_batches, int n, int dp_lm, int dp_me,
-                            const int* tok_by_pos, long long* enc_out,
+                            const int* tok_by_pos, int* mbtok_out,
                             cudaStream_t stream);
 // output_order composition (src/reorder.cpp:370-391).
 cudaError_t launch_compose(long long n_batches, int n, int dp_lm, int dp_me,
