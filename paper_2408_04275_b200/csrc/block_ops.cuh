@@ -164,4 +164,67 @@ __device__ void tile_radix_sort(K* keys, V* vals, int n, int lo_bit,
   }
 }
 
+// One stable counting pass over n <= T*ITEMS 32-bit items in place, digit
+// given by digit(pos, item) in [0, 1 << RB).  Same warp-striped ranking as
+// tile_radix_sort; used both for the cost-key passes (digit = key bits) and
+// for the group partition after the greedy (digit = group id).
+template <int T, int ITEMS, int RB, typename DigitFn>
+__device__ void tile_pass_u32(unsigned int* items, int n, const DigitFn& digit, int* cnt,
+                              int* scan_tmp) {
+  constexpr int W = T / 32;
+  constexpr int D = 1 << RB;
+  const int lane = lane_id(), w = warp_id();
+  const unsigned lt = lanemask_lt();
+  for (int i = threadIdx.x; i < D * W; i += T) cnt[i] = 0;
+  static_assert(ITEMS % 2 == 0, "ranks are packed in pairs");
+  unsigned int k[ITEMS];
+  unsigned int rk[ITEMS / 2];  // two 16-bit ranks per register; digits recomputed
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int pos = w * 32 * ITEMS + i * 32 + lane;
+    const bool ok = pos < n;
+    k[i] = ok ? items[pos] : 0u;
+    const unsigned d = ok ? static_cast<unsigned>(digit(pos, k[i])) : D;
+    const unsigned peers = __match_any_sync(kFull, d);
+    int before = 0;
+    if (ok) before = cnt[d * W + w];
+    __syncwarp();
+    if (ok && (peers & lt) == 0) cnt[d * W + w] = before + __popc(peers);
+    __syncwarp();
+    const unsigned r = static_cast<unsigned>(before + __popc(peers & lt));
+    if (i & 1) rk[i >> 1] |= r << 16;
+    else rk[i >> 1] = r;
+  }
+  __syncthreads();
+  constexpr int PER = (D * W + T - 1) / T;
+  int local[PER];
+  int sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int idx = threadIdx.x * PER + j;
+    local[j] = idx < D * W ? cnt[idx] : 0;
+    sum += local[j];
+  }
+  int total;
+  int base = block_excl_scan<T>(sum, scan_tmp, &total);
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int idx = threadIdx.x * PER + j;
+    if (idx < D * W) cnt[idx] = base;
+    base += local[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int pos = w * 32 * ITEMS + i * 32 + lane;
+    if (pos < n) {
+      const unsigned d = static_cast<unsigned>(digit(pos, k[i]));
+      const unsigned r = (i & 1) ? (rk[i >> 1] >> 16) : (rk[i >> 1] & 0xffffu);
+      items[cnt[d * W + w] + r] = k[i];
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace dtb

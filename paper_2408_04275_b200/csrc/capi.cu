@@ -293,6 +293,14 @@ dtb_status dtb_context_create(int32_t device, dtb_context** out) {
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    // keep stream-ordered scratch cached across calls (no per-call cudaMalloc)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->err, sizeof(DevErr));
   if (e != cudaSuccess) {
     delete ctx;
@@ -941,6 +949,9 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   fa.dp_me = dp_me;
   fa.mb_orig = direct ? mb0.as<int>() : nullptr;
   fa.mb_staged = direct ? mb1.as<int>() : nullptr;
+  DBuf wide;
+  CU(wide.alloc(fused_wide_scratch_bytes(n_batches), s));
+  fa.wide_scratch = wide.as<unsigned char>();
   fa.err = ctx->err;
   CU(launch_intra_fused(fa, n_batches, s));
   if (!direct) {
@@ -1066,6 +1077,9 @@ dtb_status dtb_intra_stream_dev(dtb_context* ctx, int64_t bs, int32_t dp_lm, int
   fa.load_before = load_before;
   fa.load_after = load_after;
   fa.kept = greedy_kept;
+  DBuf wide;
+  CU(wide.alloc(fused_wide_scratch_bytes(n_batches), static_cast<cudaStream_t>(stream)));
+  fa.wide_scratch = wide.as<unsigned char>();
   fa.err = ctx->err;
   CU(launch_intra_fused(fa, n_batches, static_cast<cudaStream_t>(stream)));
   return DTB_OK;

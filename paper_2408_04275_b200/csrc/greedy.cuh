@@ -37,6 +37,7 @@ struct GreedyState {
   L* TL;      // [m] merge scratch
   int* TG;    // [m]
   int* tmp;   // [T/32 + 2] reduction scratch
+  L* gload;   // [m] final load per group id (null: not recorded)
 };
 
 template <typename L>
@@ -84,7 +85,10 @@ __device__ void greedy_rounds(int n, int m, int cap, int z0, int z1,
           const int c0 = st.cnt[g];
           for (int t = 0; t < take; ++t) assign(k + pre + t, g, c0 + t);
           st.cnt[g] = c0 + take;
-          if (take == cap_local[e] && take > 0) ++full_here;
+          if (take == cap_local[e] && take > 0) {
+            ++full_here;
+            if (st.gload) st.gload[g] = st.AL[j];
+          }
         }
         pre += cap_local[e];
       }
@@ -215,10 +219,13 @@ __device__ void greedy_rounds(int n, int m, int cap, int z0, int z1,
       const int g = st.AG[i];
       const int c0 = st.cnt[g];
       assign(k + i, g, c0);
+      const L nl = st.AL[i] + sizes(k + i);
       if (c0 + 1 < cap) {
-        st.TL[keep_pre] = st.AL[i] + sizes(k + i);
+        st.TL[keep_pre] = nl;
         st.TG[keep_pre] = g;
         ++keep_pre;
+      } else if (st.gload) {
+        st.gload[g] = nl;
       }
     }
     __syncthreads();
@@ -291,6 +298,9 @@ __device__ void greedy_rounds(int n, int m, int cap, int z0, int z1,
     k += R;
     __syncthreads();
   }
+  if (st.gload)
+    for (int j = tid; j < r; j += T) st.gload[st.AG[j]] = st.AL[j];
+  __syncthreads();
 }
 
 }  // namespace dtb

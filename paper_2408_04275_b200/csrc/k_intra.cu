@@ -1,15 +1,21 @@
 // Intra-microbatch reordering kernels (Alg. 2).
 //
-//  * intra_generic_kernel  — intra_partition(sizes, m, order, equal_counts)
+//  * intra_generic_kernel — intra_partition(sizes, m, order, equal_counts)
 //    for arbitrary doubles (reference: src/reorder.cpp:30-90).  One CTA per
-//    problem; keys/values in global scratch.
-//  * intra_fused_kernel    — the disaggregated hot path, one CTA per global
-//    batch, everything staged in shared memory: per-sample cost from the CSR
-//    (Sample::cost_size, core.hpp:160-167) -> stable radix sort by cost ->
-//    greedy equal-count partition -> block_group_loads of greedy and identity
-//    orders -> keep-greedy-if-no-worse decision (src/reorder.cpp:340-354) ->
-//    output order, both load vectors and the per-position token keys the
-//    microbatch stage consumes.
+//    problem after a stable device radix sort of (orderable key, index).
+//  * intra_fused_kernel — the disaggregated hot path, one CTA per global
+//    batch, staged in shared memory: per-sample cost from the CSR
+//    (Sample::cost_size, core.hpp:160-167) -> stable LSD radix sort by cost
+//    -> greedy equal-count partition (greedy.cuh) -> block_group_loads of the
+//    greedy and the identity order -> keep-greedy-if-no-worse
+//    (src/reorder.cpp:340-354) -> output order, both load vectors and the
+//    microbatch token keys the simulator consumes.
+//
+// Fused layout: 16-bit cost keys, 16-bit sample indices and 16-bit
+// (group, slot) assignments (96 KB for a 16K batch) so two CTAs share an SM
+// and one CTA's loads overlap the other's sort/greedy.  A batch whose costs
+// or (group, slot) ranges do not fit 16 bits is processed by the same code
+// with 32-bit arrays in a global scratch slot (`wide_scratch`).
 #include <cub/cub.cuh>
 
 #include "block_ops.cuh"
@@ -28,13 +34,12 @@ __device__ __forceinline__ unsigned long long ord_bits(double x) {
 
 // ------------------------------------------------------------------ generic
 constexpr int kGenT = 1024;
-constexpr int kGenEmax = 4;    // m <= 4096
+constexpr int kGenEmax = 4;  // m <= 4096
 
 __global__ void __launch_bounds__(kGenT)
 intra_keys_kernel(const double* __restrict__ sizes, int n, int order,
                   unsigned long long* __restrict__ keys, int* __restrict__ vals) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += gridDim.x * blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const unsigned long long k = ord_bits(sizes[i]);
     keys[i] = order == DTB_DESCENDING ? ~k : k;
     vals[i] = i;
@@ -43,12 +48,11 @@ intra_keys_kernel(const double* __restrict__ sizes, int n, int order,
 
 __global__ void __launch_bounds__(kGenT)
 intra_generic_kernel(const double* __restrict__ sizes, int n, int m, int order,
-                     int equal_counts, const int* __restrict__ vals,
-                     int* __restrict__ g_of, int* __restrict__ slot_of,
-                     int* __restrict__ flat_out, long long* __restrict__ offsets_out,
-                     GreedyState<double> st) {
+                     int equal_counts, const int* __restrict__ vals, int* __restrict__ g_of,
+                     int* __restrict__ slot_of, int* __restrict__ flat_out,
+                     long long* __restrict__ offsets_out, GreedyState<double> st) {
   __shared__ int s_tmp[kGenT / 32 + 2];
-  // zero run in sorted order
+  // the zero run in sorted order (zeros are contiguous; -0.0 == 0.0)
   int below = 0, zeros = 0;
   for (int i = threadIdx.x; i < n; i += kGenT) {
     const double x = sizes[i];
@@ -64,9 +68,8 @@ intra_generic_kernel(const double* __restrict__ sizes, int n, int m, int order,
     g_of[k] = g;
     slot_of[k] = slot;
   };
-  greedy_rounds<kGenT, kGenEmax, double>(n, m, cap, tot_below,
-                                         tot_below + tot_zeros, size_at, assign,
-                                         st);
+  greedy_rounds<kGenT, kGenEmax, double>(n, m, cap, tot_below, tot_below + tot_zeros, size_at,
+                                         assign, st);
   // group offsets (exclusive scan of counts) and the flat order
   const int E = (m + kGenT - 1) / kGenT;
   int local = 0;
@@ -86,203 +89,342 @@ intra_generic_kernel(const double* __restrict__ sizes, int n, int m, int order,
   }
   if (threadIdx.x == 0) offsets_out[m] = total;
   __syncthreads();
-  for (int k = threadIdx.x; k < n; k += kGenT) {
-    flat_out[st.TG[g_of[k]] + slot_of[k]] = vals[k];
-  }
+  for (int k = threadIdx.x; k < n; k += kGenT) flat_out[st.TG[g_of[k]] + slot_of[k]] = vals[k];
 }
 
 // -------------------------------------------------------------------- fused
-// One CTA per global batch of n <= kFusedT * kFusedItems samples.
 constexpr int kFusedT = 512;
 constexpr int kFusedItems = 32;
-constexpr int kFusedMaxN = kFusedT * kFusedItems;  // 16384
-constexpr int kFusedEmax = 1;                      // m <= 512
+constexpr int kFusedMaxN = kFusedT * kFusedItems;  // 16384 samples per batch
+constexpr int kNarrowMaxM = 128;                    // groups in the smem path
+constexpr int kWideMaxM = 512;                      // groups in the global path
+constexpr int kRB = 7;                              // radix digit bits
 
-struct FusedSmem {
-  unsigned int keys[kFusedMaxN];        // cost (asc) or ~cost (desc)
-  unsigned short vals[kFusedMaxN];      // batch-local sample index
-  unsigned int asg[kFusedMaxN];         // (group << 16) | slot per sorted item
-  int radix_cnt[256 * (kFusedT / 32)];
-  long long AL[kFusedT], TL[kFusedT];
-  int AG[kFusedT], TG[kFusedT], cnt[kFusedT], off[kFusedT];
-  unsigned long long blk_greedy[kFusedT], blk_ident[kFusedT];
+// Narrow (shared-memory) state, ~102 KB so two CTAs share an SM.
+//   items[k] = (key << 16) | sample index, key = modality tokens (asc) or
+//   0x7fff - tokens (desc); cost_size = 2 * tokens, so sorting by key is
+//   sorting by cost, and one array carries key, index and token.
+struct NarrowSmem {
+  unsigned int items[kFusedMaxN];
+  unsigned char grp[kFusedMaxN];  // greedy group of sorted item k
+  int radix_cnt[(1 << kRB) * (kFusedT / 32)];
+  long long AL[kNarrowMaxM], TL[kNarrowMaxM], gload[kNarrowMaxM];
+  unsigned long long blk_ident[kNarrowMaxM], blk_greedy[kNarrowMaxM];
+  int AG[kNarrowMaxM], TG[kNarrowMaxM], cnt[kNarrowMaxM];
   int tmp[kFusedT / 32 + 2];
   long long tmpll[kFusedT / 32 + 1];
+  unsigned int s_and, s_or;
 };
 
-size_t fused_smem_bytes() { return sizeof(FusedSmem); }
+constexpr size_t kFusedSmem = sizeof(NarrowSmem);
+// Wide fallback (any cost <= 2^32-1, m <= 512) in a global scratch slot.
+constexpr size_t kWidePerBatch = static_cast<size_t>(kFusedMaxN) * (4 + 2 + 4) +
+                                 static_cast<size_t>(kWideMaxM) * (8 * 5 + 4 * 4) + 1024;
+
+size_t fused_smem_bytes() { return kFusedSmem; }
 int fused_max_n() { return kFusedMaxN; }
-int fused_max_m() { return kFusedT; }
+int fused_max_m() { return kWideMaxM; }
+size_t fused_wide_scratch_bytes(long long n_batches) { return kWidePerBatch * n_batches; }
 
-__global__ void __launch_bounds__(kFusedT, 1)
-intra_fused_kernel(FusedArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  FusedSmem& S = *reinterpret_cast<FusedSmem*>(smem_raw);
-  const int n = a.n;
-  const int m = a.m;
-  const long long b = blockIdx.x;
+// Microbatch key of position pos (span == 1 stream layout [b][pg][dp_me]).
+__device__ __forceinline__ long long mb_index(const FusedArgs& a, long long b, int pos) {
+  return (b * a.pg + pos % a.pg) * a.dp_me + pos / a.pg;
+}
+
+__device__ __forceinline__ void write_outputs_common(const FusedArgs& a, long long b, int g,
+                                                     unsigned long long ident,
+                                                     unsigned long long after) {
+  if (a.load_before) a.load_before[b * a.m + g] = static_cast<double>(ident);
+  if (a.load_after) a.load_after[b * a.m + g] = static_cast<double>(after);
+}
+
+// ---- wide path: 32-bit keys, (group, slot) assignments, global scratch.
+__device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowSmem& S) {
+  const int n = a.n, m = a.m, tid = threadIdx.x;
   const long long first = b * n;
-  const int tid = threadIdx.x;
-
-  // ---- 1. per-sample cost (Sample::cost_size) and sort keys
+  const bool desc = a.order == DTB_DESCENDING;
+  unsigned char* slot = a.wide_scratch + static_cast<size_t>(b) * kWidePerBatch;
+  auto* keys = reinterpret_cast<unsigned int*>(slot);
+  auto* vals = reinterpret_cast<unsigned short*>(slot + 4ull * kFusedMaxN);
+  auto* asg = reinterpret_cast<unsigned int*>(slot + 6ull * kFusedMaxN);
+  char* st_mem = reinterpret_cast<char*>(slot + 10ull * kFusedMaxN);
+  GreedyState<long long> st;
+  st.AL = reinterpret_cast<long long*>(st_mem);
+  st.TL = st.AL + kWideMaxM;
+  st.gload = st.TL + kWideMaxM;
+  auto* blk_g = reinterpret_cast<unsigned long long*>(st.gload + kWideMaxM);
+  auto* blk_i = blk_g + kWideMaxM;
+  st.AG = reinterpret_cast<int*>(blk_i + kWideMaxM);
+  st.TG = st.AG + kWideMaxM;
+  st.cnt = st.TG + kWideMaxM;
+  int* off = st.cnt + kWideMaxM;
+  st.tmp = S.tmp;
   unsigned int kand = ~0u, kor = 0u;
   int zeros = 0;
-  long long maxc = 0;
+  for (int g = tid; g < m; g += kFusedT) blk_i[g] = blk_g[g] = 0ull;
+  __syncthreads();
+  const int pg = n / m;
   for (int i = tid; i < n; i += kFusedT) {
-    const long long g = first + i;
+    const long long gi = first + i;
     long long t = 0;
-    for (int q = a.img_off[g]; q < a.img_off[g + 1]; ++q) t += a.img_tok[q];
+    for (int x = a.img_off[gi]; x < a.img_off[gi + 1]; ++x) t += a.img_tok[x];
     if (a.aud_off != nullptr)
-      for (int q = a.aud_off[g]; q < a.aud_off[g + 1]; ++q) t += a.aud_tok[q];
-    const long long cost = t + t;
-    maxc = cost > maxc ? cost : maxc;
-    if (cost < 0) maxc = 0x100000000ll;  // negative tokens: out of key range
-    const unsigned int c = static_cast<unsigned int>(cost);
-    const unsigned int key = a.order == DTB_DESCENDING ? ~c : c;
-    S.keys[i] = key;
-    S.vals[i] = static_cast<unsigned short>(i);
+      for (int x = a.aud_off[gi]; x < a.aud_off[gi + 1]; ++x) t += a.aud_tok[x];
+    const unsigned int c = static_cast<unsigned int>(t + t);
+    const unsigned int key = desc ? ~c : c;
+    keys[i] = key;
+    vals[i] = static_cast<unsigned short>(i);
     kand &= key;
     kor |= key;
-    zeros += cost == 0;
-    if (a.orig_tok != nullptr) a.orig_tok[first + i] = static_cast<int>(t);
-    if (a.mb_orig != nullptr && i < a.pg * a.dp_me)
-      a.mb_orig[(b * a.pg + i % a.pg) * a.dp_me + i / a.pg] = static_cast<int>(t);
+    zeros += c == 0;
+    atomicAdd(&blk_i[min(i / pg, m - 1)], static_cast<unsigned long long>(c));
+    if (a.mb_orig != nullptr && i < a.pg * a.dp_me) a.mb_orig[mb_index(a, b, i)] = static_cast<int>(t);
   }
-  const long long bmax = block_max_ll<kFusedT>(maxc, S.tmpll);
-  if (bmax > 0xffffffffll) {
-    if (tid == 0) dev_fail(a.err, E_COST_RANGE, static_cast<int>(b));
-    return;
+  if (tid == 0) {
+    S.s_and = ~0u;
+    S.s_or = 0u;
   }
+  __syncthreads();
+  atomicAnd(&S.s_and, kand);
+  atomicOr(&S.s_or, kor);
   int tot_zeros;
   block_excl_scan<kFusedT>(zeros, S.tmp, &tot_zeros);
-  {
-    __shared__ unsigned int s_and, s_or;
-    if (tid == 0) {
-      s_and = ~0u;
-      s_or = 0u;
-    }
-    __syncthreads();
-    atomicAnd(&s_and, kand);
-    atomicOr(&s_or, kor);
-    __syncthreads();
-    const unsigned int varying = s_and ^ s_or;
+  const unsigned int varying = S.s_and ^ S.s_or;
+  if (a.intra) {
     const int lo = varying ? __ffs(static_cast<int>(varying)) - 1 : 0;
     const int hi = varying ? 32 - __clz(static_cast<int>(varying)) : 0;
-    // ---- 2. stable LSD radix sort by cost (index order breaks ties)
-    // digit width: split the varying window into the fewest <=8-bit passes
-    const int width = hi - lo;
-    const int passes = (width + 7) / 8;
-    const int rb = passes ? (width + passes - 1) / passes : 8;
-    if (rb <= 7)
-      tile_radix_sort<kFusedT, kFusedItems, 7>(S.keys, S.vals, n, lo, hi,
-                                               S.radix_cnt, S.tmp);
-    else
-      tile_radix_sort<kFusedT, kFusedItems, 8>(S.keys, S.vals, n, lo, hi,
-                                               S.radix_cnt, S.tmp);
-  }
-
-  // ---- 3. greedy equal-count partition
-  const bool desc = a.order == DTB_DESCENDING;
-  const int z0 = desc ? n - tot_zeros : 0;
-  const int z1 = desc ? n : tot_zeros;
-  const int cap = (n + m - 1) / m;
-  GreedyState<long long> st{S.AL, S.AG, S.cnt, S.TL, S.TG, S.tmp};
-  auto size_at = [&](int k) -> long long {
-    const unsigned int key = S.keys[k];
-    return static_cast<long long>(desc ? ~key : key);
-  };
-  auto assign = [&](int k, int g, int slot) {
-    S.asg[k] = (static_cast<unsigned int>(g) << 16) | static_cast<unsigned int>(slot);
-  };
-  if (a.intra) {
-    greedy_rounds<kFusedT, kFusedEmax, long long>(n, m, cap, z0, z1, size_at,
-                                                  assign, st);
-  }
-
-  // ---- 4. block_group_loads of the greedy and the identity order
-  const int pg = n / m;  // block size (src/reorder.cpp:113)
-  for (int g = tid; g < m; g += kFusedT) {
-    S.blk_greedy[g] = 0ull;
-    S.blk_ident[g] = 0ull;
-  }
-  int pre_local = (tid < m && a.intra) ? S.cnt[tid] : 0;
-  int total;
-  const int pre = block_excl_scan<kFusedT>(pre_local, S.tmp, &total);
-  if (tid < m) S.off[tid] = pre;
-  __syncthreads();
-  for (int k = tid; k < n; k += kFusedT) {
-    const unsigned int key = S.keys[k];
-    const unsigned long long sz = desc ? ~key : key;
-    const int idx = S.vals[k];
-    atomicAdd(&S.blk_ident[min(idx / pg, m - 1)], sz);
-    if (a.intra) {
-      const unsigned int as = S.asg[k];
-      const int pos = S.off[as >> 16] + static_cast<int>(as & 0xffffu);
-      atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], sz);
+    tile_radix_sort<kFusedT, kFusedItems, kRB>(keys, vals, n, lo, hi, S.radix_cnt, S.tmp);
+    const int z0 = desc ? n - tot_zeros : 0;
+    const int z1 = desc ? n : tot_zeros;
+    const int cap = (n + m - 1) / m;
+    auto size_at = [&](int k) -> long long {
+      return static_cast<long long>(desc ? ~keys[k] : keys[k]);
+    };
+    auto assign = [&](int k, int g, int sl) {
+      asg[k] = (static_cast<unsigned>(g) << 16) | static_cast<unsigned>(sl);
+    };
+    greedy_rounds<kFusedT, 1, long long>(n, m, cap, z0, z1, size_at, assign, st);
+    int pre_local = tid < m ? st.cnt[tid] : 0;
+    int total;
+    const int pre = block_excl_scan<kFusedT>(pre_local, S.tmp, &total);
+    if (tid < m) off[tid] = pre;
+    __syncthreads();
+    for (int k = tid; k < n; k += kFusedT) {
+      const unsigned as = asg[k];
+      const int pos = off[as >> 16] + static_cast<int>(as & 0xffffu);
+      atomicAdd(&blk_g[min(pos / pg, m - 1)], static_cast<unsigned long long>(size_at(k)));
     }
+    __syncthreads();
   }
-  __syncthreads();
   long long mg = 0, mi = 0;
   for (int g = tid; g < m; g += kFusedT) {
-    mg = max(mg, static_cast<long long>(S.blk_greedy[g]));
-    mi = max(mi, static_cast<long long>(S.blk_ident[g]));
+    mg = max(mg, static_cast<long long>(blk_g[g]));
+    mi = max(mi, static_cast<long long>(blk_i[g]));
   }
-  // src/reorder.cpp:350-353: keep the greedy split when its max block load
-  // is no worse than the incoming order's.
   mg = block_max_ll<kFusedT>(mg, S.tmpll);
   mi = block_max_ll<kFusedT>(mi, S.tmpll);
   const bool keep = a.intra && mg <= mi;
   if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
-  for (int g = tid; g < m; g += kFusedT) {
-    if (a.load_before) a.load_before[b * m + g] = static_cast<double>(S.blk_ident[g]);
-    if (a.load_after)
-      a.load_after[b * m + g] =
-          static_cast<double>(keep ? S.blk_greedy[g] : S.blk_ident[g]);
-  }
-
-  // ---- 5. the intra order (batch-local indices) and staged token keys
+  for (int g = tid; g < m; g += kFusedT) write_outputs_common(a, b, g, blk_i[g], keep ? blk_g[g] : blk_i[g]);
   const int mb_span = a.pg * a.dp_me;
-  auto put_staged = [&](int pos, unsigned int key) {
-    const int tok = static_cast<int>((desc ? ~key : key) >> 1);  // cost_size / 2
+  for (int k = tid; k < n; k += kFusedT) {
+    const unsigned int key = keys[k];
+    const int tok = static_cast<int>((desc ? ~key : key) >> 1);
+    int pos = vals[k];
+    if (keep) {
+      const unsigned as = asg[k];
+      pos = off[as >> 16] + static_cast<int>(as & 0xffffu);
+    }
+    a.order_out[first + pos] = keep ? vals[k] : pos;
     if (a.staged_tok != nullptr) a.staged_tok[first + pos] = tok;
-    if (a.mb_staged != nullptr && pos < mb_span)
-      a.mb_staged[(b * a.pg + pos % a.pg) * a.dp_me + pos / a.pg] = tok;
-  };
+    if (a.mb_staged != nullptr && pos < mb_span) a.mb_staged[mb_index(a, b, pos)] = tok;
+  }
+}
+
+__global__ void __launch_bounds__(kFusedT, 2)
+intra_fused_kernel(FusedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw);
+  const int n = a.n, m = a.m, tid = threadIdx.x;
+  const int lane = lane_id(), w = warp_id();
+  const long long b = blockIdx.x;
+  const long long first = b * n;
+  const int pg = n / m;
+  const bool desc = a.order == DTB_DESCENDING;
+
+  // ---- 1. per-sample cost (Sample::cost_size = 2 * modality tokens).  Each
+  // warp streams a contiguous run of samples, 32 per step, with 8 steps of
+  // independent offset loads in flight; identity block loads
+  // (block_group_loads of the incoming order) are warp-reduced when a step's
+  // 32 samples share a block.
+  for (int g = tid; g < m; g += kFusedT) S.blk_ident[g] = 0ull;
+  if (tid == 0) {
+    S.s_and = ~0u;
+    S.s_or = 0u;
+  }
+  __syncthreads();
+  unsigned int kand = ~0u, kor = 0u;
+  int zeros = 0;
+  int maxtok = 0;
+  constexpr int U = 4;
+  const int per_warp = (n + (kFusedT / 32) - 1) / (kFusedT / 32);
+  const int w_lo = w * per_warp;
+  const int w_hi = min(n, w_lo + per_warp);
+  for (int s0 = w_lo; s0 < w_hi; s0 += 32 * U) {
+    int ib[U], ie[U], ab[U], ae[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = s0 + u * 32 + lane;
+      const bool ok = i < w_hi;
+      ib[u] = ok ? __ldg(a.img_off + first + i) : 0;
+      ie[u] = ok ? __ldg(a.img_off + first + i + 1) : 0;
+      ab[u] = ok && a.aud_off ? __ldg(a.aud_off + first + i) : 0;
+      ae[u] = ok && a.aud_off ? __ldg(a.aud_off + first + i + 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = s0 + u * 32 + lane;
+      const bool ok = i < w_hi;
+      long long t = 0;
+      for (int x = ib[u]; x < ie[u]; ++x) t += __ldg(a.img_tok + x);
+      for (int x = ab[u]; x < ae[u]; ++x) t += __ldg(a.aud_tok + x);
+      // identity block loads: warp-reduce when all 32 samples share a block
+      const int blk = ok ? min(i / pg, m - 1) : -1;
+      const long long cost = ok ? t + t : 0;
+      const int blk0 = __shfl_sync(kFull, blk, 0);
+      if (__all_sync(kFull, blk == blk0 || blk < 0)) {
+        long long sum = cost;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+        if (lane == 0 && blk0 >= 0) atomicAdd(&S.blk_ident[blk0], static_cast<unsigned long long>(sum));
+      } else if (ok) {
+        atomicAdd(&S.blk_ident[blk], static_cast<unsigned long long>(cost));
+      }
+      if (!ok) continue;
+      const int tok = t > 0x7fffffffll ? 0x7fffffff : (t < 0 ? 0x7fffffff : static_cast<int>(t));
+      maxtok = max(maxtok, tok);
+      const unsigned key = desc ? static_cast<unsigned>(0x7fff - min(tok, 0x7fff))
+                                : static_cast<unsigned>(min(tok, 0x7fff));
+      kand &= key;
+      kor |= key;
+      zeros += t == 0;
+      S.items[i] = (key << 16) | static_cast<unsigned>(i);
+      if (a.orig_tok != nullptr) a.orig_tok[first + i] = tok;
+      if (a.mb_orig != nullptr && i < a.pg * a.dp_me) a.mb_orig[mb_index(a, b, i)] = tok;
+    }
+  }
+  atomicAnd(&S.s_and, kand);
+  atomicOr(&S.s_or, kor);
+  const int tmax = block_min<kFusedT>(-maxtok, S.tmp);  // -max
+  int tot_zeros;
+  block_excl_scan<kFusedT>(zeros, S.tmp, &tot_zeros);
+  if (-tmax > 0x7fff || m > kNarrowMaxM || n > 65536) {
+    // costs beyond 16 bits (or too many groups) take the 32-bit path
+    fused_wide(a, b, S);
+    return;
+  }
+  bool keep = false;
+  if (a.intra) {
+    // ---- 2. stable LSD radix sort by key over its varying bit window
+    const unsigned varying = S.s_and ^ S.s_or;
+    const int lo = varying ? __ffs(static_cast<int>(varying)) - 1 : 0;
+    const int hi = varying ? 32 - __clz(static_cast<int>(varying)) : 0;
+    for (int sh = lo; sh < hi; sh += kRB) {
+      const int bits = min(kRB, hi - sh);
+      const unsigned mask = (1u << bits) - 1u;
+      tile_pass_u32<kFusedT, kFusedItems, kRB>(
+          S.items, n, [&](int, unsigned it) { return ((it >> 16) >> sh) & mask; }, S.radix_cnt,
+          S.tmp);
+    }
+    // ---- 3. greedy equal-count partition (sizes = 2 * tokens)
+    const int z0 = desc ? n - tot_zeros : 0;
+    const int z1 = desc ? n : tot_zeros;
+    const int cap = (n + m - 1) / m;
+    auto size_at = [&](int k) -> long long {
+      const unsigned key = S.items[k] >> 16;
+      const long long tok = desc ? 0x7fff - static_cast<long long>(key) : key;
+      return tok + tok;
+    };
+    auto assign = [&](int k, int g, int) { S.grp[k] = static_cast<unsigned char>(g); };
+    GreedyState<long long> st{S.AL, S.AG, S.cnt, S.TL, S.TG, S.tmp, S.gload};
+    greedy_rounds<kFusedT, 1, long long>(n, m, cap, z0, z1, size_at, assign, st);
+    // ---- 4. flat order = sorted items stably partitioned by group: the
+    // items of a group keep assignment order (IntraPartition::flat).
+    tile_pass_u32<kFusedT, kFusedItems, kRB>(
+        S.items, n, [&](int pos, unsigned) { return static_cast<unsigned>(S.grp[pos]); },
+        S.radix_cnt, S.tmp);
+    // greedy block loads: group loads when blocks are groups, else sums over
+    // the flat order's blocks
+    if (n % m == 0) {
+      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = static_cast<unsigned long long>(S.gload[g]);
+    } else {
+      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = 0ull;
+      __syncthreads();
+      for (int pos = tid; pos < n; pos += kFusedT) {
+        const unsigned key = S.items[pos] >> 16;
+        const long long tok = desc ? 0x7fff - static_cast<long long>(key) : key;
+        atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], static_cast<unsigned long long>(tok + tok));
+      }
+    }
+    __syncthreads();
+    long long mg = 0, mi = 0;
+    for (int g = tid; g < m; g += kFusedT) {
+      mg = max(mg, static_cast<long long>(S.blk_greedy[g]));
+      mi = max(mi, static_cast<long long>(S.blk_ident[g]));
+    }
+    mg = block_max_ll<kFusedT>(mg, S.tmpll);
+    mi = block_max_ll<kFusedT>(mi, S.tmpll);
+    // src/reorder.cpp:350-353: keep the greedy split when its max block load
+    // is no worse than the incoming order's (integer loads: exact).
+    keep = mg <= mi;
+  } else {
+    __syncthreads();
+  }
+  if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
+  for (int g = tid; g < m; g += kFusedT)
+    write_outputs_common(a, b, g, S.blk_ident[g], keep ? S.blk_greedy[g] : S.blk_ident[g]);
+  // ---- 5. outputs: the intra order and the staged microbatch keys
+  const int mb_span = a.pg * a.dp_me;
   if (keep) {
-    for (int k = tid; k < n; k += kFusedT) {
-      const unsigned int as = S.asg[k];
-      const int pos = S.off[as >> 16] + static_cast<int>(as & 0xffffu);
-      a.order_out[first + pos] = S.vals[k];
-      put_staged(pos, S.keys[k]);
+    for (int pos = tid; pos < n; pos += kFusedT) {  // coalesced
+      const unsigned it = S.items[pos];
+      const unsigned key = it >> 16;
+      const int tok = desc ? 0x7fff - static_cast<int>(key) : static_cast<int>(key);
+      a.order_out[first + pos] = static_cast<int>(it & 0xffffu);
+      if (a.staged_tok != nullptr) a.staged_tok[first + pos] = tok;
+      if (a.mb_staged != nullptr && pos < mb_span) a.mb_staged[mb_index(a, b, pos)] = tok;
     }
   } else {
     for (int i = tid; i < n; i += kFusedT) a.order_out[first + i] = i;
-    for (int k = tid; k < n; k += kFusedT) put_staged(S.vals[k], S.keys[k]);
+    for (int k = tid; k < n; k += kFusedT) {
+      const unsigned it = S.items[k];
+      const int pos = static_cast<int>(it & 0xffffu);
+      const unsigned key = it >> 16;
+      const int tok = desc ? 0x7fff - static_cast<int>(key) : static_cast<int>(key);
+      if (a.staged_tok != nullptr) a.staged_tok[first + pos] = tok;
+      if (a.mb_staged != nullptr && pos < mb_span) a.mb_staged[mb_index(a, b, pos)] = tok;
+    }
   }
 }
 
 // ------------------------------------------------------------- host glue
-cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches,
-                               cudaStream_t stream) {
+cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(intra_fused_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sizeof(FusedSmem)));
+                                         static_cast<int>(kFusedSmem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  intra_fused_kernel<<<static_cast<unsigned>(n_batches), kFusedT,
-                       sizeof(FusedSmem), stream>>>(a);
+  intra_fused_kernel<<<static_cast<unsigned>(n_batches), kFusedT, kFusedSmem, stream>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_intra_generic(const double* sizes, int n, int m, int order,
-                                 int equal_counts, void* scratch,
-                                 size_t scratch_bytes, int* flat_out,
+cudaError_t launch_intra_generic(const double* sizes, int n, int m, int order, int equal_counts,
+                                 void* scratch, size_t scratch_bytes, int* flat_out,
                                  long long* offsets_out, cudaStream_t stream) {
-  // scratch layout: keys[n] u64, keys_alt[n] u64, vals[n], vals_alt[n],
-  // g_of[n], slot_of[n], greedy state (5 * m words), cub temp.
+  // scratch: keys[n] u64 x2, vals[n] x2, g_of[n], slot_of[n], greedy state, cub temp
   char* p = static_cast<char*>(scratch);
   auto take = [&](size_t bytes) {
     char* r = p;
@@ -302,6 +444,7 @@ cudaError_t launch_intra_generic(const double* sizes, int n, int m, int order,
   st.TG = reinterpret_cast<int*>(take(sizeof(int) * m));
   st.cnt = reinterpret_cast<int*>(take(sizeof(int) * m));
   st.tmp = reinterpret_cast<int*>(take(sizeof(int) * (kGenT / 32 + 2)));
+  st.gload = nullptr;
   const size_t used = static_cast<size_t>(p - static_cast<char*>(scratch));
   if (used > scratch_bytes) return cudaErrorMemoryAllocation;
   const int grid = (n + kGenT - 1) / kGenT;
@@ -313,9 +456,8 @@ cudaError_t launch_intra_generic(const double* sizes, int n, int m, int order,
   cub::DoubleBuffer<int> dv(vals, vals2);
   cudaError_t e = cub::DeviceRadixSort::SortPairs(p, temp, dk, dv, n, 0, 64, stream);
   if (e != cudaSuccess) return e;
-  intra_generic_kernel<<<1, kGenT, 0, stream>>>(sizes, n, m, order, equal_counts,
-                                                dv.Current(), g_of, slot_of,
-                                                flat_out, offsets_out, st);
+  intra_generic_kernel<<<1, kGenT, 0, stream>>>(sizes, n, m, order, equal_counts, dv.Current(),
+                                                g_of, slot_of, flat_out, offsets_out, st);
   return cudaGetLastError();
 }
 

@@ -32,9 +32,11 @@ struct FusedArgs {
   int dp_me;
   int* mb_orig;         // identity assembly, or null
   int* mb_staged;       // intra-ordered assembly, or null
+  unsigned char* wide_scratch;  // [n_batches * fused_wide_scratch_bytes(1)]
   DevErr* err;
 };
 
+size_t fused_wide_scratch_bytes(long long n_batches);
 size_t fused_smem_bytes();
 int fused_max_n();
 int fused_max_m();
