@@ -193,6 +193,103 @@ __device__ __forceinline__ int dev_unit_stage(const DevCM& cm, const dtb_plan& p
   return 0;
 }
 
+// build_stage_times entries of one unit with every microbatch-independent
+// quantity hoisted: the plan/profile constants are read once per thread,
+// the interpolation parameter t is shared between the forward and backward
+// columns (the reference computes the same t twice from the same inputs),
+// and divisions by exactly 1.0 (pp == 1, vpp == 1, one sample per
+// microbatch) are skipped since x / 1.0 == x in IEEE arithmetic.
+struct UnitEval {
+  const double* xs;
+  const double* yf;
+  const double* yb;
+  int n;            // profile rows at the unit's TP (0: analytic)
+  int analytic;
+  double two_pc;    // 2.0 * param_count (analytic)
+  double denom;     // peak * efficiency
+  double ratio;     // analytic bwd/fwd
+  double bfac;      // backward factor
+  double two_hidden;
+  double coupling;
+  double bw;
+  double pp;
+  double vpp;
+  bool pp1, vpp1;
+
+  __device__ __forceinline__ void init(const DevCM& cm, const dtb_plan& p, int u) {
+    const dtb_parallelism& pc = p.unit[u];
+    const int ti = tp_index(pc.tp);
+    analytic = !cm.nonempty[u];
+    n = (analytic || ti < 0) ? 0 : cm.cnt[u][ti];
+    const int o = (analytic || ti < 0) ? 0 : cm.off[u][ti];
+    xs = cm.load + o;
+    yf = cm.fwd + o;
+    yb = cm.bwd + o;
+    two_pc = 2.0 * cm.param_count[u];
+    denom = cm.analytic_denom;
+    ratio = cm.analytic_ratio;
+    bfac = cm.bwd_factor[u];
+    two_hidden = 2.0 * cm.hidden[u];
+    coupling = coupling_of(p, u);
+    const bool intra = 2 * pc.tp * pc.dp <= cm.cluster.gpus_per_node;
+    bw = intra ? cm.cluster.intra_node_bw : cm.cluster.inter_node_bw;
+    pp = static_cast<double>(pc.pp);
+    vpp = static_cast<double>(p.vpp);
+    pp1 = pc.pp == 1;
+    vpp1 = p.vpp == 1;
+  }
+
+  // (f, b) of build_stage_times at token load x (host-validated book).
+  __device__ __forceinline__ void eval(double x, double* f, double* b) const {
+    const double comm = two_hidden * x * coupling / bw;
+    double wf, wb;
+    if (analytic) {
+      wf = two_pc * x / denom;
+      wb = ratio * wf;
+    } else if (x <= xs[0]) {
+      wf = yf[0];
+      wb = yb[0];
+    } else if (x >= xs[n - 1]) {
+      wf = yf[n - 1];
+      wb = yb[n - 1];
+    } else {
+      int lo = 0, hi = n;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (xs[mid] < x) lo = mid + 1;
+        else hi = mid;
+      }
+      if (xs[lo] == x) {
+        wf = yf[lo];
+        wb = yb[lo];
+      } else {
+        const int a = lo - 1;
+        const double t = (x - xs[a]) / (xs[lo] - xs[a]);
+        wf = yf[a] + t * (yf[lo] - yf[a]);
+        wb = yb[a] + t * (yb[lo] - yb[a]);
+      }
+    }
+    wb = wb * bfac;
+    double sf = coupling * wf, sb = coupling * wb;
+    if (!pp1) {
+      sf = sf / pp;
+      sb = sb / pp;
+    }
+    if (!vpp1) {
+      sf = sf / vpp;
+      sb = sb / vpp;
+    }
+    *f = sf + comm;
+    *b = sb + comm;
+  }
+};
+
+__device__ __forceinline__ double mb_mean_fast(long long tokens, int count) {
+  return count == 1   ? static_cast<double>(tokens)
+         : count == 0 ? 0.0
+                      : static_cast<double>(tokens) / static_cast<double>(count);
+}
+
 // One microbatch row of build_stage_times (cost_model.cpp:334-362): the
 // per-unit forward/backward entry shared by all of a unit's stages.
 struct StageRow {

@@ -435,63 +435,90 @@ struct GroupTok {
 // lives in registers; build_stage_times entries are evaluated on demand —
 // backbone entries are constants (their load is always seq_len) and every
 // encoder/generator cell needs its value exactly once, so no row cache.
-template <int P>
+template <int P, bool STREAM>
 __global__ void __launch_bounds__(128)
 group_sims_fast(GroupSimArgs a) {
   const long long gid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (gid >= a.n_batches * a.groups) return;
-  const GroupTok tok{&a, gid};
   const int l = a.l;
+  // token access: stream layout [b][i][e] or group-contiguous arrays
+  const long long bidx = gid / a.groups;
+  const int grp = static_cast<int>(gid - bidx * a.groups);
+  const int* tokp = STREAM ? a.mbtok + bidx * l * a.groups + grp : nullptr;
+  const long long* encp = STREAM ? nullptr : a.enc + gid * l;
+  const long long* genp = STREAM ? nullptr : (a.gen ? a.gen + gid * l : encp);
+  const int* cntp = STREAM ? nullptr : (a.count ? a.count + gid * l : nullptr);
+  const int* ord = a.order ? a.order + gid * l : nullptr;
+  UnitEval ue, ub, ug;
+  ue.init(a.cm, a.plan, DTB_ENCODER);
+  ub.init(a.cm, a.plan, DTB_BACKBONE);
+  ug.init(a.cm, a.plan, DTB_GENERATOR);
+  double fB, bB;
+  ub.eval(a.cm.seq_len, &fB, &bB);  // backbone load is always seq_len
   int unit[P];
 #pragma unroll
   for (int s = 0; s < P; ++s) unit[s] = stage_unit(a.plan, s);
-  int fault = 0;
-  double fB = 0.0, bB = 0.0;
-  fault = dev_unit_stage(a.cm, a.plan, DTB_BACKBONE, a.cm.seq_len, true, true, &fB, &bB);
-  auto dur = [&](int i, int s, int ph) -> double {
-    const int u = unit[s];
-    if (u == DTB_BACKBONE) return ph == DTB_FORWARD ? fB : bB;
-    long long e, g;
-    int c;
-    tok(i, &e, &g, &c);
-    double f = 0.0, b = 0.0;
-    const int code = dev_unit_stage(a.cm, a.plan, u, mb_mean(u == DTB_ENCODER ? e : g, c),
-                                    ph == DTB_FORWARD, ph != DTB_FORWARD, &f, &b);
-    if (code) fault = code;
-    return ph == DTB_FORWARD ? f : b;
-  };
+  // shift register of the live microbatch rows: slot k holds microbatch
+  // i - k while ticks 2i, 2i+1 run (every index below is a constant)
+  double rfE[P + 1], rbE[P + 1], rfG[P + 1], rbG[P + 1];
   double avail[P], prev[P], cur[P], busy[P];
 #pragma unroll
   for (int s = 0; s < P; ++s) avail[s] = prev[s] = cur[s] = busy[s] = 0.0;
+#pragma unroll
+  for (int k = 0; k <= P; ++k) rfE[k] = rbE[k] = rfG[k] = rbG[k] = 0.0;
   double iter = 0.0;
-  const int last_tick = 2 * l + 2 * P - 3;
-  for (int t = 0; t <= last_tick; ++t) {
+  int fault = 0;
+  auto cell = [&](int s, int mb, bool fwd, int k) {
+    if (mb < 0 || mb >= l) return;
+    const int u = unit[s];
+    const double x = u == DTB_BACKBONE ? (fwd ? fB : bB)
+                     : u == DTB_ENCODER ? (fwd ? rfE[k] : rbE[k])
+                                        : (fwd ? rfG[k] : rbG[k]);
+    const double dep = fwd ? (s > 0 ? prev[s - 1] : 0.0) : (s + 1 < P ? prev[s + 1] : prev[s]);
+    const double start = smax(avail[s], dep);
+    const double end = start + x;
+    avail[s] = end;
+    cur[s] = end;
+    busy[s] += x;
+    iter = smax(iter, end);
+  };
+  for (int i = 0; i < l + P - 1; ++i) {
+#pragma unroll
+    for (int k = P; k > 0; --k) {
+      rfE[k] = rfE[k - 1];
+      rbE[k] = rbE[k - 1];
+      rfG[k] = rfG[k - 1];
+      rbG[k] = rbG[k - 1];
+    }
+    if (i < l) {
+      const int src = ord ? ord[i] : i;
+      long long te, tg;
+      int c;
+      if (STREAM) {
+        te = tg = tokp[static_cast<long long>(src) * a.groups];
+        c = a.span;
+      } else {
+        te = encp[src];
+        tg = genp[src];
+        c = cntp ? cntp[src] : a.span;
+      }
+      if (te < 0 || tg < 0) fault = E_NEG_LOAD;
+      ue.eval(mb_mean_fast(te, c), &rfE[0], &rbE[0]);
+      ug.eval(mb_mean_fast(tg, c), &rfG[0], &rbG[0]);
+    }
+    // even tick 2i: F(i - s/2, s) on even s, B(i - P + (s+1)/2, s) on odd s
 #pragma unroll
     for (int s = 0; s < P; ++s) {
-      const int d = t - s;
-      if (d < 0) continue;
-      int mb, ph;
-      double dep;
-      if ((d & 1) == 0) {
-        mb = d >> 1;
-        if (mb >= l) continue;
-        ph = DTB_FORWARD;
-        dep = s > 0 ? prev[s - 1] : 0.0;
-      } else {
-        const int q = t - 2 * P + 1 + s;
-        if (q < 0) continue;
-        mb = q >> 1;
-        if (mb >= l) continue;
-        ph = DTB_BACKWARD;
-        dep = s + 1 < P ? prev[s + 1] : prev[s];
-      }
-      const double x = dur(mb, s, ph);
-      const double start = smax(avail[s], dep);
-      const double end = start + x;
-      avail[s] = end;
-      cur[s] = end;
-      busy[s] += x;
-      iter = smax(iter, end);
+      if ((s & 1) == 0) cell(s, i - s / 2, true, s / 2);
+      else cell(s, i - P + (s + 1) / 2, false, P - (s + 1) / 2);
+    }
+#pragma unroll
+    for (int s = 0; s < P; ++s) prev[s] = cur[s];
+    // odd tick 2i+1: F(i - (s-1)/2, s) on odd s, B(i - P + 1 + s/2, s) on even s
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      if (s & 1) cell(s, i - (s - 1) / 2, true, (s - 1) / 2);
+      else cell(s, i - P + 1 + s / 2, false, P - 1 - s / 2);
     }
 #pragma unroll
     for (int s = 0; s < P; ++s) prev[s] = cur[s];
@@ -589,13 +616,13 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
   const unsigned grid = static_cast<unsigned>((total + T - 1) / T);
   if (fast_sims(a)) {
     switch (plan_stages(a.plan)) {
-      case 2: group_sims_fast<2><<<grid, T, 0, stream>>>(a); break;
-      case 3: group_sims_fast<3><<<grid, T, 0, stream>>>(a); break;
-      case 4: group_sims_fast<4><<<grid, T, 0, stream>>>(a); break;
-      case 5: group_sims_fast<5><<<grid, T, 0, stream>>>(a); break;
-      case 6: group_sims_fast<6><<<grid, T, 0, stream>>>(a); break;
-      case 7: group_sims_fast<7><<<grid, T, 0, stream>>>(a); break;
-      default: group_sims_fast<8><<<grid, T, 0, stream>>>(a); break;
+      case 2: a.mbtok ? group_sims_fast<2, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<2, false><<<grid, T, 0, stream>>>(a); break;
+      case 3: a.mbtok ? group_sims_fast<3, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<3, false><<<grid, T, 0, stream>>>(a); break;
+      case 4: a.mbtok ? group_sims_fast<4, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<4, false><<<grid, T, 0, stream>>>(a); break;
+      case 5: a.mbtok ? group_sims_fast<5, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<5, false><<<grid, T, 0, stream>>>(a); break;
+      case 6: a.mbtok ? group_sims_fast<6, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<6, false><<<grid, T, 0, stream>>>(a); break;
+      case 7: a.mbtok ? group_sims_fast<7, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<7, false><<<grid, T, 0, stream>>>(a); break;
+      default: a.mbtok ? group_sims_fast<8, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<8, false><<<grid, T, 0, stream>>>(a); break;
     }
   } else {
     group_sims_kernel<<<grid, T, 0, stream>>>(a, static_cast<double*>(scratch));
