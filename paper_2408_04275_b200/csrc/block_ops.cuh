@@ -28,6 +28,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s, int* total) {
     const int y = __shfl_up_sync(kFull, x, o);
     if (lane >= o) x += y;
   }
+  __syncthreads();  // readers of the previous result in `s` are done
   if (lane == 31) s[w] = x;
   __syncthreads();
   if (w == 0) {
@@ -124,9 +125,9 @@ __device__ void tile_radix_sort(K* keys, V* vals, int n, int lo_bit,
       dig[i] = static_cast<unsigned char>(d & 0xff);
       const unsigned peers = __match_any_sync(kFull, d);
       int before = 0;
-      if (ok) before = cnt[d * W + w];
+      if (ok) before = cnt[w * D + d];
       __syncwarp();
-      if (ok && (peers & lt) == 0) cnt[d * W + w] = before + __popc(peers);
+      if (ok && (peers & lt) == 0) cnt[w * D + d] = before + __popc(peers);
       __syncwarp();
       rank[i] = static_cast<unsigned short>(before + __popc(peers & lt));
     }
@@ -139,7 +140,7 @@ __device__ void tile_radix_sort(K* keys, V* vals, int n, int lo_bit,
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int idx = threadIdx.x * PER + j;
-      local[j] = idx < D * W ? cnt[idx] : 0;
+      local[j] = idx < D * W ? cnt[(idx % W) * D + idx / W] : 0;
       sum += local[j];
     }
     int total;
@@ -147,7 +148,7 @@ __device__ void tile_radix_sort(K* keys, V* vals, int n, int lo_bit,
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int idx = threadIdx.x * PER + j;
-      if (idx < D * W) cnt[idx] = base;
+      if (idx < D * W) cnt[(idx % W) * D + idx / W] = base;
       base += local[j];
     }
     __syncthreads();
@@ -155,7 +156,7 @@ __device__ void tile_radix_sort(K* keys, V* vals, int n, int lo_bit,
     for (int i = 0; i < ITEMS; ++i) {
       const int pos = w * 32 * ITEMS + i * 32 + lane;
       if (pos < n) {
-        const int dst = cnt[dig[i] * W + w] + rank[i];
+        const int dst = cnt[w * D + dig[i]] + rank[i];
         keys[dst] = k[i];
         vals[dst] = v[i];
       }
@@ -188,9 +189,9 @@ __device__ void tile_pass_u32(unsigned int* items, int n, const DigitFn& digit, 
     const unsigned d = ok ? static_cast<unsigned>(digit(pos, k[i])) : D;
     const unsigned peers = __match_any_sync(kFull, d);
     int before = 0;
-    if (ok) before = cnt[d * W + w];
+    if (ok) before = cnt[w * D + d];
     __syncwarp();
-    if (ok && (peers & lt) == 0) cnt[d * W + w] = before + __popc(peers);
+    if (ok && (peers & lt) == 0) cnt[w * D + d] = before + __popc(peers);
     __syncwarp();
     const unsigned r = static_cast<unsigned>(before + __popc(peers & lt));
     if (i & 1) rk[i >> 1] |= r << 16;
@@ -203,7 +204,7 @@ __device__ void tile_pass_u32(unsigned int* items, int n, const DigitFn& digit, 
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int idx = threadIdx.x * PER + j;
-    local[j] = idx < D * W ? cnt[idx] : 0;
+    local[j] = idx < D * W ? cnt[(idx % W) * D + idx / W] : 0;
     sum += local[j];
   }
   int total;
@@ -211,7 +212,7 @@ __device__ void tile_pass_u32(unsigned int* items, int n, const DigitFn& digit, 
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int idx = threadIdx.x * PER + j;
-    if (idx < D * W) cnt[idx] = base;
+    if (idx < D * W) cnt[(idx % W) * D + idx / W] = base;
     base += local[j];
   }
   __syncthreads();
@@ -221,7 +222,7 @@ __device__ void tile_pass_u32(unsigned int* items, int n, const DigitFn& digit, 
     if (pos < n) {
       const unsigned d = static_cast<unsigned>(digit(pos, k[i]));
       const unsigned r = (i & 1) ? (rk[i >> 1] >> 16) : (rk[i >> 1] & 0xffffu);
-      items[cnt[d * W + w] + r] = k[i];
+      items[cnt[w * D + d] + r] = k[i];
     }
   }
   __syncthreads();

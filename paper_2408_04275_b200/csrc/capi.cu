@@ -1051,10 +1051,10 @@ dtb_status dtb_reorder_stream(dtb_context* ctx, const dtb_cost_model* cm, const 
   return sync_and_check(ctx);
 }
 
-dtb_status dtb_intra_stream_dev(dtb_context* ctx, int64_t bs, int32_t dp_lm, int32_t sort_order,
-                                const dtb_samples* samples, int64_t n_batches, int32_t* order_out,
-                                double* load_before, double* load_after, uint8_t* greedy_kept,
-                                void* stream) {
+static dtb_status intra_stream(dtb_context* ctx, int64_t bs, int32_t dp_lm, int32_t sort_order,
+                               const dtb_samples* samples, int64_t n_batches, int32_t* order_out,
+                               double* load_before, double* load_after, uint8_t* greedy_kept,
+                               unsigned long long* prof, void* stream) {
   TRY(set_device(ctx));
   if (dp_lm < 1) return fail(DTB_ERR_INTERNAL, "group count must be >= 1");
   if (bs < 1) return fail(DTB_ERR_INTERNAL, "cannot reorder an empty batch");
@@ -1080,9 +1080,28 @@ dtb_status dtb_intra_stream_dev(dtb_context* ctx, int64_t bs, int32_t dp_lm, int
   DBuf wide;
   CU(wide.alloc(fused_wide_scratch_bytes(n_batches), static_cast<cudaStream_t>(stream)));
   fa.wide_scratch = wide.as<unsigned char>();
+  fa.prof = prof;
   fa.err = ctx->err;
   CU(launch_intra_fused(fa, n_batches, static_cast<cudaStream_t>(stream)));
   return DTB_OK;
+}
+
+dtb_status dtb_intra_stream_dev(dtb_context* ctx, int64_t bs, int32_t dp_lm, int32_t sort_order,
+                                const dtb_samples* samples, int64_t n_batches, int32_t* order_out,
+                                double* load_before, double* load_after, uint8_t* greedy_kept,
+                                void* stream) {
+  return intra_stream(ctx, bs, dp_lm, sort_order, samples, n_batches, order_out, load_before,
+                      load_after, greedy_kept, nullptr, stream);
+}
+
+// Debug variant (not in the public header): per-batch phase timestamps
+// (globaltimer ns) of the fused kernel, prof_dev[n_batches][8].
+dtb_status dtb_debug_intra_stream_prof_dev(dtb_context* ctx, int64_t bs, int32_t dp_lm,
+                                           int32_t sort_order, const dtb_samples* samples,
+                                           int64_t n_batches, int32_t* order_out,
+                                           unsigned long long* prof_dev, void* stream) {
+  return intra_stream(ctx, bs, dp_lm, sort_order, samples, n_batches, order_out, nullptr,
+                      nullptr, nullptr, prof_dev, stream);
 }
 
 dtb_status dtb_disaggregated_reorder(dtb_context* ctx, const dtb_cost_model* cm,

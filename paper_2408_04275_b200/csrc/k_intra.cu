@@ -126,6 +126,12 @@ int fused_max_n() { return kFusedMaxN; }
 int fused_max_m() { return kWideMaxM; }
 size_t fused_wide_scratch_bytes(long long n_batches) { return kWidePerBatch * n_batches; }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Microbatch key of position pos (span == 1 stream layout [b][pg][dp_me]).
 __device__ __forceinline__ long long mb_index(const FusedArgs& a, long long b, int pos) {
   return (b * a.pg + pos % a.pg) * a.dp_me + pos / a.pg;
@@ -252,6 +258,7 @@ intra_fused_kernel(FusedArgs a) {
   const int pg = n / m;
   const bool desc = a.order == DTB_DESCENDING;
 
+  if (a.prof && tid == 0) a.prof[b * 8 + 0] = globaltimer();
   // ---- 1. per-sample cost (Sample::cost_size = 2 * modality tokens).  Each
   // warp streams a contiguous run of samples, 32 per step, with 8 steps of
   // independent offset loads in flight; identity block loads
@@ -325,6 +332,7 @@ intra_fused_kernel(FusedArgs a) {
   }
   bool keep = false;
   if (a.intra) {
+  if (a.prof && tid == 0) a.prof[b * 8 + 1] = globaltimer();
     // ---- 2. stable LSD radix sort by key over its varying bit window
     const unsigned varying = S.s_and ^ S.s_or;
     const int lo = varying ? __ffs(static_cast<int>(varying)) - 1 : 0;
@@ -336,6 +344,7 @@ intra_fused_kernel(FusedArgs a) {
           S.items, n, [&](int, unsigned it) { return ((it >> 16) >> sh) & mask; }, S.radix_cnt,
           S.tmp);
     }
+  if (a.prof && tid == 0) a.prof[b * 8 + 2] = globaltimer();
     // ---- 3. greedy equal-count partition (sizes = 2 * tokens)
     const int z0 = desc ? n - tot_zeros : 0;
     const int z1 = desc ? n : tot_zeros;
@@ -348,6 +357,7 @@ intra_fused_kernel(FusedArgs a) {
     auto assign = [&](int k, int g, int) { S.grp[k] = static_cast<unsigned char>(g); };
     GreedyState<long long> st{S.AL, S.AG, S.cnt, S.TL, S.TG, S.tmp, S.gload};
     greedy_rounds<kFusedT, 1, long long>(n, m, cap, z0, z1, size_at, assign, st);
+  if (a.prof && tid == 0) a.prof[b * 8 + 3] = globaltimer();
     // ---- 4. flat order = sorted items stably partitioned by group: the
     // items of a group keep assignment order (IntraPartition::flat).
     tile_pass_u32<kFusedT, kFusedItems, kRB>(
@@ -383,6 +393,7 @@ intra_fused_kernel(FusedArgs a) {
   if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
   for (int g = tid; g < m; g += kFusedT)
     write_outputs_common(a, b, g, S.blk_ident[g], keep ? S.blk_greedy[g] : S.blk_ident[g]);
+  if (a.prof && tid == 0) a.prof[b * 8 + 4] = globaltimer();
   // ---- 5. outputs: the intra order and the staged microbatch keys
   const int mb_span = a.pg * a.dp_me;
   if (keep) {
@@ -404,6 +415,10 @@ intra_fused_kernel(FusedArgs a) {
       if (a.staged_tok != nullptr) a.staged_tok[first + pos] = tok;
       if (a.mb_staged != nullptr && pos < mb_span) a.mb_staged[mb_index(a, b, pos)] = tok;
     }
+  }
+  if (a.prof) {
+    __syncthreads();
+    if (tid == 0) a.prof[b * 8 + 5] = globaltimer();
   }
 }
 

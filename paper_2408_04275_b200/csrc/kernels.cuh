@@ -33,6 +33,7 @@ struct FusedArgs {
   int* mb_orig;         // identity assembly, or null
   int* mb_staged;       // intra-ordered assembly, or null
   unsigned char* wide_scratch;  // [n_batches * fused_wide_scratch_bytes(1)]
+  unsigned long long* prof;     // optional [n_batches][8] phase timestamps (debug)
   DevErr* err;
 };
 

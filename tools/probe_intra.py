@@ -1,0 +1,80 @@
+"""Probe the fused intra kernel on the B200: per-phase timings (globaltimer
+stamps of CTA thread 0) over a stream, plus bit-exact spot checks of sampled
+batches against the oracle.  Debug tool; not part of the product path."""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batches", type=int, default=128)
+    ap.add_argument("--bs", type=int, default=16384)
+    ap.add_argument("--dp", type=int, default=128)
+    ap.add_argument("--check", type=int, default=4)
+    ap.add_argument("--order", type=int, default=0)
+    args = ap.parse_args()
+    import torch
+    from paper_2408_04275_b200 import _capi as A
+    from paper_2408_04275_b200 import native
+    from paper_2408_04275_b200.workload import synth_stream
+
+    pl = native.planner(0)
+    lib = pl.lib
+    fn = lib.lib.dtb_debug_intra_stream_prof_dev
+    fn.restype = C.c_int32
+    fn.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.POINTER(A.Samples), C.c_int64,
+                   C.c_void_p, C.c_void_p, C.c_void_p]
+    t0 = time.time()
+    s = synth_stream(args.batches * args.bs, seed=11, family="mixed")
+    print(f"synth {time.time() - t0:.1f}s", flush=True)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    d = [dev(s.image_offsets), dev(s.image_tokens), dev(s.audio_offsets), dev(s.audio_tokens)]
+    ds = A.Samples(s.n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32)) for x in d])
+    out = torch.empty(s.n, dtype=torch.int32, device="cuda")
+    prof = torch.zeros(args.batches * 8, dtype=torch.int64, device="cuda")
+    for it in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pl._check(fn(pl.ctx, args.bs, args.dp, args.order, C.byref(ds), args.batches,
+                     C.c_void_p(out.data_ptr()), C.c_void_p(prof.data_ptr()), None))
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"iter {it}: kernel {e0.elapsed_time(e1):.3f} ms", flush=True)
+    p = prof.view(args.batches, 8).cpu().numpy().astype(np.float64)
+    names = ["load+cost", "sort", "greedy", "partition+decide", "outputs"]
+    span = (p[:, 5] - p[:, 0]) / 1e3
+    print(f"per-CTA span us: median {np.median(span):.1f} max {span.max():.1f}")
+    for k, nm in enumerate(names):
+        dt = (p[:, k + 1] - p[:, k]) / 1e3
+        print(f"  {nm:18s} median {np.median(dt):8.1f} us  max {dt.max():8.1f}")
+    start = p[:, 0] - p[:, 0].min()
+    print(f"  CTA start spread: {start.max() / 1e3:.1f} us (waves)")
+    if args.check:
+        import oracle
+        import helpers as H
+        ora, kind = oracle.best()
+        model, cluster, book = H.desk_model(), H.desk_cluster(1172), H.desk_book()
+        co = ora.cost_model(model, cluster, book)
+        plan = H.plan((1, args.dp, 1), (1, args.dp, 2), (1, args.dp, 1), args.bs)
+        got = out.cpu().numpy().reshape(args.batches, args.bs)
+        rng = np.random.default_rng(0)
+        for bidx in sorted(rng.choice(args.batches, min(args.check, args.batches), replace=False)):
+            r = ora.disaggregated_reorder(co, plan, s.slice(bidx * args.bs, (bidx + 1) * args.bs),
+                                          inter=False, sort_order=args.order)
+            ok = np.array_equal(r.output_order, got[bidx])
+            print(f"  batch {bidx}: {'bit-exact' if ok else 'MISMATCH'} vs {kind}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
