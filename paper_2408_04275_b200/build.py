@@ -24,7 +24,9 @@ FLAGS = [
     "-Xptxas", "-v" if os.environ.get("DTB_PTXAS_V") else "-O3",
     "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
     "--expt-relaxed-constexpr",
-]
+] + [f"-D{d}" for d in os.environ.get("DTB_DEFINES", "").split() if d]
+if os.environ.get("DTB_DEFINES"):
+    OBJ = OBJ + "_" + "_".join(os.environ["DTB_DEFINES"].split()).replace("=", "")
 SOURCES = ["capi.cu", "k_intra.cu", "k_sched.cu", "k_inter.cu", "k_orch.cu", "k_misc.cu"]
 
 

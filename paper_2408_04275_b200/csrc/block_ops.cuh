@@ -48,6 +48,39 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s, int* total) {
   return r;
 }
 
+// Inclusive scan of one 64-bit integer per thread (exact: integer adds are
+// associative); *total gets the block sum.  `s` needs T/32 + 1 long longs.
+template <int T>
+__device__ __forceinline__ long long block_incl_scan_ll(long long v, long long* s,
+                                                        long long* total) {
+  constexpr int W = T / 32;
+  const int lane = lane_id(), w = warp_id();
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) s[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    long long t = lane < W ? s[lane] : 0;
+    long long u = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(kFull, u, o);
+      if (lane >= o) u += y;
+    }
+    if (lane < W) s[lane] = u - t;
+    if (lane == W - 1) s[W] = u;
+  }
+  __syncthreads();
+  const long long r = x + s[w];
+  *total = s[W];
+  return r;
+}
+
 // Block minimum of one int per thread (all threads get the result).
 template <int T>
 __device__ __forceinline__ int block_min(int v, int* s) {
@@ -165,6 +198,21 @@ __device__ void tile_radix_sort(K* keys, V* vals, int n, int lo_bit,
   }
 }
 
+// Lanes of the warp whose RB-bit digit equals this lane's, among lanes with
+// `ok` set: RB + 1 ballots instead of MATCH.ANY (a low-throughput
+// instruction; the ballots issue at full rate).
+template <int RB>
+__device__ __forceinline__ unsigned digit_peers(unsigned d, bool ok) {
+  unsigned peers = __ballot_sync(kFull, ok);
+#pragma unroll
+  for (int bit = 0; bit < RB; ++bit) {
+    const bool set = (d >> bit) & 1u;
+    const unsigned bal = __ballot_sync(kFull, set);
+    peers &= set ? bal : ~bal;
+  }
+  return peers;
+}
+
 // One stable counting pass over n <= T*ITEMS 32-bit items in place, digit
 // given by digit(pos, item) in [0, 1 << RB).  Same warp-striped ranking as
 // tile_radix_sort; used both for the cost-key passes (digit = key bits) and
@@ -180,14 +228,20 @@ __device__ void tile_pass_u32(unsigned int* items, int n, const DigitFn& digit, 
   static_assert(ITEMS % 2 == 0, "ranks are packed in pairs");
   unsigned int k[ITEMS];
   unsigned int rk[ITEMS / 2];  // two 16-bit ranks per register; digits recomputed
+  // all item loads first: the ranking chain below then only waits on the
+  // per-digit counters, not on item loads
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int pos = w * 32 * ITEMS + i * 32 + lane;
+    k[i] = pos < n ? items[pos] : 0u;
+  }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int pos = w * 32 * ITEMS + i * 32 + lane;
     const bool ok = pos < n;
-    k[i] = ok ? items[pos] : 0u;
-    const unsigned d = ok ? static_cast<unsigned>(digit(pos, k[i])) : D;
-    const unsigned peers = __match_any_sync(kFull, d);
+    const unsigned d = ok ? static_cast<unsigned>(digit(pos, k[i])) : 0u;
+    const unsigned peers = digit_peers<RB>(d, ok);
     int before = 0;
     if (ok) before = cnt[w * D + d];
     __syncwarp();

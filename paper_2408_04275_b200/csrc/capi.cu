@@ -952,6 +952,14 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   DBuf wide;
   CU(wide.alloc(fused_wide_scratch_bytes(n_batches), s));
   fa.wide_scratch = wide.as<unsigned char>();
+  DBuf tok16, wflag;
+  CU(tok16.alloc(2ull * total + 16, s));
+  CU(wflag.alloc(4ull * n_batches, s));
+  CU(launch_token_keys(io, it, ao, at, total, n, tok16.as<unsigned short>(),
+                       wflag.as<unsigned int>(), s));
+  fa.tok16 = tok16.as<unsigned short>();
+  fa.wide_flag = wflag.as<unsigned int>();
+  fa.div_pg = FastDiv::make(static_cast<unsigned>(per_group));
   fa.err = ctx->err;
   CU(launch_intra_fused(fa, n_batches, s));
   if (!direct) {
@@ -1080,6 +1088,19 @@ static dtb_status intra_stream(dtb_context* ctx, int64_t bs, int32_t dp_lm, int3
   DBuf wide;
   CU(wide.alloc(fused_wide_scratch_bytes(n_batches), static_cast<cudaStream_t>(stream)));
   fa.wide_scratch = wide.as<unsigned char>();
+  DBuf tok16, wflag;
+  const long long total = n_batches * bs;
+  CU(tok16.alloc(2ull * total + 16, static_cast<cudaStream_t>(stream)));
+  CU(wflag.alloc(4ull * n_batches, static_cast<cudaStream_t>(stream)));
+  CU(launch_token_keys(samples->image_offsets, samples->image_tokens, samples->audio_offsets,
+                       samples->audio_tokens, total, static_cast<int>(bs),
+                       tok16.as<unsigned short>(), wflag.as<unsigned int>(),
+                       static_cast<cudaStream_t>(stream)));
+  fa.tok16 = tok16.as<unsigned short>();
+  fa.wide_flag = wflag.as<unsigned int>();
+  fa.div_pg = FastDiv::make(static_cast<unsigned>(bs / dp_lm));
+  fa.pg = static_cast<int>(bs / dp_lm);
+  fa.dp_me = dp_lm;
   fa.prof = prof;
   fa.err = ctx->err;
   CU(launch_intra_fused(fa, n_batches, static_cast<cudaStream_t>(stream)));

@@ -62,6 +62,25 @@ __host__ __device__ __forceinline__ double smin(double a, double b) {
   return b < a ? b : a;
 }
 
+// Division by a runtime-invariant divisor 1 <= d < 2^31 for 0 <= n < 2^31
+// with one mul-hi (round-up method): q = (umulhi(n, mul) + n) >> shift.
+struct FastDiv {
+  unsigned d, mul, shift;
+  __host__ __device__ static FastDiv make(unsigned d) {
+    FastDiv f;
+    f.d = d;
+    f.shift = 0;
+    while ((1u << f.shift) < d) ++f.shift;
+    f.mul = static_cast<unsigned>(((1ull << 32) * ((1ull << f.shift) - d)) / d + 1);
+    return f;
+  }
+  __device__ __forceinline__ unsigned div(unsigned n) const {
+    const unsigned t = __umulhi(n, mul);
+    return (t + n) >> shift;
+  }
+  __device__ __forceinline__ unsigned mod(unsigned n) const { return n - div(n) * d; }
+};
+
 __host__ __device__ __forceinline__ int tp_index(int tp) {
   return tp == 1 ? 0 : tp == 2 ? 1 : tp == 4 ? 2 : tp == 8 ? 3 : -1;
 }

@@ -38,6 +38,7 @@ struct GreedyState {
   int* TG;    // [m]
   int* tmp;   // [T/32 + 2] reduction scratch
   L* gload;   // [m] final load per group id (null: not recorded)
+  long long* tmpll;  // [T/32 + 1] 64-bit scan scratch (ASC_INT fast path)
 };
 
 template <typename L>
@@ -48,12 +49,22 @@ __device__ __forceinline__ bool key_lt(L a, int ga, L b, int gb) {
 // Block-uniform greedy driver.  sizes(k): size of the k-th sorted item;
 // assign(k, g, slot): record the assignment.  Items [z0, z1) are the zero run
 // (size == 0).  m <= T * E_MAX.
-template <int T, int E_MAX, typename L, typename SizeFn, typename AssignFn>
+//
+// ASC_INT: integer sizes in ascending order.  Then a full round keeps A's
+// order automatically: L_j <= L_j+1 and s_j <= s_j+1 give
+// L_j + s_j <= L_j+1 + s_j+1, with equality only if both loads were equal
+// (so g_j < g_j+1 still orders them) — integer adds are exact.  Only
+// condition (b), newkey_0 > A[r-1], remains, and because integer sums are
+// associative it is evaluated for all speculative rounds at once from two
+// block-wide prefix scans (columns 0 and r-1), not by one thread per round.
+template <int T, int E_MAX, typename L, bool ASC_INT = false, typename SizeFn,
+          typename AssignFn>
 __device__ void greedy_rounds(int n, int m, int cap, int z0, int z1,
                               const SizeFn& sizes, const AssignFn& assign,
                               GreedyState<L> st) {
   const int tid = threadIdx.x;
-  const int E = (m + T - 1) / T;  // entries per thread (blocked)
+  constexpr int E = E_MAX;  // entries per thread (blocked; compile-time so
+                            // per-entry arrays stay in registers)
   for (int j = tid; j < m; j += T) {
     st.AL[j] = L(0);
     st.AG[j] = j;
@@ -122,7 +133,55 @@ __device__ void greedy_rounds(int n, int m, int cap, int z0, int z1,
       }
       room = block_min<T>(room, st.tmp);
       const int T_rounds = r > 0 ? min(room, (lim - k) / r) : 0;
-      if (T_rounds >= 1) {
+      if (ASC_INT && T_rounds >= 1) {
+        int tstar = T_rounds;
+        if (r >= 2) {
+          const long long l0 = static_cast<long long>(st.AL[0]);
+          const long long ll = static_cast<long long>(st.AL[r - 1]);
+          const int g0 = st.AG[0], gl = st.AG[r - 1];
+          long long c0 = 0, cl = 0;  // column sums of earlier chunks
+          for (int t0 = 0; t0 < T_rounds; t0 += T) {
+            const int t = t0 + tid;
+            const bool ok = t < T_rounds;
+            const long long s0 = ok ? static_cast<long long>(sizes(k + t * r)) : 0;
+            const long long sl = ok ? static_cast<long long>(sizes(k + t * r + r - 1)) : 0;
+            long long tot0, totl;
+            const long long inc0 = block_incl_scan_ll<T>(s0, st.tmpll, &tot0);
+            const long long incl = block_incl_scan_ll<T>(sl, st.tmpll, &totl);
+            // round t: newkey_0 = L0 + sum_{t'<=t} s0, A[r-1] = Llast + sum_{t'<t} sl
+            const long long new0 = l0 + c0 + inc0;
+            const long long last = ll + cl + (incl - sl);
+            const int f = ok && !key_lt(last, gl, new0, g0) ? t : 0x7fffffff;
+            const int first = block_min<T>(f, st.tmp);
+            if (first != 0x7fffffff) {
+              tstar = first;
+              break;
+            }
+            c0 += tot0;
+            cl += totl;
+          }
+        }
+        if (tstar > 0) {
+          for (int e = 0; e < E; ++e) {
+            const int j = tid * E + e;
+            if (j >= r) break;
+            const int g = st.AG[j];
+            const int cs = st.cnt[g];
+            L l = st.AL[j];
+#pragma unroll 4
+            for (int t = 0; t < tstar; ++t) {
+              const int item = k + t * r + j;
+              l = l + sizes(item);
+              assign(item, g, cs + t);
+            }
+            st.AL[j] = l;
+            st.cnt[g] = cs + tstar;
+          }
+          k += tstar * r;
+          __syncthreads();
+          continue;
+        }
+      } else if (T_rounds >= 1) {
         int fail = T_rounds;
         // columns owned: j = tid*E .. tid*E+E-1 plus j+1 for the pair check
         for (int e = 0; e < E; ++e) {

@@ -99,6 +99,9 @@ constexpr int kFusedMaxN = kFusedT * kFusedItems;  // 16384 samples per batch
 constexpr int kNarrowMaxM = 128;                    // groups in the smem path
 constexpr int kWideMaxM = 512;                      // groups in the global path
 constexpr int kRB = 7;                              // radix digit bits
+#ifndef DTB_FUSED_MIN_BLOCKS
+#define DTB_FUSED_MIN_BLOCKS 2  // two CTAs per SM (64 registers per thread)
+#endif
 
 // Narrow (shared-memory) state, ~102 KB so two CTAs share an SM.
 //   items[k] = (key << 16) | sample index, key = modality tokens (asc) or
@@ -134,7 +137,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Microbatch key of position pos (span == 1 stream layout [b][pg][dp_me]).
 __device__ __forceinline__ long long mb_index(const FusedArgs& a, long long b, int pos) {
-  return (b * a.pg + pos % a.pg) * a.dp_me + pos / a.pg;
+  const unsigned qd = a.div_pg.div(static_cast<unsigned>(pos));
+  return (b * a.pg + (static_cast<unsigned>(pos) - qd * a.pg)) * a.dp_me + qd;
 }
 
 __device__ __forceinline__ void write_outputs_common(const FusedArgs& a, long long b, int g,
@@ -209,7 +213,11 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
     auto assign = [&](int k, int g, int sl) {
       asg[k] = (static_cast<unsigned>(g) << 16) | static_cast<unsigned>(sl);
     };
-    greedy_rounds<kFusedT, 1, long long>(n, m, cap, z0, z1, size_at, assign, st);
+    st.tmpll = S.tmpll;
+    if (desc)
+      greedy_rounds<kFusedT, 1, long long, false>(n, m, cap, z0, z1, size_at, assign, st);
+    else
+      greedy_rounds<kFusedT, 1, long long, true>(n, m, cap, z0, z1, size_at, assign, st);
     int pre_local = tid < m ? st.cnt[tid] : 0;
     int total;
     const int pre = block_excl_scan<kFusedT>(pre_local, S.tmp, &total);
@@ -247,7 +255,7 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
   }
 }
 
-__global__ void __launch_bounds__(kFusedT, 2)
+__global__ void __launch_bounds__(kFusedT, DTB_FUSED_MIN_BLOCKS)
 intra_fused_kernel(FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw);
@@ -259,11 +267,14 @@ intra_fused_kernel(FusedArgs a) {
   const bool desc = a.order == DTB_DESCENDING;
 
   if (a.prof && tid == 0) a.prof[b * 8 + 0] = globaltimer();
-  // ---- 1. per-sample cost (Sample::cost_size = 2 * modality tokens).  Each
-  // warp streams a contiguous run of samples, 32 per step, with 8 steps of
-  // independent offset loads in flight; identity block loads
-  // (block_group_loads of the incoming order) are warp-reduced when a step's
-  // 32 samples share a block.
+  // ---- 1. token keys of the batch from the cost pass: 8 samples per
+  // 128-bit load, all loads issued before use.  cost_size = 2 * tokens.
+  // Batches with a saturated token (or outside the 16-bit layout's limits)
+  // take the 32-bit path straight from the CSR.
+  if (a.wide_flag[b] || m > kNarrowMaxM || n > kFusedMaxN || (n & 7)) {
+    fused_wide(a, b, S);
+    return;
+  }
   for (int g = tid; g < m; g += kFusedT) S.blk_ident[g] = 0ull;
   if (tid == 0) {
     S.s_and = ~0u;
@@ -272,64 +283,53 @@ intra_fused_kernel(FusedArgs a) {
   __syncthreads();
   unsigned int kand = ~0u, kor = 0u;
   int zeros = 0;
-  int maxtok = 0;
-  constexpr int U = 4;
-  const int per_warp = (n + (kFusedT / 32) - 1) / (kFusedT / 32);
-  const int w_lo = w * per_warp;
-  const int w_hi = min(n, w_lo + per_warp);
-  for (int s0 = w_lo; s0 < w_hi; s0 += 32 * U) {
-    int ib[U], ie[U], ab[U], ae[U];
+  {
+    constexpr int V = kFusedMaxN / 8 / kFusedT;  // 128-bit loads per thread
+    const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
+    const int nv = n >> 3;
+    uint4 q[V];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = s0 + u * 32 + lane;
-      const bool ok = i < w_hi;
-      ib[u] = ok ? __ldg(a.img_off + first + i) : 0;
-      ie[u] = ok ? __ldg(a.img_off + first + i + 1) : 0;
-      ab[u] = ok && a.aud_off ? __ldg(a.aud_off + first + i) : 0;
-      ae[u] = ok && a.aud_off ? __ldg(a.aud_off + first + i + 1) : 0;
+    for (int v = 0; v < V; ++v) {
+      const int idx = tid + v * kFusedT;
+      q[v] = idx < nv ? __ldg(src + idx) : make_uint4(0, 0, 0, 0);
     }
+    const int mb_span = a.pg * a.dp_me;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = s0 + u * 32 + lane;
-      const bool ok = i < w_hi;
-      long long t = 0;
-      for (int x = ib[u]; x < ie[u]; ++x) t += __ldg(a.img_tok + x);
-      for (int x = ab[u]; x < ae[u]; ++x) t += __ldg(a.aud_tok + x);
-      // identity block loads: warp-reduce when all 32 samples share a block
-      const int blk = ok ? min(i / pg, m - 1) : -1;
-      const long long cost = ok ? t + t : 0;
-      const int blk0 = __shfl_sync(kFull, blk, 0);
-      if (__all_sync(kFull, blk == blk0 || blk < 0)) {
-        long long sum = cost;
+    for (int v = 0; v < V; ++v) {
+      const int idx = tid + v * kFusedT;
+      if (idx >= nv) break;
+      const unsigned words[4] = {q[v].x, q[v].y, q[v].z, q[v].w};
+      const int i0 = idx * 8;
+      const unsigned blk0 = min(a.div_pg.div(static_cast<unsigned>(i0)), static_cast<unsigned>(m - 1));
+      const unsigned blk7 = min(a.div_pg.div(static_cast<unsigned>(i0 + 7)), static_cast<unsigned>(m - 1));
+      unsigned long long run = 0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
-        if (lane == 0 && blk0 >= 0) atomicAdd(&S.blk_ident[blk0], static_cast<unsigned long long>(sum));
-      } else if (ok) {
-        atomicAdd(&S.blk_ident[blk], static_cast<unsigned long long>(cost));
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j;
+        const unsigned tok = (words[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        const unsigned key = desc ? 0x7fffu - tok : tok;
+        kand &= key;
+        kor |= key;
+        zeros += tok == 0;
+        S.items[i] = (key << 16) | static_cast<unsigned>(i);
+        const unsigned qd = a.div_pg.div(static_cast<unsigned>(i));
+        if (blk0 == blk7) {
+          run += 2ull * tok;
+        } else {
+          atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2ull * tok);
+        }
+        if (a.orig_tok != nullptr) a.orig_tok[first + i] = static_cast<int>(tok);
+        if (a.mb_orig != nullptr && i < mb_span)
+          a.mb_orig[(b * a.pg + (static_cast<unsigned>(i) - qd * a.pg)) * a.dp_me + qd] =
+              static_cast<int>(tok);
       }
-      if (!ok) continue;
-      const int tok = t > 0x7fffffffll ? 0x7fffffff : (t < 0 ? 0x7fffffff : static_cast<int>(t));
-      maxtok = max(maxtok, tok);
-      const unsigned key = desc ? static_cast<unsigned>(0x7fff - min(tok, 0x7fff))
-                                : static_cast<unsigned>(min(tok, 0x7fff));
-      kand &= key;
-      kor |= key;
-      zeros += t == 0;
-      S.items[i] = (key << 16) | static_cast<unsigned>(i);
-      if (a.orig_tok != nullptr) a.orig_tok[first + i] = tok;
-      if (a.mb_orig != nullptr && i < a.pg * a.dp_me) a.mb_orig[mb_index(a, b, i)] = tok;
+      if (blk0 == blk7) atomicAdd(&S.blk_ident[blk0], run);
     }
   }
   atomicAnd(&S.s_and, kand);
   atomicOr(&S.s_or, kor);
-  const int tmax = block_min<kFusedT>(-maxtok, S.tmp);  // -max
   int tot_zeros;
   block_excl_scan<kFusedT>(zeros, S.tmp, &tot_zeros);
-  if (-tmax > 0x7fff || m > kNarrowMaxM || n > 65536) {
-    // costs beyond 16 bits (or too many groups) take the 32-bit path
-    fused_wide(a, b, S);
-    return;
-  }
   bool keep = false;
   if (a.intra) {
   if (a.prof && tid == 0) a.prof[b * 8 + 1] = globaltimer();
@@ -355,8 +355,11 @@ intra_fused_kernel(FusedArgs a) {
       return tok + tok;
     };
     auto assign = [&](int k, int g, int) { S.grp[k] = static_cast<unsigned char>(g); };
-    GreedyState<long long> st{S.AL, S.AG, S.cnt, S.TL, S.TG, S.tmp, S.gload};
-    greedy_rounds<kFusedT, 1, long long>(n, m, cap, z0, z1, size_at, assign, st);
+    GreedyState<long long> st{S.AL, S.AG, S.cnt, S.TL, S.TG, S.tmp, S.gload, S.tmpll};
+    if (desc)
+      greedy_rounds<kFusedT, 1, long long, false>(n, m, cap, z0, z1, size_at, assign, st);
+    else
+      greedy_rounds<kFusedT, 1, long long, true>(n, m, cap, z0, z1, size_at, assign, st);
   if (a.prof && tid == 0) a.prof[b * 8 + 3] = globaltimer();
     // ---- 4. flat order = sorted items stably partitioned by group: the
     // items of a group keep assignment order (IntraPartition::flat).
@@ -422,6 +425,68 @@ intra_fused_kernel(FusedArgs a) {
   }
 }
 
+// ------------------------------------------------------------ cost pass
+// Streaming pass over the CSR: 4 consecutive samples per thread; all offset
+// loads, then the first subsequences of every sample (predicated) are in
+// flight before any is consumed; one 8-byte store of four 16-bit keys.
+__global__ void __launch_bounds__(256)
+token_keys_kernel(const int* __restrict__ io, const int* __restrict__ it,
+                  const int* __restrict__ ao, const int* __restrict__ at, long long total,
+                  int n, unsigned short* __restrict__ tok16, unsigned int* __restrict__ flag) {
+  const long long g0 = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) * 4;
+  if (g0 >= total) return;
+  int ib[5], ab[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    ib[j] = g0 + j <= total ? __ldg(io + g0 + j) : 0;
+    ab[j] = ao != nullptr && g0 + j <= total ? __ldg(ao + g0 + j) : 0;
+  }
+  constexpr int KI = 3, KA = 1;
+  int tv[4][KI + KA];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int q = 0; q < KI; ++q) tv[j][q] = ib[j] + q < ib[j + 1] ? __ldg(it + ib[j] + q) : 0;
+#pragma unroll
+    for (int q = 0; q < KA; ++q) tv[j][KI + q] = ab[j] + q < ab[j + 1] ? __ldg(at + ab[j] + q) : 0;
+  }
+  unsigned short out[4];
+  bool wide = false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    long long t = 0;
+#pragma unroll
+    for (int q = 0; q < KI + KA; ++q) t += tv[j][q];
+    for (int x = ib[j] + KI; x < ib[j + 1]; ++x) t += __ldg(it + x);
+    for (int x = ab[j] + KA; x < ab[j + 1]; ++x) t += __ldg(at + x);
+    const bool valid = g0 + j < total;
+    if (valid && (t < 0 || t > 0x7fff)) wide = true;
+    out[j] = static_cast<unsigned short>(t < 0 || t > 0x7fff ? 0x7fff : t);
+  }
+  if (g0 + 3 < total) {
+    uint2 pk;
+    pk.x = static_cast<unsigned>(out[0]) | (static_cast<unsigned>(out[1]) << 16);
+    pk.y = static_cast<unsigned>(out[2]) | (static_cast<unsigned>(out[3]) << 16);
+    *reinterpret_cast<uint2*>(tok16 + g0) = pk;
+  } else {
+    for (int j = 0; j < 4 && g0 + j < total; ++j) tok16[g0 + j] = out[j];
+  }
+  if (wide) {
+    for (int j = 0; j < 4 && g0 + j < total; ++j) atomicOr(flag + (g0 + j) / n, 1u);
+  }
+}
+
+cudaError_t launch_token_keys(const int* io, const int* it, const int* ao, const int* at,
+                              long long total, int n, unsigned short* tok16, unsigned int* flag,
+                              cudaStream_t stream) {
+  cudaMemsetAsync(flag, 0, sizeof(unsigned int) * ((total + n - 1) / n), stream);
+  const long long threads = (total + 3) / 4;
+  if (threads > 0)
+    token_keys_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(
+        io, it, ao, at, total, n, tok16, flag);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- host glue
 cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches, cudaStream_t stream) {
   static bool configured = false;
@@ -460,6 +525,7 @@ cudaError_t launch_intra_generic(const double* sizes, int n, int m, int order, i
   st.cnt = reinterpret_cast<int*>(take(sizeof(int) * m));
   st.tmp = reinterpret_cast<int*>(take(sizeof(int) * (kGenT / 32 + 2)));
   st.gload = nullptr;
+  st.tmpll = nullptr;
   const size_t used = static_cast<size_t>(p - static_cast<char*>(scratch));
   if (used > scratch_bytes) return cudaErrorMemoryAllocation;
   const int grid = (n + kGenT - 1) / kGenT;

@@ -34,8 +34,21 @@ struct FusedArgs {
   int* mb_staged;       // intra-ordered assembly, or null
   unsigned char* wide_scratch;  // [n_batches * fused_wide_scratch_bytes(1)]
   unsigned long long* prof;     // optional [n_batches][8] phase timestamps (debug)
+  // Output of the cost pass (launch_token_keys): modality tokens per sample,
+  // saturated to 0x7fff, and a per-batch flag set when any sample saturated
+  // (that batch then takes the 32-bit path from the CSR).
+  const unsigned short* tok16;
+  const unsigned int* wide_flag;
+  FastDiv div_pg;
   DevErr* err;
 };
+
+// Cost pass: tok16[i] = min(modality tokens of sample i, 0x7fff) for the
+// whole stream, wide_flag[i / n] |= 1 on saturation or negative tokens.
+cudaError_t launch_token_keys(const int* img_off, const int* img_tok, const int* aud_off,
+                              const int* aud_tok, long long total, int n,
+                              unsigned short* tok16, unsigned int* wide_flag,
+                              cudaStream_t stream);
 
 size_t fused_wide_scratch_bytes(long long n_batches);
 size_t fused_smem_bytes();
