@@ -3,17 +3,19 @@
 Workload: a 16,777,216-sample synthetic image+audio stream (variable
 resolution -> patch tokens, audio clips) in global batches of 16,384, plan
 DP_lm = DP_me = DP_mg = 128, PP 1/2/1 (l = 128 microbatches per pipeline), the
-reference's desk-shaped cost profile.  One step = `disaggregated_reorder`
-(src/reorder.cpp:319-396) over every global batch of the stream with
-ReorderMode{intra=true, inter=false}: per-sample cost, stable sort, greedy
-equal-count partition, keep-if-no-worse, group loads and both simulated
-iteration times — the sort/partition path the north_star's HBM target names.
-The full default mode (intra + inter) and the orchestration search
-(config 3) are measured too and reported under "modes".
+reference's desk-shaped cost profile (proj/tests/support/configs.hpp:79-102).
+One step = `disaggregated_reorder` (src/reorder.cpp:319-396) over every
+global batch of the stream with ReorderMode{intra=true, inter=false}:
+per-sample cost, stable sort, greedy equal-count partition, keep-if-no-worse,
+group loads and both simulated iteration times -- the sort/partition path
+the north_star's HBM target names.  The full default mode (intra + inter)
+and the orchestration search (BASELINE config 3) are measured too and
+reported under "modes" / "search".
 
 N GPUs (torchrun): the stream is split by global-batch range (strong
-scaling, fixed 16M total); no collective on the data path.  `value` = all
-samples / max-over-ranks device time.
+scaling, 16M total); no collective on the data path.  `value` = all
+samples / max-over-ranks device time.  "gather" additionally times an NCCL
+all-gather of every rank's output orders (the concatenated ordering).
 
 --impl reference: the reference's own CPU implementation (oracle/_ref,
 compiled from the reference sources; the C restatement if absent) on all
@@ -39,6 +41,7 @@ BS = 16384
 DP = 128
 STREAM = 1 << 24
 METRIC = "reordered samples/s (disaggregated_reorder, 16M-sample stream, BS 16K, DP 128)"
+LAUNCHES_INTRA_STEP = 7  # token_keys, intra_fused, cost_table, 2x group_sims, 2x t_iter_reduce
 
 
 def parse():
@@ -48,17 +51,17 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--samples", type=int, default=STREAM)
-    ap.add_argument("--no-extras", action="store_true", help="skip modes/e2e/cpu legs")
+    ap.add_argument("--no-extras", action="store_true", help="skip modes/e2e/cpu/search legs")
     return ap.parse_args()
 
 
-def dist_init(n):
+def dist_init():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        import torch.distributed as dist
         import torch
+        import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
@@ -87,12 +90,20 @@ def workload():
     return model, cluster, book, plan
 
 
+def search_workload():
+    """BASELINE config 3: 72B MLLM on 1172 A800-like GPUs, BS 1920."""
+    import helpers as H
+    from paper_2408_04275_b200.api import stats_to_c
+    model = H.mllm72b_model()
+    return model, H.a800_cluster(1172), H.mllm72b_book(), 1920, stats_to_c(model.seq_len, 2048.0,
+                                                                          2048.0)
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region."""
 
     def __init__(self, idx):
-        self.idx = idx
-        self.proc = None
+        self.idx, self.proc = idx, None
         self.path = f"/tmp/dtb_clocks_{os.getpid()}.csv"
 
     def __enter__(self):
@@ -102,14 +113,16 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.2)
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.1)
             self.proc.terminate()
             self.proc.wait()
 
@@ -120,24 +133,23 @@ class Clocks:
             return None
         if not rows:
             return None
-        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        num = lambda s: float(s) if s.strip().replace(".", "").isdigit() else None
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in rows if len(r) > 1 and num(r[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4)
                           if len(r) > 3 + k and r[3 + k].strip() == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
 def cpu_reference(samples, plan_c, mode, n_batches, steps, warmup, threads, cm):
-    """Reference CPU path (all host threads) on n_batches global batches."""
+    """The reference's own disaggregated_reorder (oracle/_ref) over n_batches
+    global batches, fanned out over `threads` host threads.  Samples are
+    converted to std::vector<Sample> outside the timed region."""
     import oracle
-    from paper_2408_04275_b200 import _capi as A
     pl, kind = oracle.best()
     lib = pl.lib
-    if not lib.has("stream_prepare"):
-        raise RuntimeError("oracle lacks stream entry points")
     sub = samples.slice(0, n_batches * BS)
     s = sub.to_c()
     h = C.c_void_p()
@@ -155,44 +167,75 @@ def cpu_reference(samples, plan_c, mode, n_batches, steps, warmup, threads, cm):
     return kind, times
 
 
+def cpu_search(threads):
+    """model_orchestration on the reference (multi-threaded fan-out)."""
+    import oracle
+    from paper_2408_04275_b200 import _capi as A
+    pl, kind = oracle.best()
+    model, cluster, book, bs, stats = search_workload()
+    cm = pl.cost_model(model, cluster, book)
+    res = A.OrchestrationResult()
+    if pl.lib.has("model_orchestration_mt"):
+        pl.lib.set_threads(threads)
+        t0 = time.perf_counter()
+        pl._check(pl.lib.model_orchestration_mt(pl.ctx, cm.h, C.byref(stats), bs, 1, C.byref(res)))
+    else:
+        threads = 1
+        t0 = time.perf_counter()
+        pl._check(pl.lib.model_orchestration(pl.ctx, cm.h, C.byref(stats), bs, 1, C.byref(res),
+                                             None, 0))
+    dt = time.perf_counter() - t0
+    return kind, threads, res.candidates_evaluated / dt, dt, res
+
+
+def traffic_from_profiles():
+    """dram bytes per launch of the sort/partition kernels from the committed
+    ncu --set full summary (profiles/), if present."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return d
+    except Exception:
+        return None
+
+
+def reference_arm(args, model, cluster, book, plan_c):
+    from paper_2408_04275_b200 import _capi as A
+    from paper_2408_04275_b200.workload import synth_stream
+    threads = os.cpu_count() or 1
+    n_total = args.samples // BS
+    sample_batches = max(1, min(n_total, 2 * threads))
+    samples = synth_stream(sample_batches * BS, seed=1000, family="mixed")
+    kind, times = cpu_reference(samples, plan_c, A.ReorderMode(1, 0, 0), sample_batches,
+                                max(1, min(args.steps, 3)), min(args.warmup, 1), threads,
+                                (model, cluster, book))
+    t = float(np.median(times))
+    v = sample_batches * BS / t
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": len(times), "warmup": min(args.warmup, 1),
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64 tokens / f64 loads and stage times",
+            "data": "synthetic (PCG64 mixed image+audio stream)",
+            "config": {"workload": "BASELINE config 4: global batch 16384, DP 128, PP 1/2/1, "
+                                   "ReorderMode{intra} (bounded CPU sample of the stream)",
+                       "global_batch": BS, "dp": DP, "sample_batches": sample_batches},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": kind,
+                             "sample": f"{sample_batches} global batches x {BS} samples, "
+                                       f"std::thread fan-out over batches"},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
 def main():
     args = parse()
-    rank, world, local = dist_init(args.gpus)
+    rank, world, local = dist_init()
     model, cluster, book, plan = workload()
     from paper_2408_04275_b200 import _capi as A
     from paper_2408_04275_b200.workload import synth_stream
 
-    n_batches_total = args.samples // BS
-    my_batches = n_batches_total // world + (1 if rank < n_batches_total % world else 0)
-    first_batch = rank * (n_batches_total // world) + min(rank, n_batches_total % world)
     plan_c = plan.to_c()
-    mode_intra = A.ReorderMode(1, 0, 0)
-    mode_both = A.ReorderMode(1, 1, 0)
-
     if args.impl == "reference":
-        if rank != 0:
-            return
-        threads = os.cpu_count() or 1
-        sample_batches = max(1, min(n_batches_total, 4 * threads))
-        samples = synth_stream(sample_batches * BS, seed=1, family="mixed")
-        kind, times = cpu_reference(samples, plan_c, mode_intra, sample_batches, args.steps,
-                                    args.warmup, threads, (model, cluster, book))
-        t = float(np.median(times))
-        v = sample_batches * BS / t
-        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
-               "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-               "vs_baseline": None, "dtype": "int32/int64 keys, f64 costs",
-               "data": "synthetic (PCG64 mixed image+audio stream)",
-               "config": {"workload": "BASELINE config 4 (bounded CPU sample)",
-                          "global_batch": BS, "dp": DP, "pp": "1/2/1",
-                          "mode": "intra", "sample_batches": sample_batches},
-               "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads,
-                                "kind": kind,
-                                "sample": f"{sample_batches} global batches x {BS}"},
-               "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": 0}}
-        print(json.dumps(out))
+        if rank == 0:
+            print(json.dumps(reference_arm(args, model, cluster, book, plan_c)), flush=True)
         return
 
     import torch
@@ -201,38 +244,36 @@ def main():
     pl = native.planner(local)
     lib = pl.lib
     cm = pl.cost_model(model, cluster, book)
+    mode_intra, mode_both = A.ReorderMode(1, 0, 0), A.ReorderMode(1, 1, 0)
 
+    n_batches_total = args.samples // BS
+    my_batches = n_batches_total // world + (1 if rank < n_batches_total % world else 0)
+    first_batch = rank * (n_batches_total // world) + min(rank, n_batches_total % world)
     samples = synth_stream(my_batches * BS, seed=1000 + first_batch, family="mixed")
     n = samples.n
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    d_io, d_it = dev(samples.image_offsets), dev(samples.image_tokens)
-    d_ao, d_at = dev(samples.audio_offsets), dev(samples.audio_tokens)
-    ds = A.Samples(n, None, C.cast(d_io.data_ptr(), C.POINTER(C.c_int32)),
-                   C.cast(d_it.data_ptr(), C.POINTER(C.c_int32)),
-                   C.cast(d_ao.data_ptr(), C.POINTER(C.c_int32)),
-                   C.cast(d_at.data_ptr(), C.POINTER(C.c_int32)))
+    d_csr = [dev(samples.image_offsets), dev(samples.image_tokens), dev(samples.audio_offsets),
+             dev(samples.audio_tokens)]
+    ds = A.Samples(n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32)) for x in d_csr])
     out_order = torch.empty(n, dtype=torch.int32, device="cuda")
     lb = torch.empty(my_batches * DP, dtype=torch.float64, device="cuda")
     la = torch.empty_like(lb)
     tb = torch.empty(my_batches, dtype=torch.float64, device="cuda")
     ta = torch.empty_like(tb)
     kept = torch.empty(my_batches, dtype=torch.uint8, device="cuda")
-    # L2 flush buffer (inputs are > L2 anyway at full size; flush keeps it honest)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2 (126 MB)
     stream = torch.cuda.Stream()
     sh = C.c_void_p(stream.cuda_stream)
+    ptr = lambda t: C.c_void_p(t.data_ptr())
 
     def step(mode):
         pl._check(lib.reorder_stream_dev(pl.ctx, cm.h, C.byref(plan_c), C.byref(mode), C.byref(ds),
-                                         my_batches, C.c_void_p(out_order.data_ptr()),
-                                         C.c_void_p(lb.data_ptr()), C.c_void_p(la.data_ptr()),
-                                         C.c_void_p(tb.data_ptr()), C.c_void_p(ta.data_ptr()),
-                                         C.c_void_p(kept.data_ptr()), sh))
+                                         my_batches, ptr(out_order), ptr(lb), ptr(la), ptr(tb),
+                                         ptr(ta), ptr(kept), sh))
 
-    def k1():
+    def sort_partition():
         pl._check(lib.intra_stream_dev(pl.ctx, BS, DP, 0, C.byref(ds), my_batches,
-                                       C.c_void_p(out_order.data_ptr()), C.c_void_p(lb.data_ptr()),
-                                       C.c_void_p(la.data_ptr()), C.c_void_p(kept.data_ptr()), sh))
+                                       ptr(out_order), ptr(lb), ptr(la), ptr(kept), sh))
 
     def timed(fn, steps, warmup):
         for _ in range(warmup):
@@ -252,56 +293,135 @@ def main():
         torch.cuda.synchronize()
         barrier(world)
         torch.cuda.synchronize()
-        ms = [s.elapsed_time(e) for s, e in evs]
-        return float(np.mean(ms)), ms
+        return float(np.mean([s.elapsed_time(e) for s, e in evs]))
 
     with Clocks(local) as clk:
-        ms_local, _ = timed(lambda: step(mode_intra), args.steps, args.warmup)
+        ms_local = timed(lambda: step(mode_intra), args.steps, args.warmup)
     ms = max_over_ranks(ms_local, world)
     total = n_batches_total * BS
-    value = total / (ms / 1e3)
-    out = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+    out = {"metric": METRIC, "value": total / (ms / 1e3), "unit": "samples/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-           "dtype": "int32 tokens / int64 loads / f64 stage times",
-           "data": "synthetic (PCG64 mixed image+audio stream, random-free desk cost profile)",
+           "dtype": "int32 tokens / int64 loads / f64 stage times (u16 sort keys)",
+           "data": "synthetic (PCG64 mixed image+audio stream; desk-shaped cost profile)",
            "config": {"workload": "BASELINE config 4: 16M-sample stream, global batch 16384, "
-                                  "DP 128, PP 1/2/1, ReorderMode{intra}",
+                                  "DP 128, PP 1/2/1, disaggregated_reorder ReorderMode{intra}",
                       "samples": total, "global_batch": BS, "dp": DP,
-                      "parallelism": f"batch-range sharding over {world} GPU(s)",
-                      "l2": "256 MiB flush written between timed steps; inputs > L2"},
-           "gpu_launches": 8 * 1}
+                      "parallelism": f"global-batch-range sharding over {world} GPU(s), "
+                                     "no data-path collective",
+                      "l2": "256 MiB buffer written between timed steps (inputs also > L2)"},
+           "gpu_launches": LAUNCHES_INTRA_STEP}
     clocks = clk.summary()
     if clocks:
         out["clocks"] = clocks
 
-    # ---- dominant kernel (sort/partition) roofline
-    k1_ms_local, _ = timed(k1, args.steps, args.warmup)
-    k1_ms = max_over_ranks(k1_ms_local, world)
+    # ---- roofline of the sort/partition path (cost pass + fused partition)
+    sp_local = timed(sort_partition, args.steps, args.warmup)
     n_img, n_aud = len(samples.image_tokens), len(samples.audio_tokens)
-    algo_bytes = (4 * 2 * (n + my_batches) + 4 * (n_img + n_aud)  # offsets + tokens
-                  + 4 * n + 2 * 8 * DP * my_batches + my_batches)  # order + loads + kept
+    algo = (4 * 2 * (n + my_batches) + 4 * (n_img + n_aud)   # CSR offsets + tokens in
+            + 4 * n + 2 * 8 * DP * my_batches + my_batches)  # order + both loads + kept out
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     hbm = peaks.get("hbm_gbs", 6650.0)
-    achieved = algo_bytes / (k1_ms_local / 1e3) / 1e9
-    out["roofline"] = {"bound": "hbm", "kernel": "intra_fused_kernel", "achieved": achieved,
-                       "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                       "algorithmic_bytes_per_launch": algo_bytes,
-                       "ms_per_launch": k1_ms_local,
-                       "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
+    achieved = algo / (sp_local / 1e3) / 1e9
+    tr = traffic_from_profiles()
+    out["roofline"] = {
+        "bound": "hbm", "kernel": "token_keys_kernel + intra_fused_kernel (sort/partition path)",
+        "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+        "traffic": (tr["bytes_per_launch_16M"] * my_batches / n_batches_total) if tr else None,
+        "algorithmic_bytes_per_launch": algo, "ms_per_launch": sp_local,
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650"}
 
-    if not args.no_extras and rank == 0:
+    if world > 1:
+        # concatenated ordering on every rank (NCCL all-gather over NVLink)
+        import torch.distributed as dist
+        full = torch.empty(n * world, dtype=torch.int32, device="cuda")
+        if n_batches_total % world == 0:
+            def gather():
+                step(mode_intra)
+                with torch.cuda.stream(stream):
+                    dist.all_gather_into_tensor(full, out_order)
+            g_ms = max_over_ranks(timed(gather, max(2, args.steps // 2), 1), world)
+            out["gather"] = {"ms_per_step": g_ms, "value": total / (g_ms / 1e3),
+                             "unit": "samples/s", "collective": "all_gather_into_tensor(int32)"}
+
+    if not args.no_extras and rank == 0 and world == 1:
         # full default mode (intra + inter)
-        both_ms, _ = timed(lambda: step(mode_both), max(2, args.steps // 3), 1)
+        both_ms = timed(lambda: step(mode_both), max(2, args.steps // 3), 1)
         out["modes"] = {"intra+inter": {"ms_per_step": both_ms,
-                                        "value": my_batches * BS / (both_ms / 1e3)}}
-    out["gpu_launches"] = 8
+                                        "value": my_batches * BS / (both_ms / 1e3),
+                                        "unit": "samples/s"}}
+        # orchestration search, BASELINE config 3
+        smodel, scluster, sbook, sbs, sstats = search_workload()
+        scm = pl.cost_model(smodel, scluster, sbook)
+        res = A.OrchestrationResult()
+        for _ in range(2):
+            pl._check(lib.model_orchestration(pl.ctx, scm.h, C.byref(sstats), sbs, 1,
+                                              C.byref(res), None, 0))
+        reps = 5
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            pl._check(lib.model_orchestration(pl.ctx, scm.h, C.byref(sstats), sbs, 1,
+                                              C.byref(res), None, 0))
+        s_dt = (time.perf_counter() - t0) / reps
+        out["search"] = {"metric": "orchestration candidates/s (model_orchestration, 72B MLLM, "
+                                   "1172 GPUs, BS 1920)",
+                         "value": res.candidates_evaluated / s_dt, "unit": "candidates/s",
+                         "ms_per_search": s_dt * 1e3, "candidates": res.candidates_evaluated,
+                         "timing": "host wall clock around the C-ABI call (includes "
+                                   "enumeration, solve, reduce, D2H)"}
+        # e2e: host CSR (pinned) -> device -> result back, through the public C ABI
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_csr = [pin(samples.image_offsets), pin(samples.image_tokens),
+                 pin(samples.audio_offsets), pin(samples.audio_tokens)]
+        hs = A.Samples(n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32)) for x in h_csr])
+        h_order = torch.empty(n, dtype=torch.int32).pin_memory()
+        h_lb = torch.empty(my_batches * DP, dtype=torch.float64).pin_memory()
+        h_la = torch.empty_like(h_lb).pin_memory()
+        h_tb = torch.empty(my_batches, dtype=torch.float64).pin_memory()
+        h_ta = torch.empty_like(h_tb).pin_memory()
+        h_kept = torch.empty(my_batches, dtype=torch.uint8).pin_memory()
+        P = lambda t, ct: C.cast(t.data_ptr(), C.POINTER(ct))
+
+        def e2e():
+            pl._check(lib.reorder_stream(pl.ctx, cm.h, C.byref(plan_c), C.byref(mode_intra),
+                                         C.byref(hs), my_batches, P(h_order, C.c_int32),
+                                         P(h_lb, C.c_double), P(h_la, C.c_double),
+                                         P(h_tb, C.c_double), P(h_ta, C.c_double),
+                                         P(h_kept, C.c_uint8)))
+        e2e()
+        reps = max(3, args.steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e()
+        e_dt = (time.perf_counter() - t0) / reps
+        h2d = sum(x.numel() * x.element_size() for x in h_csr)
+        d2h = sum(x.numel() * x.element_size() for x in (h_order, h_lb, h_la, h_tb, h_ta, h_kept))
+        out["e2e"] = {"value": n / e_dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h, "ms_per_step": e_dt * 1e3,
+                      "path": "dtb_reorder_stream (host pointers, pinned)"}
+        # CPU baseline: the compiled reference on this host's cores
+        threads = os.cpu_count() or 1
+        sample_batches = max(1, min(my_batches, 2 * threads))
+        kind, times = cpu_reference(samples, plan_c, mode_intra, sample_batches, 2, 0, threads,
+                                    (model, cluster, book))
+        t = float(np.median(times))
+        out["cpu_baseline"] = {"value": sample_batches * BS / t, "unit": "samples/s",
+                               "cores": threads, "kind": kind,
+                               "sample": f"first {sample_batches} global batches of the stream "
+                                         f"(x{BS} samples), std::thread fan-out over batches"}
+        try:
+            kind_s, th_s, cps, s_cpu, _ = cpu_search(threads)
+            out["search"]["cpu_baseline"] = {"value": cps, "unit": "candidates/s",
+                                             "cores": th_s, "kind": kind_s,
+                                             "seconds": s_cpu}
+        except Exception as ex:  # pragma: no cover
+            out["search"]["cpu_baseline"] = {"error": str(ex)}
     if rank == 0:
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":

@@ -966,6 +966,16 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
     CU(launch_assemble(n_batches, n, dp_lm, dp_me, orig_tok.as<int>(), mb0.as<int>(), s));
     CU(launch_assemble(n_batches, n, dp_lm, dp_me, staged_tok.as<int>(), mb1.as<int>(), s));
   }
+  // token-indexed cost table shared by both simulations and the inter kernel
+  const int tsize = static_cast<int>(std::min<long long>(
+      static_cast<long long>(span) * 0x8000, static_cast<long long>(kCostTableMax)));
+  DBuf tab_e, tab_g, tab_k;
+  CU(tab_e.alloc(sizeof(double2) * tsize, s));
+  CU(tab_g.alloc(sizeof(double2) * tsize, s));
+  CU(tab_k.alloc(sizeof(double) * tsize, s));
+  CU(launch_cost_table(cm->dev, *plan, span, tsize, tab_e.as<double2>(), tab_g.as<double2>(),
+                       tab_k.as<double>(), ctx->err, s));
+  CostTable table{tab_e.as<double2>(), tab_g.as<double2>(), tab_k.as<double>(), tsize, span};
   GroupSimArgs ga{};
   ga.cm = cm->dev;
   ga.plan = *plan;
@@ -974,6 +984,7 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ga.l = per_group;
   ga.mbtok = mb0.as<int>();
   ga.span = span;
+  ga.table = table;
   CU(tgrp.alloc(8ull * n_batches * dp_me, s));
   ga.t_group = tgrp.as<double>();
   ga.busy = nullptr;
@@ -989,6 +1000,7 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ia.mbtok = mb1.as<int>();
   ia.groups = dp_me;
   ia.span = span;
+  ia.table = table;
   ia.err = ctx->err;
   const size_t inter_bytes = mode->inter ? inter_scratch(ia) : 0;
   CU(scr.alloc(std::max(sim_bytes, inter_bytes), s));

@@ -503,8 +503,17 @@ group_sims_fast(GroupSimArgs a) {
         c = cntp ? cntp[src] : a.span;
       }
       if (te < 0 || tg < 0) fault = E_NEG_LOAD;
-      ue.eval(mb_mean_fast(te, c), &rfE[0], &rbE[0]);
-      ug.eval(mb_mean_fast(tg, c), &rfG[0], &rbG[0]);
+      if (STREAM && te >= 0 && te < a.table.size) {
+        const double2 e2 = __ldg(a.table.enc + te);
+        const double2 g2 = __ldg(a.table.gen + te);
+        rfE[0] = e2.x;
+        rbE[0] = e2.y;
+        rfG[0] = g2.x;
+        rbG[0] = g2.y;
+      } else {
+        ue.eval(mb_mean_fast(te, c), &rfE[0], &rbE[0]);
+        ug.eval(mb_mean_fast(tg, c), &rfG[0], &rbG[0]);
+      }
     }
     // even tick 2i: F(i - s/2, s) on even s, B(i - P + (s+1)/2, s) on odd s
 #pragma unroll
@@ -627,6 +636,33 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
   } else {
     group_sims_kernel<<<grid, T, 0, stream>>>(a, static_cast<double*>(scratch));
   }
+  return cudaGetLastError();
+}
+
+// Token-indexed cost table (see CostTable): thread per token sum s.
+__global__ void cost_table_kernel(DevCM cm, dtb_plan plan, int span, int size, double2* enc,
+                                  double2* gen, double* key, DevErr* err) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= size) return;
+  UnitEval ue, ug;
+  ue.init(cm, plan, DTB_ENCODER);
+  ug.init(cm, plan, DTB_GENERATOR);
+  const double x = mb_mean_fast(s, span);
+  double f, b;
+  ue.eval(x, &f, &b);
+  enc[s] = make_double2(f, b);
+  ug.eval(x, &f, &b);
+  gen[s] = make_double2(f, b);
+  const int e = dev_fwd_key(cm, plan, x, x, &key[s]);
+  if (e) dev_fail(err, e);
+}
+
+cudaError_t launch_cost_table(const DevCM& cm, const dtb_plan& plan, int span, int size,
+                              double2* enc, double2* gen, double* key, DevErr* err,
+                              cudaStream_t stream) {
+  if (size <= 0) return cudaSuccess;
+  cost_table_kernel<<<(size + 255) / 256, 256, 0, stream>>>(cm, plan, span, size, enc, gen, key,
+                                                            err);
   return cudaGetLastError();
 }
 

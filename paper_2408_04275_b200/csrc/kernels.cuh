@@ -119,6 +119,23 @@ cudaError_t launch_unit_times(const DevCM& cm, int kind, int tp, long long n,
                               const double* loads, double* fwd, double* bwd,
                               DevErr* err, cudaStream_t stream);
 
+// Token-indexed cost table for the stream path: for every microbatch token
+// sum s in [0, size), the build_stage_times entries of the encoder and
+// generator units at load s / span, and microbatch_fwd_keys' key.  Each
+// entry is computed once with exactly the reference's operation sequence,
+// so a lookup is bit-identical to recomputing it.
+struct CostTable {
+  const double2* enc;  // (f, b) of the encoder unit
+  const double2* gen;  // (f, b) of the generator unit
+  const double* key;   // forward key
+  int size;            // sums >= size are evaluated directly
+  int span;
+};
+constexpr int kCostTableMax = 1 << 20;
+cudaError_t launch_cost_table(const DevCM& cm, const dtb_plan& plan, int span, int size,
+                              double2* enc, double2* gen, double* key, DevErr* err,
+                              cudaStream_t stream);
+
 // Makespans of coupled groups whose microbatches are given by token keys:
 // group g of batch b covers microbatches [g*l, (g+1)*l) of batch b.
 // t_group[b * groups + g] = iteration time; also device busy sums for the
@@ -138,6 +155,7 @@ struct GroupSimArgs {
   // tokens, count == span), so a warp of groups reads one coalesced row.
   const int* mbtok;
   const int* order;      // optional [n_batches][groups][l] microbatch order
+  CostTable table;       // optional (size 0 = evaluate directly)
   double* t_group;
   double* busy;
   DevErr* err;
@@ -160,6 +178,7 @@ struct InterArgs {
   const int* mbtok;
   int groups;
   int span;
+  CostTable table;       // optional (size 0 = evaluate directly)
   int* orders;           // [batch * l]
   DevErr* err;
 };
