@@ -901,7 +901,11 @@ static dtb_status stream_checks(const dtb_cost_model* cm, const dtb_plan* plan,
   return DTB_OK;
 }
 
-// Device pipeline for n_batches global batches (all pointers device).
+// Device pipeline for n_batches global batches (all pointers device):
+//   token_keys (cost pass) -> intra_fused (sort/greedy/decision, per batch)
+//   -> cost table -> group sims on the input order (t_iter_before)
+//   -> [inter_reorder per coupled group] -> compose -> group sims on the
+//   reordered groups (t_iter_after).
 static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan* plan,
                              const dtb_reorder_mode* mode, const int* io, const int* it,
                              const int* ao, const int* at, long long n_batches, int* order_out,
@@ -914,8 +918,7 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   const int span = dp_lm / dp_me;
   const long long n_mb = n_batches * dp_me * static_cast<long long>(per_group);
   const long long total = n_batches * static_cast<long long>(n);
-  const bool direct = span == 1;  // K1 writes microbatch keys itself
-  DBuf intra, orig_tok, staged_tok, mb0, mb1, tgrp, inter, scr;
+  DBuf intra, tok16, tok16s, tok32, tok32s, wflag, kept_buf, wide, mb0, mb1, tgrp, inter, scr;
   // without inter the intra order is the output order whenever every
   // position belongs to a microbatch
   const bool compose_needed = mode->inter || dp_me * span * per_group != n;
@@ -924,12 +927,19 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
     CU(intra.alloc(4ull * total, s));
     intra_out = intra.as<int>();
   }
-  CU(mb0.alloc(4ull * n_mb, s));
-  CU(mb1.alloc(4ull * n_mb, s));
-  if (!direct) {
-    CU(orig_tok.alloc(4ull * total, s));
-    CU(staged_tok.alloc(4ull * total, s));
+  unsigned char* kept_dev = kept;
+  if (kept_dev == nullptr) {
+    CU(kept_buf.alloc(n_batches, s));
+    kept_dev = kept_buf.as<unsigned char>();
   }
+  CU(tok16.alloc(2ull * total + 16, s));
+  CU(tok16s.alloc(2ull * total + 16, s));
+  CU(tok32.alloc(4ull * total, s));
+  CU(tok32s.alloc(4ull * total, s));
+  CU(wflag.alloc(4ull * n_batches, s));
+  CU(wide.alloc(fused_wide_scratch_bytes(n_batches), s));
+  CU(launch_token_keys(io, it, ao, at, total, n, tok16.as<unsigned short>(),
+                       wflag.as<unsigned int>(), s));
   FusedArgs fa{};
   fa.n = n;
   fa.m = dp_lm;
@@ -942,29 +952,25 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   fa.order_out = intra_out;
   fa.load_before = lb;
   fa.load_after = la;
-  fa.kept = kept;
-  fa.orig_tok = direct ? nullptr : orig_tok.as<int>();
-  fa.staged_tok = direct ? nullptr : staged_tok.as<int>();
+  fa.kept = kept_dev;
+  fa.tok16_staged = tok16s.as<unsigned short>();
+  fa.tok32_orig = tok32.as<int>();
+  fa.tok32_staged = tok32s.as<int>();
   fa.pg = per_group;
   fa.dp_me = dp_me;
-  fa.mb_orig = direct ? mb0.as<int>() : nullptr;
-  fa.mb_staged = direct ? mb1.as<int>() : nullptr;
-  DBuf wide;
-  CU(wide.alloc(fused_wide_scratch_bytes(n_batches), s));
   fa.wide_scratch = wide.as<unsigned char>();
-  DBuf tok16, wflag;
-  CU(tok16.alloc(2ull * total + 16, s));
-  CU(wflag.alloc(4ull * n_batches, s));
-  CU(launch_token_keys(io, it, ao, at, total, n, tok16.as<unsigned short>(),
-                       wflag.as<unsigned int>(), s));
   fa.tok16 = tok16.as<unsigned short>();
   fa.wide_flag = wflag.as<unsigned int>();
   fa.div_pg = FastDiv::make(static_cast<unsigned>(per_group));
   fa.err = ctx->err;
   CU(launch_intra_fused(fa, n_batches, s));
-  if (!direct) {
-    CU(launch_assemble(n_batches, n, dp_lm, dp_me, orig_tok.as<int>(), mb0.as<int>(), s));
-    CU(launch_assemble(n_batches, n, dp_lm, dp_me, staged_tok.as<int>(), mb1.as<int>(), s));
+  const TokSrc tok{tok16.as<unsigned short>(), tok16s.as<unsigned short>(), tok32.as<int>(),
+                   tok32s.as<int>(), kept_dev, wflag.as<unsigned int>(), n};
+  if (span > 1) {  // assembled microbatch sums [b][e][i]
+    CU(mb0.alloc(4ull * n_mb, s));
+    CU(mb1.alloc(4ull * n_mb, s));
+    CU(launch_assemble(n_batches, n, dp_lm, dp_me, tok, false, mb0.as<int>(), s));
+    CU(launch_assemble(n_batches, n, dp_lm, dp_me, tok, true, mb1.as<int>(), s));
   }
   // token-indexed cost table shared by both simulations and the inter kernel
   const int tsize = static_cast<int>(std::min<long long>(
@@ -982,7 +988,10 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ga.n_batches = n_batches;
   ga.groups = dp_me;
   ga.l = per_group;
-  ga.mbtok = mb0.as<int>();
+  ga.stream = true;
+  ga.tok = tok;
+  ga.staged = false;
+  ga.mbsum = span > 1 ? mb0.as<int>() : nullptr;
   ga.span = span;
   ga.table = table;
   CU(tgrp.alloc(8ull * n_batches * dp_me, s));
@@ -997,7 +1006,9 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ia.vpp = plan->vpp;
   ia.cm = cm->dev;
   ia.plan = *plan;
-  ia.mbtok = mb1.as<int>();
+  ia.stream = true;
+  ia.tok = tok;
+  ia.mbsum = span > 1 ? mb1.as<int>() : nullptr;
   ia.groups = dp_me;
   ia.span = span;
   ia.table = table;
@@ -1014,7 +1025,8 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   if (compose_needed)
     CU(launch_compose(n_batches, n, dp_lm, dp_me, intra_out, mode->inter ? inter.as<int>() : nullptr,
                       order_out, s));
-  ga.mbtok = mb1.as<int>();
+  ga.staged = true;
+  ga.mbsum = span > 1 ? mb1.as<int>() : nullptr;
   ga.order = mode->inter ? inter.as<int>() : nullptr;
   CU(launch_group_sims(ga, scr.p, s));
   CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, ta, s));

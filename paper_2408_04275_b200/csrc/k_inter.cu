@@ -384,7 +384,8 @@ __global__ void inter_kernel(InterArgs a, char* scratch, long long begin,
     const long long bb = prob / a.groups;
     const int grp = static_cast<int>(prob % a.groups);
     for (int i = 0; i < l && !e; ++i) {
-      const long long v = a.mbtok[(bb * l + i) * a.groups + grp];
+      const long long v = a.span == 1 ? a.tok.get(bb, grp * l + i, true)
+                                      : a.mbsum[(bb * a.groups + grp) * static_cast<long long>(l) + i];
       const double me = mb_mean(v, a.span);
       const double mg = me;
       StageRow r;

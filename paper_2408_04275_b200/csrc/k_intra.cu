@@ -188,7 +188,7 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
     kor |= key;
     zeros += c == 0;
     atomicAdd(&blk_i[min(i / pg, m - 1)], static_cast<unsigned long long>(c));
-    if (a.mb_orig != nullptr && i < a.pg * a.dp_me) a.mb_orig[mb_index(a, b, i)] = static_cast<int>(t);
+    if (a.tok32_orig != nullptr) a.tok32_orig[first + i] = static_cast<int>(t);
   }
   if (tid == 0) {
     S.s_and = ~0u;
@@ -240,7 +240,6 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
   const bool keep = a.intra && mg <= mi;
   if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
   for (int g = tid; g < m; g += kFusedT) write_outputs_common(a, b, g, blk_i[g], keep ? blk_g[g] : blk_i[g]);
-  const int mb_span = a.pg * a.dp_me;
   for (int k = tid; k < n; k += kFusedT) {
     const unsigned int key = keys[k];
     const int tok = static_cast<int>((desc ? ~key : key) >> 1);
@@ -250,8 +249,7 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
       pos = off[as >> 16] + static_cast<int>(as & 0xffffu);
     }
     a.order_out[first + pos] = keep ? vals[k] : pos;
-    if (a.staged_tok != nullptr) a.staged_tok[first + pos] = tok;
-    if (a.mb_staged != nullptr && pos < mb_span) a.mb_staged[mb_index(a, b, pos)] = tok;
+    if (a.tok32_staged != nullptr) a.tok32_staged[first + pos] = tok;
   }
 }
 
@@ -293,7 +291,6 @@ intra_fused_kernel(FusedArgs a) {
       const int idx = tid + v * kFusedT;
       q[v] = idx < nv ? __ldg(src + idx) : make_uint4(0, 0, 0, 0);
     }
-    const int mb_span = a.pg * a.dp_me;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int idx = tid + v * kFusedT;
@@ -312,16 +309,12 @@ intra_fused_kernel(FusedArgs a) {
         kor |= key;
         zeros += tok == 0;
         S.items[i] = (key << 16) | static_cast<unsigned>(i);
-        const unsigned qd = a.div_pg.div(static_cast<unsigned>(i));
         if (blk0 == blk7) {
           run += 2ull * tok;
         } else {
+          const unsigned qd = a.div_pg.div(static_cast<unsigned>(i));
           atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2ull * tok);
         }
-        if (a.orig_tok != nullptr) a.orig_tok[first + i] = static_cast<int>(tok);
-        if (a.mb_orig != nullptr && i < mb_span)
-          a.mb_orig[(b * a.pg + (static_cast<unsigned>(i) - qd * a.pg)) * a.dp_me + qd] =
-              static_cast<int>(tok);
       }
       if (blk0 == blk7) atomicAdd(&S.blk_ident[blk0], run);
     }
@@ -397,27 +390,19 @@ intra_fused_kernel(FusedArgs a) {
   for (int g = tid; g < m; g += kFusedT)
     write_outputs_common(a, b, g, S.blk_ident[g], keep ? S.blk_greedy[g] : S.blk_ident[g]);
   if (a.prof && tid == 0) a.prof[b * 8 + 4] = globaltimer();
-  // ---- 5. outputs: the intra order and the staged microbatch keys
-  const int mb_span = a.pg * a.dp_me;
+  // ---- 5. outputs, coalesced: the intra order and, when the greedy split is
+  // kept, its per-position tokens (identity batches reuse the cost pass's
+  // tokens, see TokSrc)
   if (keep) {
-    for (int pos = tid; pos < n; pos += kFusedT) {  // coalesced
+    for (int pos = tid; pos < n; pos += kFusedT) {
       const unsigned it = S.items[pos];
       const unsigned key = it >> 16;
-      const int tok = desc ? 0x7fff - static_cast<int>(key) : static_cast<int>(key);
       a.order_out[first + pos] = static_cast<int>(it & 0xffffu);
-      if (a.staged_tok != nullptr) a.staged_tok[first + pos] = tok;
-      if (a.mb_staged != nullptr && pos < mb_span) a.mb_staged[mb_index(a, b, pos)] = tok;
+      if (a.tok16_staged != nullptr)
+        a.tok16_staged[first + pos] = static_cast<unsigned short>(desc ? 0x7fffu - key : key);
     }
   } else {
     for (int i = tid; i < n; i += kFusedT) a.order_out[first + i] = i;
-    for (int k = tid; k < n; k += kFusedT) {
-      const unsigned it = S.items[k];
-      const int pos = static_cast<int>(it & 0xffffu);
-      const unsigned key = it >> 16;
-      const int tok = desc ? 0x7fff - static_cast<int>(key) : static_cast<int>(key);
-      if (a.staged_tok != nullptr) a.staged_tok[first + pos] = tok;
-      if (a.mb_staged != nullptr && pos < mb_span) a.mb_staged[mb_index(a, b, pos)] = tok;
-    }
   }
   if (a.prof) {
     __syncthreads();

@@ -157,27 +157,27 @@ cudaError_t launch_select(const double* keys, const int* pending, int np, int k,
 
 // assemble_microbatches (workload.cpp:179-204) as token sums: microbatch i of
 // coupled group e = samples at positions (e*span + j)*per_group + i, j < span.
-__global__ void assemble_kernel(long long n_batches, int n, int dp_lm, int dp_me,
-                                const int* tok, int* mbtok) {
+__global__ void assemble_kernel(long long n_batches, int n, int dp_lm, int dp_me, TokSrc tok,
+                                bool staged, int* mbsum) {
   const int per_group = n / dp_lm;
   const int span = dp_lm / dp_me;
   const long long per_batch = static_cast<long long>(dp_me) * per_group;
   const long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (x >= n_batches * per_batch) return;
   const long long b = x / per_batch;
-  const int r = static_cast<int>(x % per_batch);  // r = i * dp_me + e (output order)
-  const int i = r / dp_me, e = r % dp_me;
+  const int r = static_cast<int>(x % per_batch);  // r = e * per_group + i
+  const int e = r / per_group, i = r % per_group;
   long long s = 0;
-  for (int j = 0; j < span; ++j) s += tok[b * n + static_cast<long long>(e * span + j) * per_group + i];
-  mbtok[x] = static_cast<int>(s);
+  for (int j = 0; j < span; ++j) s += tok.get(b, (e * span + j) * per_group + i, staged);
+  mbsum[x] = static_cast<int>(s);
 }
 
-cudaError_t launch_assemble(long long n_batches, int n, int dp_lm, int dp_me, const int* tok,
-                            int* enc, cudaStream_t stream) {
+cudaError_t launch_assemble(long long n_batches, int n, int dp_lm, int dp_me, TokSrc tok,
+                            bool staged, int* mbsum, cudaStream_t stream) {
   const long long total = n_batches * dp_me * static_cast<long long>(n / dp_lm);
   if (total == 0) return cudaSuccess;
   assemble_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(
-      n_batches, n, dp_lm, dp_me, tok, enc);
+      n_batches, n, dp_lm, dp_me, tok, staged, mbsum);
   return cudaGetLastError();
 }
 

@@ -407,18 +407,25 @@ cudaError_t launch_unit_times(const DevCM& cm, int kind, int tp, long long n,
 
 // ------------------------------------------------- coupled-group iteration
 // Microbatch token keys of coupled group `gid`, position i (after the
-// group's optional reorder): stream layout [b][i][e] (int32, enc == gen,
-// count == span) or group-contiguous int64 enc/gen/count arrays.
+// group's optional reorder): stream form (positions of TokSrc when span == 1,
+// assembled sums otherwise; enc == gen, count == span) or group-contiguous
+// int64 enc/gen/count arrays.
+__device__ __forceinline__ long long stream_tok(const GroupSimArgs& a, long long b, int grp,
+                                                int src_i) {
+  if (a.span == 1) return a.tok.get(b, grp * a.l + src_i, a.staged);
+  return a.mbsum[(b * a.groups + grp) * static_cast<long long>(a.l) + src_i];
+}
+
 struct GroupTok {
   const GroupSimArgs* a;
   long long gid;
   __device__ __forceinline__ void operator()(int i, long long* e, long long* g, int* c) const {
     const int l = a->l;
     const int src_i = a->order ? a->order[gid * l + i] : i;
-    if (a->mbtok) {
+    if (a->stream) {
       const long long b = gid / a->groups;
       const int grp = static_cast<int>(gid % a->groups);
-      const long long v = a->mbtok[(b * l + src_i) * a->groups + grp];
+      const long long v = stream_tok(*a, b, grp, src_i);
       *e = v;
       *g = v;
       *c = a->span;
@@ -444,7 +451,6 @@ group_sims_fast(GroupSimArgs a) {
   // token access: stream layout [b][i][e] or group-contiguous arrays
   const long long bidx = gid / a.groups;
   const int grp = static_cast<int>(gid - bidx * a.groups);
-  const int* tokp = STREAM ? a.mbtok + bidx * l * a.groups + grp : nullptr;
   const long long* encp = STREAM ? nullptr : a.enc + gid * l;
   const long long* genp = STREAM ? nullptr : (a.gen ? a.gen + gid * l : encp);
   const int* cntp = STREAM ? nullptr : (a.count ? a.count + gid * l : nullptr);
@@ -495,7 +501,7 @@ group_sims_fast(GroupSimArgs a) {
       long long te, tg;
       int c;
       if (STREAM) {
-        te = tg = tokp[static_cast<long long>(src) * a.groups];
+        te = tg = stream_tok(a, bidx, grp, src);
         c = a.span;
       } else {
         te = encp[src];
@@ -625,13 +631,13 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
   const unsigned grid = static_cast<unsigned>((total + T - 1) / T);
   if (fast_sims(a)) {
     switch (plan_stages(a.plan)) {
-      case 2: a.mbtok ? group_sims_fast<2, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<2, false><<<grid, T, 0, stream>>>(a); break;
-      case 3: a.mbtok ? group_sims_fast<3, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<3, false><<<grid, T, 0, stream>>>(a); break;
-      case 4: a.mbtok ? group_sims_fast<4, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<4, false><<<grid, T, 0, stream>>>(a); break;
-      case 5: a.mbtok ? group_sims_fast<5, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<5, false><<<grid, T, 0, stream>>>(a); break;
-      case 6: a.mbtok ? group_sims_fast<6, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<6, false><<<grid, T, 0, stream>>>(a); break;
-      case 7: a.mbtok ? group_sims_fast<7, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<7, false><<<grid, T, 0, stream>>>(a); break;
-      default: a.mbtok ? group_sims_fast<8, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<8, false><<<grid, T, 0, stream>>>(a); break;
+      case 2: a.stream ? group_sims_fast<2, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<2, false><<<grid, T, 0, stream>>>(a); break;
+      case 3: a.stream ? group_sims_fast<3, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<3, false><<<grid, T, 0, stream>>>(a); break;
+      case 4: a.stream ? group_sims_fast<4, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<4, false><<<grid, T, 0, stream>>>(a); break;
+      case 5: a.stream ? group_sims_fast<5, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<5, false><<<grid, T, 0, stream>>>(a); break;
+      case 6: a.stream ? group_sims_fast<6, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<6, false><<<grid, T, 0, stream>>>(a); break;
+      case 7: a.stream ? group_sims_fast<7, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<7, false><<<grid, T, 0, stream>>>(a); break;
+      default: a.stream ? group_sims_fast<8, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<8, false><<<grid, T, 0, stream>>>(a); break;
     }
   } else {
     group_sims_kernel<<<grid, T, 0, stream>>>(a, static_cast<double*>(scratch));

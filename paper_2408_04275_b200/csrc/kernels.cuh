@@ -23,15 +23,15 @@ struct FusedArgs {
   double* load_before;  // [n_batches * m] or null
   double* load_after;   // [n_batches * m] or null
   unsigned char* kept;  // [n_batches] or null
-  int* orig_tok;        // [n_batches * n] modality tokens, input order, or null
-  int* staged_tok;      // [n_batches * n] modality tokens, intra order, or null
-  // span == 1 (DP_me == DP_lm): microbatch (e, i) is position e*pg + i, so the
-  // kernel writes the microbatch token keys directly in the stream layout
-  // [n_batches][pg][dp_me] consumed by the simulator / inter kernels.
+  // Per-position modality tokens of the intra order (see TokSrc): u16 for
+  // batches whose greedy split was kept (identity batches reuse tok16), and
+  // 32-bit input/staged copies for batches on the 32-bit path.  Any may be
+  // null when no consumer needs them.
+  unsigned short* tok16_staged;  // [n_batches * n]
+  int* tok32_orig;               // [n_batches * n]
+  int* tok32_staged;             // [n_batches * n]
   int pg;               // samples per backbone group (global_batch / dp_lm)
   int dp_me;
-  int* mb_orig;         // identity assembly, or null
-  int* mb_staged;       // intra-ordered assembly, or null
   unsigned char* wide_scratch;  // [n_batches * fused_wide_scratch_bytes(1)]
   unsigned long long* prof;     // optional [n_batches][8] phase timestamps (debug)
   // Output of the cost pass (launch_token_keys): modality tokens per sample,
@@ -49,6 +49,24 @@ cudaError_t launch_token_keys(const int* img_off, const int* img_tok, const int*
                               const int* aud_tok, long long total, int n,
                               unsigned short* tok16, unsigned int* wide_flag,
                               cudaStream_t stream);
+
+// Modality tokens of position `pos` of global batch b, in the input order
+// (staged == false) or the intra order (staged == true), written by the cost
+// pass / fused kernel (FusedArgs).
+struct TokSrc {
+  const unsigned short* t16;         // input order (cost pass)
+  const unsigned short* t16_staged;  // intra order where kept[b]
+  const int* t32;                    // 32-bit path batches
+  const int* t32_staged;
+  const unsigned char* kept;
+  const unsigned int* wide;
+  int n;
+  __device__ __forceinline__ long long get(long long b, int pos, bool staged) const {
+    const long long x = b * n + pos;
+    if (wide[b]) return staged ? t32_staged[x] : t32[x];
+    return (staged && kept[b]) ? t16_staged[x] : t16[x];
+  }
+};
 
 size_t fused_wide_scratch_bytes(long long n_batches);
 size_t fused_smem_bytes();
@@ -150,10 +168,13 @@ struct GroupSimArgs {
   const long long* gen;
   const int* count;      // sample counts (null = `span` for all)
   int span;
-  // Stream layout instead of enc/gen/count: modality-token sums of the
-  // assembled microbatches, [n_batches][l][groups] (encoder == generator
-  // tokens, count == span), so a warp of groups reads one coalesced row.
-  const int* mbtok;
+  // Stream form instead of enc/gen/count (encoder == generator tokens,
+  // count == span): span == 1 reads microbatch (e, i) = position e*l + i of
+  // `tok`; span > 1 reads assembled sums `mbsum` [n_batches][groups][l].
+  bool stream;
+  TokSrc tok;
+  bool staged;           // read tok's intra order
+  const int* mbsum;
   const int* order;      // optional [n_batches][groups][l] microbatch order
   CostTable table;       // optional (size 0 = evaluate directly)
   double* t_group;
@@ -172,10 +193,13 @@ struct InterArgs {
   const double* bwd;
   const double* keys;    // [batch * l], or null (computed from tokens)
   // Disaggregated form: rows from per-microbatch token sums via the cost
-  // model, stream layout [batch / groups][l][groups] (problem = b*groups+e).
+  // model; problem = b*groups + e, microbatch i = staged position e*l + i
+  // (span == 1, `tok`) or mbsum[b][e][i] (span > 1).
   DevCM cm;
   dtb_plan plan;
-  const int* mbtok;
+  bool stream;
+  TokSrc tok;
+  const int* mbsum;
   int groups;
   int span;
   CostTable table;       // optional (size 0 = evaluate directly)
@@ -217,11 +241,9 @@ cudaError_t launch_memory_check(const DevCM& cm, const dtb_plan& plan,
 
 // ------------------------------------------------ disaggregated glue
 // Microbatch token sums of assembled coupled groups (assemble_microbatches,
-// src/workload.cpp:179-204) from per-position token keys, written in the
-// stream layout [n_batches][pg][dp_me].
-cudaError_t launch_assemble(long long n_batches, int n, int dp_lm, int dp_me,
-                            const int* tok_by_pos, int* mbtok_out,
-                            cudaStream_t stream);
+// src/workload.cpp:179-204) from per-position tokens, [n_batches][dp_me][pg].
+cudaError_t launch_assemble(long long n_batches, int n, int dp_lm, int dp_me, TokSrc tok,
+                            bool staged, int* mbsum_out, cudaStream_t stream);
 // output_order composition (src/reorder.cpp:370-391).
 cudaError_t launch_compose(long long n_batches, int n, int dp_lm, int dp_me,
                            const int* intra, const int* inter, int* out,

@@ -219,8 +219,16 @@ def check_disaggregated(impl, oracle, rng, modes=None):
                       dict(intra=False, inter=True)]
     model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
     ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
-    for pl, fam in disagg_cases(rng):
-        batch = synth_stream(pl.global_batch, int(rng.integers(1, 1 << 30)), fam)
+    cases = list(disagg_cases(rng))
+    # a batch with oversized samples (> 32767 tokens: the kernel's 32-bit path)
+    big = H.plan((1, 8, 1), (1, 8, 2), (1, 8, 1), 512)
+    cases.append((big, "big"))
+    for pl, fam in cases:
+        if fam == "big":
+            batch = synth_stream(pl.global_batch, 77, "skewed")
+            batch.image_tokens[:5] = np.array([40000, 70000, 1, 33000, 123456], dtype=np.int32)
+        else:
+            batch = synth_stream(pl.global_batch, int(rng.integers(1, 1 << 30)), fam)
         for md in modes:
             ra = impl.disaggregated_reorder(ci, pl, batch, **md)
             rb = oracle.disaggregated_reorder(co, pl, batch, **md)
