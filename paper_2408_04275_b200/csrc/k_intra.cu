@@ -270,6 +270,8 @@ intra_fused_kernel(FusedArgs a) {
   // Batches with a saturated token (or outside the 16-bit layout's limits)
   // take the 32-bit path straight from the CSR.
   if (a.wide_flag[b] || m > kNarrowMaxM || n > kFusedMaxN || (n & 7)) {
+    // consumers (TokSrc) then read this batch's 32-bit token copies
+    if (tid == 0) a.wide_flag[b] = 1u;
     fused_wide(a, b, S);
     return;
   }

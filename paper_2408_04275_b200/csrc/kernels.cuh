@@ -38,7 +38,7 @@ struct FusedArgs {
   // saturated to 0x7fff, and a per-batch flag set when any sample saturated
   // (that batch then takes the 32-bit path from the CSR).
   const unsigned short* tok16;
-  const unsigned int* wide_flag;
+  unsigned int* wide_flag;  // set by the kernel for every batch it runs on the 32-bit path
   FastDiv div_pg;
   DevErr* err;
 };
