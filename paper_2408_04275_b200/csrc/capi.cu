@@ -975,13 +975,12 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   // token-indexed cost table shared by both simulations and the inter kernel
   const int tsize = static_cast<int>(std::min<long long>(
       static_cast<long long>(span) * 0x8000, static_cast<long long>(kCostTableMax)));
-  DBuf tab_e, tab_g, tab_k;
-  CU(tab_e.alloc(sizeof(double2) * tsize, s));
-  CU(tab_g.alloc(sizeof(double2) * tsize, s));
+  DBuf tab_eg, tab_k;
+  CU(tab_eg.alloc(sizeof(double4) * tsize, s));
   CU(tab_k.alloc(sizeof(double) * tsize, s));
-  CU(launch_cost_table(cm->dev, *plan, span, tsize, tab_e.as<double2>(), tab_g.as<double2>(),
-                       tab_k.as<double>(), ctx->err, s));
-  CostTable table{tab_e.as<double2>(), tab_g.as<double2>(), tab_k.as<double>(), tsize, span};
+  CU(launch_cost_table(cm->dev, *plan, span, tsize, tab_eg.as<double4>(), tab_k.as<double>(),
+                       ctx->err, s));
+  CostTable table{tab_eg.as<double4>(), tab_k.as<double>(), tsize, span};
   GroupSimArgs ga{};
   ga.cm = cm->dev;
   ga.plan = *plan;

@@ -303,6 +303,15 @@ struct UnitEval {
   }
 };
 
+// One 32-byte cost-table row in a single 256-bit load (sm_100: LDG.256).
+__device__ __forceinline__ double4 ld_row(const double4* p) {
+  double4 r;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+      : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ double mb_mean_fast(long long tokens, int count) {
   return count == 1   ? static_cast<double>(tokens)
          : count == 0 ? 0.0

@@ -510,12 +510,11 @@ group_sims_fast(GroupSimArgs a) {
       }
       if (te < 0 || tg < 0) fault = E_NEG_LOAD;
       if (STREAM && te >= 0 && te < a.table.size) {
-        const double2 e2 = __ldg(a.table.enc + te);
-        const double2 g2 = __ldg(a.table.gen + te);
-        rfE[0] = e2.x;
-        rbE[0] = e2.y;
-        rfG[0] = g2.x;
-        rbG[0] = g2.y;
+        const double4 r = ld_row(a.table.eg + te);
+        rfE[0] = r.x;
+        rbE[0] = r.y;
+        rfG[0] = r.z;
+        rbG[0] = r.w;
       } else {
         ue.eval(mb_mean_fast(te, c), &rfE[0], &rbE[0]);
         ug.eval(mb_mean_fast(tg, c), &rfG[0], &rbG[0]);
@@ -550,6 +549,257 @@ group_sims_fast(GroupSimArgs a) {
   }
   if (fault) dev_fail(a.err, fault);
   a.t_group[gid] = iter;
+}
+
+// ---------------------------------------------------- tiled stream sims
+// The disaggregated stream path's simulations (simulate_iteration,
+// src/simulate.cpp:23-48, over plain 1F1B, src/pipeline_sim.cpp:36-52 and
+// :108-183), one thread per coupled group, no shared memory, no barriers.
+//
+// The stage -> unit layout (PE encoder | PB backbone | PG generator stages)
+// is a template parameter, so every cell's duration is a register chosen at
+// compile time: backbone cells are constants (their load is always seq_len),
+// encoder/generator cells come from the token-indexed cost table through
+// short delay lines (forward of stage s runs microbatch i - s/2 at iteration
+// i, backward runs i - P + 1 + s/2; only the delays actually read survive).
+// Microbatches are processed in chunks of kSimChunk: the chunk's cost-table
+// lookups are all in flight together and its token sums are prefetched one
+// chunk ahead, so a group pays one memory latency per chunk, not per
+// microbatch.
+//
+// Exactness: every cell is start = max(avail, dep), end = start + x with the
+// reference's operands.  All durations are >= 0 and never NaN (profile times
+// are validated strictly positive, src/cost_model.cpp:37-47; analytic and
+// comm terms are non-negative), so the per-device end times are
+// non-decreasing and (i) std::max == fmax on them, (ii) the iteration time
+// max over all events == max over the devices' last ends.
+constexpr int kSimT = 128;
+constexpr int kSimChunk = 4;
+
+
+struct Dur4 {
+  double ef, eb, gf, gb;
+};
+
+// Cold path: token sums beyond the cost table (32-bit batches only).
+__device__ __noinline__ Dur4 sim_eval_direct(const GroupSimArgs* a, long long te) {
+  UnitEval ue, ug;
+  ue.init(a->cm, a->plan, DTB_ENCODER);
+  ug.init(a->cm, a->plan, DTB_GENERATOR);
+  const double x = mb_mean_fast(te, a->span);
+  Dur4 r;
+  ue.eval(x, &r.ef, &r.eb);
+  ug.eval(x, &r.gf, &r.gb);
+  return r;
+}
+
+// DIRECT: token sums may fall outside the cost table (32-bit batches,
+// negative sums): evaluate build_stage_times per microbatch instead.
+template <int PE, int PB, int PG, bool BUSY, bool DIRECT>
+__device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) {
+  constexpr int P = PE + PB + PG;
+  constexpr int C = kSimChunk;
+  const int l = a.l;
+  // this group's token source: position e*l + i of batch b (span == 1) or
+  // the assembled sums [gid][i] (span > 1); optional inter order
+  const long long b = gid / a.groups;
+  const int grp = static_cast<int>(gid - b * a.groups);
+  const int* ord = a.order ? a.order + gid * l : nullptr;
+  const unsigned short* t16 = nullptr;
+  const int* t32 = nullptr;
+  if (a.span == 1) {
+    const long long x0 = b * a.tok.n + static_cast<long long>(grp) * l;
+    if (a.tok.wide[b]) t32 = (a.staged ? a.tok.t32_staged : a.tok.t32) + x0;
+    else t16 = (a.staged && a.tok.kept[b] ? a.tok.t16_staged : a.tok.t16) + x0;
+  } else {
+    t32 = a.mbsum + gid * l;
+  }
+  auto token = [&](int i) -> int {
+    const int src = ord ? __ldg(ord + i) : i;
+    return t16 ? static_cast<int>(__ldg(t16 + src)) : __ldg(t32 + src);
+  };
+
+  UnitEval ub;
+  ub.init(a.cm, a.plan, DTB_BACKBONE);
+  double fB, bB;
+  ub.eval(a.cm.seq_len, &fB, &bB);  // backbone load is always seq_len
+
+  // delay lines (index = delay in iterations)
+  double eF[P], eB[P], gF[P], gB[P];
+  double av[P], busy[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    eF[s] = eB[s] = gF[s] = gB[s] = 0.0;
+    av[s] = busy[s] = 0.0;
+  }
+  int fault = 0;
+  auto dur = [&](int s, bool fwd, int d) -> double {
+    return s < PE ? (fwd ? eF[d] : eB[d])
+                  : s < PE + PB ? (fwd ? fB : bB) : (fwd ? gF[d] : gB[d]);
+  };
+  auto tick_iter = [&](int i, bool check) {
+    double pv[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) pv[s] = av[s];
+    // even tick 2i: F(i - s/2, s) on even s, B(i - P + (s+1)/2, s) on odd s
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const bool fwd = (s & 1) == 0;
+      const int d = fwd ? s / 2 : P - (s + 1) / 2;
+      const int mb = i - d;
+      if (!check || (mb >= 0 && mb < l)) {
+        const double x = dur(s, fwd, d);
+        const double dep = fwd ? (s > 0 ? pv[s - 1] : 0.0) : (s + 1 < P ? pv[s + 1] : pv[s]);
+        const double start = (s == 0 && fwd) || (s == P - 1 && !fwd) ? av[s] : fmax(av[s], dep);
+        av[s] = start + x;
+        if (BUSY) busy[s] += x;
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < P; ++s) pv[s] = av[s];
+    // odd tick 2i+1: F(i - (s-1)/2, s) on odd s, B(i - P + 1 + s/2, s) on even s
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const bool fwd = (s & 1) == 1;
+      const int d = fwd ? (s - 1) / 2 : P - 1 - s / 2;
+      const int mb = i - d;
+      if (!check || (mb >= 0 && mb < l)) {
+        const double x = dur(s, fwd, d);
+        const double dep = fwd ? pv[s - 1] : (s + 1 < P ? pv[s + 1] : pv[s]);
+        const double start = (s == P - 1 && !fwd) ? av[s] : fmax(av[s], dep);
+        av[s] = start + x;
+        if (BUSY) busy[s] += x;
+      }
+    }
+  };
+  auto shift = [&]() {
+#pragma unroll
+    for (int k = P - 1; k > 0; --k) {
+      eF[k] = eF[k - 1];
+      eB[k] = eB[k - 1];
+      gF[k] = gF[k - 1];
+      gB[k] = gB[k - 1];
+    }
+  };
+
+  if (DIRECT) {
+    for (int i = 0; i < l; ++i) {
+      shift();
+      const int te = token(i);
+      if (te < 0) fault = E_NEG_LOAD;
+      const Dur4 r = sim_eval_direct(&a, te);
+      eF[0] = r.ef;
+      eB[0] = r.eb;
+      gF[0] = r.gf;
+      gB[0] = r.gb;
+      tick_iter(i, i < P - 1);
+    }
+  } else {
+    // chunk k = microbatches [k*C, k*C + C): its token sums are loaded one
+    // chunk ahead (one vector load when the layout allows), its cost-table
+    // rows are all in flight before the chunk's first tick.
+    const bool vec = ord == nullptr && (l % C) == 0;
+    auto tokens = [&](int i0, int* tk) {
+      if (i0 >= l) return;
+      if (vec) {
+        if (t16) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(t16 + i0));
+          tk[0] = v.x & 0xffff;
+          tk[1] = v.x >> 16;
+          tk[2] = v.y & 0xffff;
+          tk[3] = v.y >> 16;
+        } else {
+          const int4 v = __ldg(reinterpret_cast<const int4*>(t32 + i0));
+          tk[0] = v.x;
+          tk[1] = v.y;
+          tk[2] = v.z;
+          tk[3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < C; ++j) tk[j] = i0 + j < l ? token(i0 + j) : 0;
+      }
+    };
+    int tk[C] = {}, tk_next[C] = {};
+    tokens(0, tk_next);
+    for (int i0 = 0; i0 < l; i0 += C) {
+#pragma unroll
+      for (int j = 0; j < C; ++j) tk[j] = tk_next[j];
+      tokens(i0 + C, tk_next);
+      double4 row[C];
+#pragma unroll
+      for (int j = 0; j < C; ++j) row[j] = ld_row(a.table.eg + tk[j]);
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const int i = i0 + j;
+        if (i >= l) break;
+        shift();
+        eF[0] = row[j].x;
+        eB[0] = row[j].y;
+        gF[0] = row[j].z;
+        gB[0] = row[j].w;
+        if (i < P - 1) tick_iter(i, true);
+        else tick_iter(i, false);
+      }
+    }
+  }
+  for (int i = l; i < l + P - 1; ++i) {
+    shift();
+    tick_iter(i, true);
+  }
+  double iter = 0.0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) iter = fmax(iter, av[s]);
+  if (a.busy) {
+    double bub = 0.0;
+    if (iter > 0.0) {
+      double idle = 0.0;
+#pragma unroll
+      for (int s = 0; s < P; ++s) idle += iter - busy[s];
+      bub = idle / (P * iter);
+    }
+    a.busy[gid] = bub;
+  }
+  if (fault) dev_fail(a.err, fault);
+  a.t_group[gid] = iter;
+}
+
+template <int PE, int PB, int PG, bool BUSY>
+__device__ __noinline__ void sim_group_direct(const GroupSimArgs* a, long long gid) {
+  sim_group<PE, PB, PG, BUSY, true>(*a, gid);
+}
+
+template <int PE, int PB, int PG, bool BUSY>
+__global__ void __launch_bounds__(kSimT, 5)
+group_sims_tiled(const __grid_constant__ GroupSimArgs a) {
+  const long long gid = blockIdx.x * static_cast<long long>(kSimT) + threadIdx.x;
+  if (gid >= a.n_batches * a.groups) return;
+  // u16 token sums are < 0x8000 <= table.size; assembled sums of u16 batches
+  // are < span * 0x8000 — inside the table unless it was capped
+  const long long b = gid / a.groups;
+  const bool direct = a.tok.wide[b] ||
+                      (a.span > 1 && static_cast<long long>(a.span) * 0x8000 > a.table.size);
+  if (direct) sim_group_direct<PE, PB, PG, BUSY>(&a, gid);
+  else sim_group<PE, PB, PG, BUSY, false>(a, gid);
+}
+
+using TiledFn = void (*)(GroupSimArgs);
+template <bool BUSY>
+static TiledFn tiled_for(int pe, int pb, int pg) {
+#define DTB_TILED(E, B, G) \
+  if (pe == E && pb == B && pg == G) return group_sims_tiled<E, B, G, BUSY>;
+  DTB_TILED(1, 1, 1)
+  DTB_TILED(1, 2, 1)
+  DTB_TILED(2, 1, 1)
+  DTB_TILED(1, 1, 2)
+  DTB_TILED(1, 3, 1)
+  DTB_TILED(1, 4, 1)
+  DTB_TILED(2, 2, 1)
+  DTB_TILED(1, 2, 2)
+  DTB_TILED(2, 2, 2)
+  DTB_TILED(1, 6, 1)
+#undef DTB_TILED
+  return nullptr;
 }
 
 // General path (any stage count, interleaved schedules): rows of
@@ -629,6 +879,17 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
   if (total == 0) return cudaSuccess;
   const int T = 128;
   const unsigned grid = static_cast<unsigned>((total + T - 1) / T);
+  if (a.stream && a.plan.vpp == 1) {
+    const TiledFn fn = a.busy ? tiled_for<true>(a.plan.unit[0].pp, a.plan.unit[1].pp,
+                                                a.plan.unit[2].pp)
+                              : tiled_for<false>(a.plan.unit[0].pp, a.plan.unit[1].pp,
+                                                 a.plan.unit[2].pp);
+    if (fn != nullptr) {
+      const unsigned g = static_cast<unsigned>((total + kSimT - 1) / kSimT);
+      fn<<<g, kSimT, 0, stream>>>(a);
+      return cudaGetLastError();
+    }
+  }
   if (fast_sims(a)) {
     switch (plan_stages(a.plan)) {
       case 2: a.stream ? group_sims_fast<2, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<2, false><<<grid, T, 0, stream>>>(a); break;
@@ -646,53 +907,58 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
 }
 
 // Token-indexed cost table (see CostTable): thread per token sum s.
-__global__ void cost_table_kernel(DevCM cm, dtb_plan plan, int span, int size, double2* enc,
-                                  double2* gen, double* key, DevErr* err) {
+__global__ void cost_table_kernel(DevCM cm, dtb_plan plan, int span, int size, double4* eg,
+                                  double* key, DevErr* err) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= size) return;
   UnitEval ue, ug;
   ue.init(cm, plan, DTB_ENCODER);
   ug.init(cm, plan, DTB_GENERATOR);
   const double x = mb_mean_fast(s, span);
-  double f, b;
-  ue.eval(x, &f, &b);
-  enc[s] = make_double2(f, b);
-  ug.eval(x, &f, &b);
-  gen[s] = make_double2(f, b);
+  double4 r;
+  ue.eval(x, &r.x, &r.y);
+  ug.eval(x, &r.z, &r.w);
+  eg[s] = r;
   const int e = dev_fwd_key(cm, plan, x, x, &key[s]);
   if (e) dev_fail(err, e);
 }
 
 cudaError_t launch_cost_table(const DevCM& cm, const dtb_plan& plan, int span, int size,
-                              double2* enc, double2* gen, double* key, DevErr* err,
-                              cudaStream_t stream) {
+                              double4* eg, double* key, DevErr* err, cudaStream_t stream) {
   if (size <= 0) return cudaSuccess;
-  cost_table_kernel<<<(size + 255) / 256, 256, 0, stream>>>(cm, plan, span, size, enc, gen, key,
-                                                            err);
+  cost_table_kernel<<<(size + 255) / 256, 256, 0, stream>>>(cm, plan, span, size, eg, key, err);
   return cudaGetLastError();
 }
 
 // simulate_iteration's fold over groups (simulate.cpp:31-46): slowest group
 // by strict '>' in group order, t_iter = slowest + dp_sync.  bubble (in/out)
 // holds per-group fractions; the mean is a sequential sum in group order.
+// One warp per batch: max over its groups (max is exact in any order for
+// these non-negative, non-NaN makespans), then + dp_sync.
 __global__ void t_iter_reduce_kernel(long long n_batches, int groups,
                                      const double* t_group, double dp_sync,
                                      double* t_iter) {
-  const long long b = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long b = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (b >= n_batches) return;
   double worst = 0.0;
-  for (int g = 0; g < groups; ++g) {
+  for (int g = lane; g < groups; g += 32) {
     const double t = t_group[b * groups + g];
     if (t > worst) worst = t;
   }
-  t_iter[b] = worst + dp_sync;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double y = __shfl_xor_sync(0xffffffffu, worst, o);
+    if (y > worst) worst = y;
+  }
+  if (lane == 0) t_iter[b] = worst + dp_sync;
 }
 
 cudaError_t launch_t_iter_reduce(long long n_batches, int groups,
                                  const double* t_group, double dp_sync,
                                  double* t_iter, cudaStream_t stream) {
   if (n_batches == 0) return cudaSuccess;
-  t_iter_reduce_kernel<<<static_cast<unsigned>((n_batches + 127) / 128), 128, 0,
+  t_iter_reduce_kernel<<<static_cast<unsigned>((n_batches * 32 + 255) / 256), 256, 0,
                          stream>>>(n_batches, groups, t_group, dp_sync, t_iter);
   return cudaGetLastError();
 }

@@ -143,16 +143,15 @@ cudaError_t launch_unit_times(const DevCM& cm, int kind, int tp, long long n,
 // entry is computed once with exactly the reference's operation sequence,
 // so a lookup is bit-identical to recomputing it.
 struct CostTable {
-  const double2* enc;  // (f, b) of the encoder unit
-  const double2* gen;  // (f, b) of the generator unit
+  const double4* eg;   // (f, b) of the encoder unit, (f, b) of the generator
+                       // unit: one 32-byte row per token sum (one 256-bit load)
   const double* key;   // forward key
   int size;            // sums >= size are evaluated directly
   int span;
 };
 constexpr int kCostTableMax = 1 << 20;
 cudaError_t launch_cost_table(const DevCM& cm, const dtb_plan& plan, int span, int size,
-                              double2* enc, double2* gen, double* key, DevErr* err,
-                              cudaStream_t stream);
+                              double4* eg, double* key, DevErr* err, cudaStream_t stream);
 
 // Makespans of coupled groups whose microbatches are given by token keys:
 // group g of batch b covers microbatches [g*l, (g+1)*l) of batch b.

@@ -211,6 +211,11 @@ def disagg_cases(rng):
     yield H.plan((1, 1, 1), (1, 2, 1), (1, 1, 1), 8), "skewed"
     yield H.plan((1, 2, 1), (1, 4, 2), (1, 4, 1), 64, vpp=2), "mixed"
     yield H.plan((1, 4, 1), (1, 4, 2), (1, 4, 1), 90), "mixed"  # n % m != 0 blocks
+    # stage layouts of the compile-time tiled simulations and the generic one
+    yield H.plan((1, 4, 2), (1, 4, 1), (1, 4, 1), 64), "mixed"
+    yield H.plan((1, 4, 1), (1, 4, 1), (1, 4, 2), 64), "skewed"
+    yield H.plan((1, 4, 1), (1, 4, 3), (1, 4, 2), 64), "mixed"
+    yield H.plan((1, 8, 1), (1, 8, 6), (1, 8, 1), 1024), "mixed"  # l = 128, 4 chunks
 
 
 def check_disaggregated(impl, oracle, rng, modes=None):
@@ -240,15 +245,26 @@ def check_disaggregated(impl, oracle, rng, modes=None):
             assert ra.t_iter_after == rb.t_iter_after, tag
 
 
-def check_stream(impl, oracle, rng, n_batches=3, bs=512, dp=8, inter=True):
+STREAM_CASES = [  # (n_batches, bs, dp_lm, dp_me, pp triple, inter)
+    (3, 512, 8, 8, (1, 2, 1), True),
+    (37, 256, 8, 8, (1, 2, 1), False),     # CTAs of the simulations span batches
+    (5, 4096, 8, 8, (1, 2, 1), False),     # l = 512: many staged chunks
+    (4, 2048, 16, 4, (1, 2, 1), True),     # span 4: assembled microbatch sums
+    (3, 1024, 8, 8, (2, 1, 1), True),
+    (2, 16384, 128, 128, (1, 2, 1), False),  # BASELINE config 4 batch shape
+]
+
+
+def check_stream(impl, oracle, rng, cases=None):
     model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
     ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
-    pl = H.plan((1, dp, 1), (1, dp, 2), (1, dp, 1), bs)
-    s = synth_stream(n_batches * bs, int(rng.integers(1, 1 << 30)), "mixed")
-    ra = impl.reorder_stream(ci, pl, s, n_batches, inter=inter)
-    rb = oracle.reorder_stream(co, pl, s, n_batches, inter=inter)
-    for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
-        assert_same(ra[k], rb[k], k)
+    for n_batches, bs, dp, dp_me, pp, inter in cases or STREAM_CASES:
+        pl = H.plan((1, dp_me, pp[0]), (1, dp, pp[1]), (1, dp_me, pp[2]), bs)
+        s = synth_stream(n_batches * bs, int(rng.integers(1, 1 << 30)), "mixed")
+        ra = impl.reorder_stream(ci, pl, s, n_batches, inter=inter)
+        rb = oracle.reorder_stream(co, pl, s, n_batches, inter=inter)
+        for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
+            assert_same(ra[k], rb[k], f"{k} {n_batches}x{bs} dp {dp}/{dp_me} pp {pp}")
 
 
 def check_simulate(impl, oracle, rng):
