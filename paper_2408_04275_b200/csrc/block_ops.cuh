@@ -198,19 +198,13 @@ __device__ void tile_radix_sort(K* keys, V* vals, int n, int lo_bit,
   }
 }
 
-// Lanes of the warp whose RB-bit digit equals this lane's, among lanes with
-// `ok` set: RB + 1 ballots instead of MATCH.ANY (a low-throughput
-// instruction; the ballots issue at full rate).
+// Lanes of the warp whose digit equals this lane's, among lanes with `ok`
+// set.  MATCH.ANY measured on B200 (tools/bench_match.cu): ~2.4 SM-cycles
+// per warp-op versus ~21 for the 7-ballot restatement.
 template <int RB>
 __device__ __forceinline__ unsigned digit_peers(unsigned d, bool ok) {
-  unsigned peers = __ballot_sync(kFull, ok);
-#pragma unroll
-  for (int bit = 0; bit < RB; ++bit) {
-    const bool set = (d >> bit) & 1u;
-    const unsigned bal = __ballot_sync(kFull, set);
-    peers &= set ? bal : ~bal;
-  }
-  return peers;
+  const unsigned peers = __match_any_sync(kFull, ok ? d : 0xffffffffu);
+  return ok ? peers : 0u;
 }
 
 // One stable counting pass over n <= T*ITEMS 32-bit items in place, digit
@@ -277,6 +271,199 @@ __device__ void tile_pass_u32(unsigned int* items, int n, const DigitFn& digit, 
       const unsigned d = static_cast<unsigned>(digit(pos, k[i]));
       const unsigned r = (i & 1) ? (rk[i >> 1] >> 16) : (rk[i >> 1] & 0xffffu);
       items[cnt[w * D + d] + r] = k[i];
+    }
+  }
+  __syncthreads();
+}
+
+// Bijective in-block swizzle of sorted positions (stays inside its 32-item
+// block): strided gathers of sorted items (stride r = active groups in the
+// greedy, consecutive slots of one group in the write-out) spread over banks.
+__device__ __forceinline__ int swz(int k) {
+  const int x = k >> 5;
+  return k ^ ((x ^ (x >> 2) ^ (x >> 4)) & 31);
+}
+
+// One stable counting pass of a block radix sort of u16 sample indices by
+// the u16 keys key[idx], in place, over ALL T * ITEMS slots (the caller pads
+// past n with indices whose key has the largest digit in every pass, so they
+// stay at the end and no per-item bounds predicates are needed).  Only the
+// indices stay live across the block scan, two per register (ITEMS / 2
+// registers); keys are re-read from shared memory and per-item ranks are
+// parked there (u16 `ranks`).  Warp-striped ranking as in tile_pass_u32
+// keeps equal digits in input order.  SWZ: write swizzled positions.
+// key[v] for a shared-memory u16 array, address formed inside the asm so the
+// compiler cannot keep ITEMS addresses alive between the two phases of a
+// pass (it would rather spill them than recompute one shift-add).
+__device__ __forceinline__ unsigned lds_u16_at(unsigned base, unsigned v) {
+  unsigned short x;
+  asm volatile("{\n\t.reg .u32 a;\n\tmad.lo.u32 a, %1, 2, %2;\n\tld.shared.u16 %0, [a];\n\t}"
+               : "=h"(x)
+               : "r"(v), "r"(base));
+  return x;
+}
+
+template <int T, int ITEMS, int RB, bool SWZ, typename DigitFn>
+__device__ void tile_pass_idx16(unsigned short* idx, const unsigned short* key,
+                                const DigitFn& digit, int* cnt, int* scan_tmp,
+                                unsigned short* ranks) {
+  constexpr int W = T / 32;
+  constexpr int D = 1 << RB;
+  constexpr int PAIRS = (ITEMS + 1) / 2;
+  // counters are digit-major (cnt[d * W + w]): the stable (digit, warp)
+  // order is then a contiguous scan
+  const int lane = lane_id(), w = warp_id();
+  const unsigned lt = lanemask_lt();
+  for (int i = threadIdx.x; i < D * W; i += T) cnt[i] = 0;
+  unsigned int k2[PAIRS];
+  const int base_pos = w * 32 * ITEMS + lane;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const unsigned v = idx[base_pos + i * 32];
+    if (i & 1) k2[i >> 1] |= v << 16;
+    else k2[i >> 1] = v;
+  }
+  // opaque: the compiler would otherwise keep ITEMS unpacked registers
+#pragma unroll
+  for (int q = 0; q < PAIRS; ++q) asm volatile("" : "+r"(k2[q]));
+  auto item = [&](int i) -> unsigned { return (i & 1) ? (k2[i >> 1] >> 16) : (k2[i >> 1] & 0xffffu); };
+  const unsigned key_base = static_cast<unsigned>(__cvta_generic_to_shared(key));
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    // peers by MATCH.ANY; the lowest peer reserves the group's ranks with
+    // one shared atomic whose return value is the count before this slot:
+    // no load -> add -> store chain between consecutive slots of a warp
+    // (same-address atomics of a warp retire in program order)
+    const unsigned d = static_cast<unsigned>(digit(lds_u16_at(key_base, item(i))));
+    const unsigned peers = __match_any_sync(kFull, d);
+    const int leader = __ffs(peers) - 1;
+    int old = 0;
+    if (lane == leader) old = atomicAdd(cnt + d * W + w, __popc(peers));
+    const int before = __shfl_sync(kFull, old, leader);
+    ranks[base_pos + i * 32] = static_cast<unsigned short>(before + __popc(peers & lt));
+  }
+  __syncthreads();
+  constexpr int PER = (D * W + T - 1) / T;
+  int local[PER];
+  int sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int x = threadIdx.x * PER + j;
+    local[j] = x < D * W ? cnt[x] : 0;
+    sum += local[j];
+  }
+  int total;
+  int base = block_excl_scan<T>(sum, scan_tmp, &total);
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int x = threadIdx.x * PER + j;
+    if (x < D * W) cnt[x] = base;
+    base += local[j];
+  }
+  // the key base address for the scatter phase comes back from memory, so
+  // ptxas cannot prove the key addresses equal to the ranking phase's and
+  // keep them (spilled) across the scan instead of recomputing them
+  if (threadIdx.x == 0) cnt[D * W] = static_cast<int>(key_base);
+  __syncthreads();
+  const unsigned key_base2 = static_cast<unsigned>(*static_cast<volatile int*>(cnt + D * W));
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const unsigned v = item(i);
+    const unsigned d = static_cast<unsigned>(digit(lds_u16_at(key_base2, v)));
+    const int dst = cnt[d * W + w] + ranks[base_pos + i * 32];
+    idx[SWZ ? swz(dst) : dst] = static_cast<unsigned short>(v);
+  }
+  __syncthreads();
+}
+
+// One stable counting pass (per-THREAD counters, blocked arrangement) of a
+// block radix sort of u16 sample indices by the u16 keys key[idx], in place.
+// Thread t owns slots [t*ITEMS, (t+1)*ITEMS) — contiguous, so the stable
+// order is (digit, thread, item) — and counts its digits in private u16
+// counters c(d, t), packed two per 32-bit word, digit-major, one pad word
+// per 16 (conflict-free raking scan).  Counting and the scatter's
+// position reservation are shared-memory atomics on the counter words: no
+// load -> add -> store chain between a thread's items (same-thread atomics
+// on one address retire in program order, which is exactly the stable
+// order), no warp votes or matches (their throughput bounded the
+// warp-striped variant), no per-item rank storage.  The caller pads past n
+// with indices whose key has the largest digit in every pass.
+// ITEMS % 4 == 0 (64-bit loads of a thread's slots).  Counter storage:
+// blocked_cnt_words(T, RB) 32-bit words.
+__host__ __device__ constexpr int blocked_cnt_words(int T, int RB) {
+  return (1 << RB) * T / 2 + (1 << RB) * T / 32;
+}
+
+template <int T, int ITEMS, int RB, bool SWZ, typename DigitFn>
+__device__ void tile_pass_blocked(unsigned short* idx, const unsigned short* key,
+                                  const DigitFn& digit, unsigned* cntw, int* scan_tmp) {
+  constexpr int D = 1 << RB;
+  constexpr int WORDS = D * T / 2;
+  constexpr int PER = WORDS / T;  // raking segment (16 words for RB = 5)
+  constexpr int G = 4;
+  static_assert(ITEMS % G == 0 && WORDS % T == 0 && PER % 16 == 0, "shape");
+  const int t = threadIdx.x;
+  // counter (d, t): logical u16 e = d*T + t -> padded word (e>>1) + (e>>5)
+  auto word_of = [&](unsigned d) -> int {
+    const int e = static_cast<int>(d) * T + t;
+    return (e >> 1) + (e >> 5);
+  };
+  const unsigned half = (t & 1) * 16;  // e and t have the same parity (T even)
+  for (int i = t; i < blocked_cnt_words(T, RB); i += T) cntw[i] = 0u;
+  __syncthreads();
+  const uint2* mine = reinterpret_cast<const uint2*>(idx + t * ITEMS);
+#pragma unroll 2
+  for (int g = 0; g < ITEMS / G; ++g) {
+    const uint2 p = mine[g];
+    const unsigned v[G] = {p.x & 0xffffu, p.x >> 16, p.y & 0xffffu, p.y >> 16};
+    unsigned d[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) d[j] = static_cast<unsigned>(digit(key[v[j]]));
+#pragma unroll
+    for (int j = 0; j < G; ++j) atomicAdd(cntw + word_of(d[j]), 1u << half);
+  }
+  // this thread's items, two per register, held across the scan (the
+  // scatter is in place)
+  uint2 it[ITEMS / G];
+#pragma unroll
+  for (int g = 0; g < ITEMS / G; ++g) {
+    it[g] = mine[g];
+    asm volatile("" : "+r"(it[g].x), "+r"(it[g].y));  // keep them packed
+  }
+  __syncthreads();
+  // raking exclusive scan over (d, t) = logical word order: thread t owns
+  // logical words [t*PER, (t+1)*PER) = padded words t*(PER + PER/16) + ...
+  unsigned* seg = cntw + t * (PER + PER / 16);
+  unsigned local[PER];
+  int sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    local[j] = seg[j + j / 16];
+    sum += static_cast<int>((local[j] & 0xffffu) + (local[j] >> 16));
+  }
+  int total;
+  int base = block_excl_scan<T>(sum, scan_tmp, &total);
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const unsigned lo = local[j] & 0xffffu, hi = local[j] >> 16;
+    seg[j + j / 16] = static_cast<unsigned>(base) | (static_cast<unsigned>(base + lo) << 16);
+    base += static_cast<int>(lo + hi);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < ITEMS / G; ++g) {
+    const unsigned v[G] = {it[g].x & 0xffffu, it[g].x >> 16, it[g].y & 0xffffu, it[g].y >> 16};
+    unsigned d[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) d[j] = static_cast<unsigned>(digit(key[v[j]]));
+    unsigned old[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) old[j] = atomicAdd(cntw + word_of(d[j]), 1u << half);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int dst = static_cast<int>((old[j] >> half) & 0xffffu);
+      idx[SWZ ? swz(dst) : dst] = static_cast<unsigned short>(v[j]);
     }
   }
   __syncthreads();

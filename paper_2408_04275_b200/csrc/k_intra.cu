@@ -20,6 +20,7 @@
 
 #include "block_ops.cuh"
 #include "greedy.cuh"
+#include "greedy_fused.cuh"
 #include "kernels.cuh"
 
 namespace dtb {
@@ -93,9 +94,11 @@ intra_generic_kernel(const double* __restrict__ sizes, int n, int m, int order,
 }
 
 // -------------------------------------------------------------------- fused
-constexpr int kFusedT = 512;
-constexpr int kFusedItems = 32;
-constexpr int kFusedMaxN = kFusedT * kFusedItems;  // 16384 samples per batch
+// 384 threads x 43 items: two CTAs per SM leave 85 registers per thread,
+// enough to hold a thread's 43 items across a radix pass without spilling.
+constexpr int kFusedT = 384;
+constexpr int kFusedMaxN = 16384;  // samples per batch
+constexpr int kFusedItems = ((kFusedMaxN + kFusedT - 1) / kFusedT + 3) / 4 * 4;  // 44
 constexpr int kNarrowMaxM = 128;                    // groups in the smem path
 constexpr int kWideMaxM = 512;                      // groups in the global path
 constexpr int kRB = 7;                              // radix digit bits
@@ -103,21 +106,31 @@ constexpr int kRB = 7;                              // radix digit bits
 #define DTB_FUSED_MIN_BLOCKS 2  // two CTAs per SM (64 registers per thread)
 #endif
 
-// Narrow (shared-memory) state, ~102 KB so two CTAs share an SM.
-//   items[k] = (key << 16) | sample index, key = modality tokens (asc) or
-//   0x7fff - tokens (desc); cost_size = 2 * tokens, so sorting by key is
-//   sorting by cost, and one array carries key, index and token.
+// Narrow (shared-memory) state, ~112 KB so two CTAs share an SM.
+//   kbi[i]   = sort key of sample i: modality tokens (asc) or 0x7fff - tokens
+//              (desc); cost_size = 2 * tokens, so sorting by key is sorting
+//              by cost.  Slots past n hold the padding key 0xffff.
+//   idx16[k] = sample index of sorted position k (after the last pass: at
+//              swizzled slot swz(k)).
+//   out16[g * capP + slot] = sorted position of the item the greedy put in
+//              slot `slot` of group g (capP = cap padded to 2 mod 4: bank
+//              spread); the sort passes park their per-item ranks here.
+constexpr int kFusedSlots = kFusedT * kFusedItems;  // sort slots incl. padding
 struct NarrowSmem {
-  unsigned int items[kFusedMaxN];
-  unsigned char grp[kFusedMaxN];  // greedy group of sorted item k
-  int radix_cnt[(1 << kRB) * (kFusedT / 32)];
-  long long AL[kNarrowMaxM], TL[kNarrowMaxM], gload[kNarrowMaxM];
-  unsigned long long blk_ident[kNarrowMaxM], blk_greedy[kNarrowMaxM];
-  int AG[kNarrowMaxM], TG[kNarrowMaxM], cnt[kNarrowMaxM];
-  int tmp[kFusedT / 32 + 2];
+  unsigned short kbi[kFusedSlots];
+  alignas(16) unsigned short idx16[kFusedSlots];
+  alignas(16) unsigned short out16[kFusedMaxN + 4 * kNarrowMaxM];  // also the sort counters
+  int radix_cnt[(1 << kRB) * (kFusedT / 32) + 1];
+  FusedGreedySmem G;
+  unsigned blk_ident[kNarrowMaxM], blk_greedy[kNarrowMaxM];
+  int off[kNarrowMaxM];
+  int tmp[kFusedT / 32 + 3];
   long long tmpll[kFusedT / 32 + 1];
   unsigned int s_and, s_or;
 };
+constexpr int kSortRB = 5;  // narrow-path digit bits (per-thread counters)
+static_assert((kFusedMaxN + 4 * kNarrowMaxM) / 2 >= blocked_cnt_words(kFusedT, kSortRB),
+              "sort counters fit in out16");
 
 constexpr size_t kFusedSmem = sizeof(NarrowSmem);
 // Wide fallback (any cost <= 2^32-1, m <= 512) in a global scratch slot.
@@ -215,13 +228,16 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
     };
     st.tmpll = S.tmpll;
     if (desc)
-      greedy_rounds<kFusedT, 1, long long, false>(n, m, cap, z0, z1, size_at, assign, st);
+      greedy_rounds<kFusedT, 2, long long, false>(n, m, cap, z0, z1, size_at, assign, st);
     else
-      greedy_rounds<kFusedT, 1, long long, true>(n, m, cap, z0, z1, size_at, assign, st);
-    int pre_local = tid < m ? st.cnt[tid] : 0;
+      greedy_rounds<kFusedT, 2, long long, true>(n, m, cap, z0, z1, size_at, assign, st);
+    // group offsets (blocked: thread owns groups 2*tid, 2*tid + 1)
+    const int g0 = 2 * tid;
+    const int c0 = g0 < m ? st.cnt[g0] : 0, c1 = g0 + 1 < m ? st.cnt[g0 + 1] : 0;
     int total;
-    const int pre = block_excl_scan<kFusedT>(pre_local, S.tmp, &total);
-    if (tid < m) off[tid] = pre;
+    const int pre = block_excl_scan<kFusedT>(c0 + c1, S.tmp, &total);
+    if (g0 < m) off[g0] = pre;
+    if (g0 + 1 < m) off[g0 + 1] = pre + c0;
     __syncthreads();
     for (int k = tid; k < n; k += kFusedT) {
       const unsigned as = asg[k];
@@ -254,7 +270,7 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
 }
 
 __global__ void __launch_bounds__(kFusedT, DTB_FUSED_MIN_BLOCKS)
-intra_fused_kernel(FusedArgs a) {
+intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw);
   const int n = a.n, m = a.m, tid = threadIdx.x;
@@ -275,7 +291,7 @@ intra_fused_kernel(FusedArgs a) {
     fused_wide(a, b, S);
     return;
   }
-  for (int g = tid; g < m; g += kFusedT) S.blk_ident[g] = 0ull;
+  for (int g = tid; g < m; g += kFusedT) S.blk_ident[g] = 0u;
   if (tid == 0) {
     S.s_and = ~0u;
     S.s_or = 0u;
@@ -284,7 +300,7 @@ intra_fused_kernel(FusedArgs a) {
   unsigned int kand = ~0u, kor = 0u;
   int zeros = 0;
   {
-    constexpr int V = kFusedMaxN / 8 / kFusedT;  // 128-bit loads per thread
+    constexpr int V = (kFusedMaxN / 8 + kFusedT - 1) / kFusedT;  // 128-bit loads per thread
     const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
     const int nv = n >> 3;
     uint4 q[V];
@@ -301,7 +317,7 @@ intra_fused_kernel(FusedArgs a) {
       const int i0 = idx * 8;
       const unsigned blk0 = min(a.div_pg.div(static_cast<unsigned>(i0)), static_cast<unsigned>(m - 1));
       const unsigned blk7 = min(a.div_pg.div(static_cast<unsigned>(i0 + 7)), static_cast<unsigned>(m - 1));
-      unsigned long long run = 0;
+      unsigned run = 0u;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int i = i0 + j;
@@ -310,78 +326,91 @@ intra_fused_kernel(FusedArgs a) {
         kand &= key;
         kor |= key;
         zeros += tok == 0;
-        S.items[i] = (key << 16) | static_cast<unsigned>(i);
+        S.kbi[i] = static_cast<unsigned short>(key);
+        S.idx16[i] = static_cast<unsigned short>(i);
         if (blk0 == blk7) {
-          run += 2ull * tok;
+          run += 2u * tok;
         } else {
           const unsigned qd = a.div_pg.div(static_cast<unsigned>(i));
-          atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2ull * tok);
+          atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2u * tok);
         }
       }
       if (blk0 == blk7) atomicAdd(&S.blk_ident[blk0], run);
     }
+  }
+  // sort padding: key 0xffff has the largest digit in every pass
+  for (int i = n + tid; i < kFusedSlots; i += kFusedT) {
+    S.kbi[i] = 0xffffu;
+    S.idx16[i] = static_cast<unsigned short>(i);
   }
   atomicAnd(&S.s_and, kand);
   atomicOr(&S.s_or, kor);
   int tot_zeros;
   block_excl_scan<kFusedT>(zeros, S.tmp, &tot_zeros);
   bool keep = false;
+  const int cap = (n + m - 1) / m;
+  const int capP = ((cap + 1) | 3) - 1;  // >= cap, == 2 mod 4
   if (a.intra) {
-  if (a.prof && tid == 0) a.prof[b * 8 + 1] = globaltimer();
-    // ---- 2. stable LSD radix sort by key over its varying bit window
+    if (a.prof && tid == 0) a.prof[b * 8 + 1] = globaltimer();
+    // ---- 2. stable LSD radix sort by key over its varying bit window; the
+    // last pass writes swizzled positions (at least one pass always runs)
     const unsigned varying = S.s_and ^ S.s_or;
     const int lo = varying ? __ffs(static_cast<int>(varying)) - 1 : 0;
-    const int hi = varying ? 32 - __clz(static_cast<int>(varying)) : 0;
-    for (int sh = lo; sh < hi; sh += kRB) {
-      const int bits = min(kRB, hi - sh);
+    const int hi = varying ? 32 - __clz(static_cast<int>(varying)) : 1;
+    for (int sh = lo; sh < hi; sh += kSortRB) {
+      const int bits = min(kSortRB, hi - sh);
       const unsigned mask = (1u << bits) - 1u;
-      tile_pass_u32<kFusedT, kFusedItems, kRB>(
-          S.items, n, [&](int, unsigned it) { return ((it >> 16) >> sh) & mask; }, S.radix_cnt,
-          S.tmp);
+      auto dig = [&](unsigned key) { return (key >> sh) & mask; };
+      // per-thread digit counters live in out16's bytes (free until the greedy)
+      unsigned* cw = reinterpret_cast<unsigned*>(S.out16);
+      if (sh + kSortRB >= hi)
+        tile_pass_blocked<kFusedT, kFusedItems, kSortRB, true>(S.idx16, S.kbi, dig, cw, S.tmp);
+      else
+        tile_pass_blocked<kFusedT, kFusedItems, kSortRB, false>(S.idx16, S.kbi, dig, cw, S.tmp);
     }
-  if (a.prof && tid == 0) a.prof[b * 8 + 2] = globaltimer();
-    // ---- 3. greedy equal-count partition (sizes = 2 * tokens)
+    if (a.prof && tid == 0) a.prof[b * 8 + 2] = globaltimer();
+    // ---- 3. greedy equal-count partition (sizes = 2 * tokens), emitted
+    // straight into the flat order's (group, slot) cells
     const int z0 = desc ? n - tot_zeros : 0;
     const int z1 = desc ? n : tot_zeros;
-    const int cap = (n + m - 1) / m;
-    auto size_at = [&](int k) -> long long {
-      const unsigned key = S.items[k] >> 16;
-      const long long tok = desc ? 0x7fff - static_cast<long long>(key) : key;
+    auto size_at = [&](int k) -> unsigned {
+      const unsigned key = S.kbi[S.idx16[swz(k)]];
+      const unsigned tok = desc ? 0x7fffu - key : key;
       return tok + tok;
     };
-    auto assign = [&](int k, int g, int) { S.grp[k] = static_cast<unsigned char>(g); };
-    GreedyState<long long> st{S.AL, S.AG, S.cnt, S.TL, S.TG, S.tmp, S.gload, S.tmpll};
+    auto emit = [&](int k, int g, int slot) {
+      S.out16[g * capP + slot] = static_cast<unsigned short>(k);
+    };
     if (desc)
-      greedy_rounds<kFusedT, 1, long long, false>(n, m, cap, z0, z1, size_at, assign, st);
+      greedy_fused<kFusedT, false>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp);
     else
-      greedy_rounds<kFusedT, 1, long long, true>(n, m, cap, z0, z1, size_at, assign, st);
-  if (a.prof && tid == 0) a.prof[b * 8 + 3] = globaltimer();
-    // ---- 4. flat order = sorted items stably partitioned by group: the
-    // items of a group keep assignment order (IntraPartition::flat).
-    tile_pass_u32<kFusedT, kFusedItems, kRB>(
-        S.items, n, [&](int pos, unsigned) { return static_cast<unsigned>(S.grp[pos]); },
-        S.radix_cnt, S.tmp);
-    // greedy block loads: group loads when blocks are groups, else sums over
-    // the flat order's blocks
+      greedy_fused<kFusedT, true>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp);
+    if (a.prof && tid == 0) a.prof[b * 8 + 3] = globaltimer();
+    // ---- 4. group offsets of the flat order and the greedy block loads
+    int c = tid < m ? S.G.gcnt[tid] : 0, tot;
+    const int o = block_excl_scan<kFusedT>(c, S.tmp, &tot);
+    if (tid < m) S.off[tid] = o;
     if (n % m == 0) {
-      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = static_cast<unsigned long long>(S.gload[g]);
+      // blocks are the groups (every group holds cap = n / m items)
+      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = S.G.gload[g];
     } else {
-      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = 0ull;
+      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = 0u;
       __syncthreads();
-      for (int pos = tid; pos < n; pos += kFusedT) {
-        const unsigned key = S.items[pos] >> 16;
-        const long long tok = desc ? 0x7fff - static_cast<long long>(key) : key;
-        atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], static_cast<unsigned long long>(tok + tok));
+      for (int g = w; g < m; g += kFusedT / 32) {
+        for (int slot = lane; slot < S.G.gcnt[g]; slot += 32) {
+          const int pos = S.off[g] + slot;
+          atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], size_at(S.out16[g * capP + slot]));
+        }
       }
     }
     __syncthreads();
-    long long mg = 0, mi = 0;
+    unsigned mg = 0u, mi = 0u;
     for (int g = tid; g < m; g += kFusedT) {
-      mg = max(mg, static_cast<long long>(S.blk_greedy[g]));
-      mi = max(mi, static_cast<long long>(S.blk_ident[g]));
+      mg = max(mg, S.blk_greedy[g]);
+      mi = max(mi, S.blk_ident[g]);
     }
-    mg = block_max_ll<kFusedT>(mg, S.tmpll);
-    mi = block_max_ll<kFusedT>(mi, S.tmpll);
+    mg = static_cast<unsigned>(block_max_ll<kFusedT>(mg, S.tmpll));
+    mi = static_cast<unsigned>(block_max_ll<kFusedT>(mi, S.tmpll));
     // src/reorder.cpp:350-353: keep the greedy split when its max block load
     // is no worse than the incoming order's (integer loads: exact).
     keep = mg <= mi;
@@ -392,16 +421,19 @@ intra_fused_kernel(FusedArgs a) {
   for (int g = tid; g < m; g += kFusedT)
     write_outputs_common(a, b, g, S.blk_ident[g], keep ? S.blk_greedy[g] : S.blk_ident[g]);
   if (a.prof && tid == 0) a.prof[b * 8 + 4] = globaltimer();
-  // ---- 5. outputs, coalesced: the intra order and, when the greedy split is
-  // kept, its per-position tokens (identity batches reuse the cost pass's
-  // tokens, see TokSrc)
+  // ---- 5. outputs, coalesced: one warp per group, lanes over its slots —
+  // the intra order and, when the greedy split is kept, its per-position
+  // tokens (identity batches reuse the cost pass's tokens, see TokSrc)
   if (keep) {
-    for (int pos = tid; pos < n; pos += kFusedT) {
-      const unsigned it = S.items[pos];
-      const unsigned key = it >> 16;
-      a.order_out[first + pos] = static_cast<int>(it & 0xffffu);
-      if (a.tok16_staged != nullptr)
-        a.tok16_staged[first + pos] = static_cast<unsigned short>(desc ? 0x7fffu - key : key);
+    for (int g = w; g < m; g += kFusedT / 32) {
+      const int base = S.off[g], cnt = S.G.gcnt[g];
+      for (int slot = lane; slot < cnt; slot += 32) {
+        const unsigned idx = S.idx16[swz(S.out16[g * capP + slot])];
+        const unsigned key = S.kbi[idx];
+        a.order_out[first + base + slot] = static_cast<int>(idx);
+        if (a.tok16_staged != nullptr)
+          a.tok16_staged[first + base + slot] = static_cast<unsigned short>(desc ? 0x7fffu - key : key);
+      }
     }
   } else {
     for (int i = tid; i < n; i += kFusedT) a.order_out[first + i] = i;
