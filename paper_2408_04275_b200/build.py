@@ -25,8 +25,9 @@ FLAGS = [
     "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
     "--expt-relaxed-constexpr",
 ] + [f"-D{d}" for d in os.environ.get("DTB_DEFINES", "").split() if d]
-if os.environ.get("DTB_DEFINES"):
+if os.environ.get("DTB_DEFINES"):  # experiment builds stay out of the product path
     OBJ = OBJ + "_" + "_".join(os.environ["DTB_DEFINES"].split()).replace("=", "")
+    OUT = os.path.join(OBJ, "libdisttrain_b200.so")
 SOURCES = ["capi.cu", "k_intra.cu", "k_sched.cu", "k_inter.cu", "k_orch.cu", "k_misc.cu"]
 
 

@@ -6,6 +6,10 @@
 #include "kernels.cuh"
 #include "sched.cuh"
 
+#ifndef DTB_SIM_EXPERIMENT
+#define DTB_SIM_EXPERIMENT 0
+#endif
+
 namespace dtb {
 
 // StageTimes::valid (pipeline_sim.cpp:214-230): 0 ok, 1 negative/NaN fwd,
@@ -694,58 +698,129 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
       gB[0] = r.gb;
       tick_iter(i, i < P - 1);
     }
+    for (int i = l; i < l + P - 1; ++i) {
+      shift();
+      tick_iter(i, true);
+    }
   } else {
-    // chunk k = microbatches [k*C, k*C + C): its token sums are loaded one
-    // chunk ahead (one vector load when the layout allows), its cost-table
-    // rows are all in flight before the chunk's first tick.
-    const bool vec = ord == nullptr && (l % C) == 0;
+    // Chunks of P microbatches, two row rings (rA, rB) used alternately:
+    // iteration j of a chunk reads delay d from cur[j - d] or, across the
+    // chunk boundary, prev[j - d + P] — every index is a compile-time
+    // constant, so the delay lines cost no register moves.  A chunk's
+    // cost-table rows are all in flight before its first tick; its token
+    // sums were loaded two chunks ahead (vector loads when possible).
+    const bool vec = ord == nullptr && (P % 4) == 0 && (l % 4) == 0;
     auto tokens = [&](int i0, int* tk) {
       if (i0 >= l) return;
+#if DTB_SIM_EXPERIMENT == 2
+#pragma unroll
+      for (int j = 0; j < P; ++j) tk[j] = (i0 + j) & 1023;
+      return;
+#endif
       if (vec) {
-        if (t16) {
-          const uint2 v = __ldg(reinterpret_cast<const uint2*>(t16 + i0));
-          tk[0] = v.x & 0xffff;
-          tk[1] = v.x >> 16;
-          tk[2] = v.y & 0xffff;
-          tk[3] = v.y >> 16;
-        } else {
-          const int4 v = __ldg(reinterpret_cast<const int4*>(t32 + i0));
-          tk[0] = v.x;
-          tk[1] = v.y;
-          tk[2] = v.z;
-          tk[3] = v.w;
+#pragma unroll
+        for (int j = 0; j < P; j += 4) {
+          if (t16) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(t16 + i0 + j));
+            tk[j] = v.x & 0xffff;
+            tk[j + 1] = v.x >> 16;
+            tk[j + 2] = v.y & 0xffff;
+            tk[j + 3] = v.y >> 16;
+          } else {
+            const int4 v = __ldg(reinterpret_cast<const int4*>(t32 + i0 + j));
+            tk[j] = v.x;
+            tk[j + 1] = v.y;
+            tk[j + 2] = v.z;
+            tk[j + 3] = v.w;
+          }
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < C; ++j) tk[j] = i0 + j < l ? token(i0 + j) : 0;
+        for (int j = 0; j < P; ++j) tk[j] = i0 + j < l ? token(i0 + j) : 0;
       }
     };
-    int tk[C] = {}, tk_next[C] = {};
-    tokens(0, tk_next);
-    for (int i0 = 0; i0 < l; i0 += C) {
+    auto tick_ring = [&](int i, bool check, const double4* cur, const double4* prev, int j) {
+      // j is a compile-time constant at every call site (fully unrolled)
+      double pv[P];
 #pragma unroll
-      for (int j = 0; j < C; ++j) tk[j] = tk_next[j];
-      tokens(i0 + C, tk_next);
-      double4 row[C];
+      for (int s = 0; s < P; ++s) pv[s] = av[s];
+      auto row = [&](int d) -> const double4& { return j - d >= 0 ? cur[j - d] : prev[j - d + P]; };
+      auto du = [&](int s, bool fwd, int d) -> double {
+        return s < PE ? (fwd ? row(d).x : row(d).y)
+                      : s < PE + PB ? (fwd ? fB : bB) : (fwd ? row(d).z : row(d).w);
+      };
 #pragma unroll
-      for (int j = 0; j < C; ++j) row[j] = ld_row(a.table.eg + tk[j]);
-#pragma unroll
-      for (int j = 0; j < C; ++j) {
-        const int i = i0 + j;
-        if (i >= l) break;
-        shift();
-        eF[0] = row[j].x;
-        eB[0] = row[j].y;
-        gF[0] = row[j].z;
-        gB[0] = row[j].w;
-        if (i < P - 1) tick_iter(i, true);
-        else tick_iter(i, false);
+      for (int s = 0; s < P; ++s) {
+        const bool fwd = (s & 1) == 0;
+        const int d = fwd ? s / 2 : P - (s + 1) / 2;
+        const int mb = i - d;
+        if (!check || (mb >= 0 && mb < l)) {
+          const double x = du(s, fwd, d);
+          const double dep = fwd ? (s > 0 ? pv[s - 1] : 0.0) : (s + 1 < P ? pv[s + 1] : pv[s]);
+          const double start = (s == 0 && fwd) || (s == P - 1 && !fwd) ? av[s] : fmax(av[s], dep);
+          av[s] = start + x;
+          if (BUSY) busy[s] += x;
+        }
       }
+#pragma unroll
+      for (int s = 0; s < P; ++s) pv[s] = av[s];
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const bool fwd = (s & 1) == 1;
+        const int d = fwd ? (s - 1) / 2 : P - 1 - s / 2;
+        const int mb = i - d;
+        if (!check || (mb >= 0 && mb < l)) {
+          const double x = du(s, fwd, d);
+          const double dep = fwd ? pv[s - 1] : (s + 1 < P ? pv[s + 1] : pv[s]);
+          const double start = (s == P - 1 && !fwd) ? av[s] : fmax(av[s], dep);
+          av[s] = start + x;
+          if (BUSY) busy[s] += x;
+        }
+      }
+    };
+    // rows of chunk c + 1 are loaded (nxt) while chunk c ticks; at the chunk
+    // boundary they become `cur`
+    auto run_chunk = [&](int i0, double4* cur, const double4* prev) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        const int i = i0 + j;
+        if (i >= l + P - 1) break;
+        if (i < P - 1 || i >= l) tick_ring(i, true, cur, prev, j);
+        else tick_ring(i, false, cur, prev, j);
+      }
+    };
+    double4 rA[P], rB[P], nxt[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) rA[j] = rB[j] = make_double4(0.0, 0.0, 0.0, 0.0);
+    // token sums run one chunk ahead of the rows they address
+    int tk[P] = {}, tk_next[P] = {};
+    tokens(0, tk_next);
+    auto load_rows = [&](int i0) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) tk[j] = tk_next[j];
+      tokens(i0 + P, tk_next);
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+        if (i0 + j < l) {
+#if DTB_SIM_EXPERIMENT == 1
+          const double x = static_cast<double>(tk[j]);
+          nxt[j] = make_double4(x, x + 1.0, x + 2.0, x + 3.0);
+#else
+          nxt[j] = ld_row(a.table.eg + tk[j]);
+#endif
+        }
+    };
+    load_rows(0);
+    for (int i0 = 0; i0 < l + P - 1; i0 += 2 * P) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) rA[j] = nxt[j];
+      load_rows(i0 + P);
+      run_chunk(i0, rA, rB);
+#pragma unroll
+      for (int j = 0; j < P; ++j) rB[j] = nxt[j];
+      load_rows(i0 + 2 * P);
+      run_chunk(i0 + P, rB, rA);
     }
-  }
-  for (int i = l; i < l + P - 1; ++i) {
-    shift();
-    tick_iter(i, true);
   }
   double iter = 0.0;
 #pragma unroll
@@ -770,7 +845,7 @@ __device__ __noinline__ void sim_group_direct(const GroupSimArgs* a, long long g
 }
 
 template <int PE, int PB, int PG, bool BUSY>
-__global__ void __launch_bounds__(kSimT, 5)
+__global__ void __launch_bounds__(kSimT, 4)
 group_sims_tiled(const __grid_constant__ GroupSimArgs a) {
   const long long gid = blockIdx.x * static_cast<long long>(kSimT) + threadIdx.x;
   if (gid >= a.n_batches * a.groups) return;
