@@ -58,6 +58,7 @@ const char* kind_name(int k) {
 struct dtb_context {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-buffer pipelines (lazy)
   DevErr* err = nullptr;  // device
 };
 
@@ -316,6 +317,8 @@ dtb_status dtb_context_destroy(dtb_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->err);
   cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+  if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
   delete ctx;
   return DTB_OK;
 }
@@ -1057,28 +1060,109 @@ dtb_status dtb_reorder_stream(dtb_context* ctx, const dtb_cost_model* cm, const 
   const dtb_reorder_mode def{1, 1, DTB_ASCENDING};
   const dtb_reorder_mode* md = mode ? mode : &def;
   TRY(stream_checks(cm, plan, md, samples->n, n_batches));
+  if (samples->image_offsets == nullptr)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "samples need image_offsets");
   cudaStream_t s = ctx->stream;
   TRY(reset_err(ctx));
-  DevSamples d;
-  TRY(upload_samples(samples, s, &d));
+  // Host buffers in, host buffers out, pipelined over chunks of global
+  // batches (batches are independent): the host->device copy of chunk c+1
+  // and the device->host copy of chunk c-1 overlap the kernels of chunk c
+  // (copy_in / compute / copy_out streams ordered by events).  Device
+  // buffers are full-size, so the CSR offsets stay absolute.
+  if (ctx->copy_in == nullptr) {
+    CU(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+  }
   const long long total = samples->n;
+  const long long bs = plan->global_batch;
   const int dp = plan->unit[DTB_BACKBONE].dp;
-  DBuf o, lb, la, tb, ta, kp;
+  const bool audio = samples->audio_offsets != nullptr;
+  const long long ni = samples->image_offsets[total];
+  const long long na = audio ? samples->audio_offsets[total] : 0;
+  DBuf io, it, ao, at, o, lb, la, tb, ta, kp;
+  CU(io.alloc(4ull * (total + 1), s));
+  CU(it.alloc(4ull * ni, s));
+  if (audio) {
+    CU(ao.alloc(4ull * (total + 1), s));
+    CU(at.alloc(4ull * na, s));
+  }
   CU(o.alloc(4ull * total, s));
   CU(lb.alloc(8ull * n_batches * dp, s));
   CU(la.alloc(8ull * n_batches * dp, s));
   CU(tb.alloc(8ull * n_batches, s));
   CU(ta.alloc(8ull * n_batches, s));
   CU(kp.alloc(n_batches, s));
-  TRY(run_stream(ctx, cm, plan, md, d.img_off, d.img_tok, d.aud_off, d.aud_tok, n_batches,
-                 o.as<int>(), lb.as<double>(), la.as<double>(), tb.as<double>(), ta.as<double>(),
-                 kp.as<unsigned char>(), s));
-  TRY(download(output_order, o, total, s));
-  TRY(download(load_before, lb, n_batches * dp, s));
-  TRY(download(load_after, la, n_batches * dp, s));
-  TRY(download(t_iter_before, tb, n_batches, s));
-  TRY(download(t_iter_after, ta, n_batches, s));
-  TRY(download(greedy_kept, kp, n_batches, s));
+  cudaEvent_t ready;
+  CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CU(cudaEventRecord(ready, s));  // allocations + error reset are ordered first
+  CU(cudaStreamWaitEvent(ctx->copy_in, ready, 0));
+  CU(cudaStreamWaitEvent(ctx->copy_out, ready, 0));
+  const long long chunk = std::max<long long>(16, (n_batches + 7) / 8);
+  const long long n_chunks = n_batches > 0 ? (n_batches + chunk - 1) / chunk : 0;
+  std::vector<cudaEvent_t> in_done(n_chunks), run_done(n_chunks);
+  dtb_status st = DTB_OK;
+  auto h2d = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy_in)
+                 : cudaSuccess;
+  };
+  auto d2h = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    return (bytes && dst) ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->copy_out)
+                          : cudaSuccess;
+  };
+  for (long long c = 0; c < n_chunks && st == DTB_OK; ++c) {
+    const long long b0 = c * chunk, nb = std::min(chunk, n_batches - b0);
+    const long long s0 = b0 * bs, s1 = (b0 + nb) * bs;
+    cudaError_t e = cudaEventCreateWithFlags(&in_done[c], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&run_done[c], cudaEventDisableTiming);
+    // inputs of the chunk: offsets [s0, s1] and their token ranges
+    const long long i0 = samples->image_offsets[s0], i1 = samples->image_offsets[s1];
+    if (e == cudaSuccess)
+      e = h2d(io.as<int>() + s0, samples->image_offsets + s0, 4ull * (s1 - s0 + 1));
+    if (e == cudaSuccess) e = h2d(it.as<int>() + i0, samples->image_tokens + i0, 4ull * (i1 - i0));
+    if (audio && e == cudaSuccess) {
+      const long long a0 = samples->audio_offsets[s0], a1 = samples->audio_offsets[s1];
+      e = h2d(ao.as<int>() + s0, samples->audio_offsets + s0, 4ull * (s1 - s0 + 1));
+      if (e == cudaSuccess) e = h2d(at.as<int>() + a0, samples->audio_tokens + a0, 4ull * (a1 - a0));
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(in_done[c], ctx->copy_in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, in_done[c], 0);
+    if (e != cudaSuccess) {
+      st = fail(DTB_ERR_CUDA, "%s", cudaGetErrorString(e));
+      break;
+    }
+    st = run_stream(ctx, cm, plan, md, io.as<int>() + s0, it.as<int>(),
+                    audio ? ao.as<int>() + s0 : nullptr, audio ? at.as<int>() : nullptr, nb,
+                    o.as<int>() + s0, lb.as<double>() + b0 * dp, la.as<double>() + b0 * dp,
+                    tb.as<double>() + b0, ta.as<double>() + b0, kp.as<unsigned char>() + b0, s);
+    if (st != DTB_OK) break;
+    e = cudaEventRecord(run_done[c], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy_out, run_done[c], 0);
+    if (e == cudaSuccess) e = d2h(output_order ? output_order + s0 : nullptr, o.as<int>() + s0,
+                                  4ull * (s1 - s0));
+    if (e == cudaSuccess)
+      e = d2h(load_before ? load_before + b0 * dp : nullptr, lb.as<double>() + b0 * dp,
+              8ull * nb * dp);
+    if (e == cudaSuccess)
+      e = d2h(load_after ? load_after + b0 * dp : nullptr, la.as<double>() + b0 * dp,
+              8ull * nb * dp);
+    if (e == cudaSuccess)
+      e = d2h(t_iter_before ? t_iter_before + b0 : nullptr, tb.as<double>() + b0, 8ull * nb);
+    if (e == cudaSuccess)
+      e = d2h(t_iter_after ? t_iter_after + b0 : nullptr, ta.as<double>() + b0, 8ull * nb);
+    if (e == cudaSuccess)
+      e = d2h(greedy_kept ? greedy_kept + b0 : nullptr, kp.as<unsigned char>() + b0, nb);
+    if (e != cudaSuccess) st = fail(DTB_ERR_CUDA, "%s", cudaGetErrorString(e));
+  }
+  // everything (copies included) completes before buffers are released
+  cudaStreamSynchronize(ctx->copy_in);
+  cudaStreamSynchronize(ctx->copy_out);
+  cudaStreamSynchronize(s);
+  for (long long c = 0; c < n_chunks; ++c) {
+    if (in_done[c]) cudaEventDestroy(in_done[c]);
+    if (run_done[c]) cudaEventDestroy(run_done[c]);
+  }
+  cudaEventDestroy(ready);
+  if (st != DTB_OK) return st;
   return sync_and_check(ctx);
 }
 
