@@ -1015,14 +1015,16 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ia.span = span;
   ia.table = table;
   ia.err = ctx->err;
-  const size_t inter_bytes = mode->inter ? inter_scratch(ia) : 0;
+  const bool inter_tok = mode->inter && inter_tok_applies(ia);
+  const size_t inter_bytes = mode->inter && !inter_tok ? inter_scratch(ia) : 0;
   CU(scr.alloc(std::max(sim_bytes, inter_bytes), s));
   CU(launch_group_sims(ga, scr.p, s));
   CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, tb, s));
   if (mode->inter) {
     CU(inter.alloc(4ull * n_mb, s));
     ia.orders = inter.as<int>();
-    CU(launch_inter(ia, scr.p, inter_bytes, s));
+    if (inter_tok) CU(launch_inter_tok(ia, s));
+    else CU(launch_inter(ia, scr.p, inter_bytes, s));
   }
   if (compose_needed)
     CU(launch_compose(n_batches, n, dp_lm, dp_me, intra_out, mode->inter ? inter.as<int>() : nullptr,

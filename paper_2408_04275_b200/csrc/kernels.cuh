@@ -207,6 +207,10 @@ struct InterArgs {
 };
 cudaError_t launch_inter(const InterArgs& a, void* scratch, size_t bytes,
                          cudaStream_t stream);
+// Shared-memory kernel for the stream token form (vpp == 1, compiled stage
+// layouts); cudaErrorNotSupported when it does not apply.
+cudaError_t launch_inter_tok(const InterArgs& a, cudaStream_t stream);
+bool inter_tok_applies(const InterArgs& a);
 size_t inter_scratch(const InterArgs& a);
 
 // --------------------------------------------------------- orchestration
