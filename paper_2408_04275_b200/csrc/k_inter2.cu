@@ -56,9 +56,13 @@ __device__ __noinline__ Row4 inter_row_direct(const InterArgs* a, long long te, 
 
 }  // namespace
 
-// Shared memory per thread (bytes) and per CTA.
+// Backward rows of recently placed positions, kept on chip: the windows
+// only ever read backward cells of positions within kBRing of the frontier.
+constexpr int kBRing = 16;
+
+// Shared memory per thread (bytes).
 __host__ __device__ inline size_t inter_tok_bytes_per_thread(int l) {
-  return static_cast<size_t>(l) * (3 * 8 + 2 + 1);
+  return static_cast<size_t>(l) * (3 * 8 + 2 + 1) + 2 * 8 * kBRing;
 }
 
 template <int PE, int PB, int PG>
@@ -74,7 +78,11 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   double* colG = colF + static_cast<size_t>(l) * T;  // [l][T] generator F
   double* colK = colG + static_cast<size_t>(l) * T;  // [l][T] forward keys
   auto* colT = reinterpret_cast<unsigned short*>(colK + static_cast<size_t>(l) * T);  // tokens
-  unsigned char* colR = reinterpret_cast<unsigned char*>(colT + static_cast<size_t>(l) * T);  // ret
+  // backward ring [kBRing][T] (encoder, generator), 8-byte aligned after the u16 tokens
+  double* colBE = reinterpret_cast<double*>(
+      (reinterpret_cast<size_t>(colT + static_cast<size_t>(l) * T) + 7) & ~size_t(7));
+  double* colBG = colBE + static_cast<size_t>(kBRing) * T;
+  unsigned char* colR = reinterpret_cast<unsigned char*>(colBG + static_cast<size_t>(kBRing) * T);
 
   UnitEval ub;
   ub.init(a.cm, a.plan, DTB_BACKBONE);
@@ -97,6 +105,8 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   auto K = [&](int i) -> double& { return colK[static_cast<size_t>(i) * T + t]; };
   auto TK = [&](int i) -> unsigned short& { return colT[static_cast<size_t>(i) * T + t]; };
   auto RET = [&](int i) -> unsigned char& { return colR[static_cast<size_t>(i) * T + t]; };
+  auto BE = [&](int pos) -> double& { return colBE[static_cast<size_t>(pos % kBRing) * T + t]; };
+  auto BG = [&](int pos) -> double& { return colBG[static_cast<size_t>(pos % kBRing) * T + t]; };
 
   // ---- fill: rows of the problem's microbatches (staged order)
   const long long bb = prob / a.groups;
@@ -155,6 +165,13 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     pend[w] = lo >= l ? 0u : (l - lo >= 32 ? 0xffffffffu : ((1u << (l - lo)) - 1u));
   }
   int npend = l;
+  auto pend_word = [&](int w) -> unsigned {
+    unsigned r = 0u;
+#pragma unroll
+    for (int z = 0; z < MW; ++z)
+      if (z == w) r = pend[z];
+    return r;
+  };
   auto clear = [&](int idx) {
 #pragma unroll
     for (int w = 0; w < MW; ++w)
@@ -179,33 +196,41 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     }
     return best;
   };
-  // select_closest, one pick: smallest (|r - key|, key > r, index)
+  // select_closest, one pick: smallest (|r - key|, key > r, index).  A
+  // uniform loop over all indices (lanes of a warp hold different problems
+  // whose pending sets differ; bit-scan loops would diverge)
   auto pick_closest = [&](double residual) -> int {
     int best = -1;
     double db = 0.0;
     bool bover = false;
-#pragma unroll
-    for (int w = 0; w < MW; ++w) {
-      unsigned m = pend[w];
-      while (m) {
-        const int idx = w * 32 + __ffs(m) - 1;
-        m &= m - 1;
+    for (int w = 0; w * 32 < l; ++w) {
+      const unsigned m = pend_word(w);
+      const int hi = min(32, l - w * 32);
+#pragma unroll 4
+      for (int b = 0; b < hi; ++b) {
+        const int idx = w * 32 + b;
         const double k = K(idx);
         const double da = fabs(residual - k);
         const bool over = !(k <= residual);
-        if (best < 0 || da < db || (da == db && !over && bover)) {
-          best = idx;
-          db = da;
-          bover = over;
-        }
+        const bool take = ((m >> b) & 1u) && (best < 0 || da < db || (da == db && !over && bover));
+        best = take ? idx : best;
+        db = take ? da : db;
+        bover = take ? over : bover;
       }
     }
     return best;
   };
 
   int nret = 0;
+  auto place = [&](int idx) {
+    double eb, gb;
+    bwd_row(idx, &eb, &gb);
+    BE(nret) = eb;
+    BG(nret) = gb;
+    RET(nret++) = static_cast<unsigned char>(idx);
+  };
   const int first = pick_min();
-  RET(nret++) = static_cast<unsigned char>(first);
+  place(first);
   clear(first);
   --npend;
   const int tail_n = min(DEV - 1, npend);
@@ -281,6 +306,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
       return s < PE ? bmeanE : s < PE + PB ? bmeanB : bmeanG;
     }
     if (s >= PE && s < PE + PB) return bB;
+    if (r < np && r + kBRing >= nret) return s < PE ? BE(r) : BG(r);
     const int row = r < np ? static_cast<int>(RET(r)) : rear_row(r - np - npend);
     double eb, gb;
     bwd_row(row, &eb, &gb);
@@ -329,15 +355,20 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     const int t_target = 2 * wi + 2 * P - 1;  // tick of B(wi, 0)
     // pending means per unit: sequential sums in ascending index order
     {
+      // x + 0.0 == x for every partial sum here (never -0.0: all terms are
+      // >= +0), so non-pending rows contribute an exact +0.0 and the loop
+      // is uniform across the warp
       double sE = 0.0, sG = 0.0;
-#pragma unroll
-      for (int w = 0; w < MW; ++w) {
-        unsigned m = pend[w];
-        while (m) {
-          const int idx = w * 32 + __ffs(m) - 1;
-          m &= m - 1;
-          sE += F(idx);
-          sG += G(idx);
+      for (int w = 0; w * 32 < l; ++w) {
+        const unsigned m = pend_word(w);
+        const int hi = min(32, l - w * 32);
+#pragma unroll 4
+        for (int b = 0; b < hi; ++b) {
+          const bool on = (m >> b) & 1u;
+          const int idx = w * 32 + b;
+          const double f = F(idx), g = G(idx);
+          sE += on ? f : 0.0;
+          sG += on ? g : 0.0;
         }
       }
       const double c = static_cast<double>(npend);
@@ -370,7 +401,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     for (int q = 0; q < take; ++q) {
       const int pick = pick_closest(residual);
       residual -= K(pick);
-      RET(nret++) = static_cast<unsigned char>(pick);
+      place(pick);
       clear(pick);
       --npend;
     }
@@ -428,8 +459,8 @@ cudaError_t launch_inter_tok(const InterArgs& a, cudaStream_t stream) {
   const size_t fixed = 8 * static_cast<size_t>(a.l + 1) + 64;
   const size_t per = inter_tok_bytes_per_thread(a.l);
   int T = 128;
-  while (T > 32 && fixed + per * T > static_cast<size_t>(max_smem)) T -= 32;
-  const size_t bytes = fixed + per * T;
+  while (T > 1 && fixed + per * T + 64 > static_cast<size_t>(max_smem)) --T;
+  const size_t bytes = fixed + per * T + 64;  // + alignment slack of the ring
   if (bytes > static_cast<size_t>(max_smem)) return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(bytes));
