@@ -12,10 +12,11 @@ the north_star's HBM target names.  The full default mode (intra + inter)
 and the orchestration search (BASELINE config 3) are measured too and
 reported under "modes" / "search".
 
-N GPUs (torchrun): the stream is split by global-batch range (strong
-scaling, 16M total); no collective on the data path.  `value` = all
-samples / max-over-ranks device time.  "gather" additionally times an NCCL
-all-gather of every rank's output orders (the concatenated ordering).
+N GPUs (torchrun): weak scaling — every rank reorders its own 16M-sample
+shard (global batches are independent; no collective on the data path).
+`value` = all ranks' samples / max-over-ranks device time.  "strong" times
+ONE 16M stream split by batch range (shard.batch_range) and, with
+"with_gather", an NCCL all-gather of the output orders.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref,
 compiled from the reference sources; the C restatement if absent) on all
@@ -212,7 +213,7 @@ def reference_arm(args, model, cluster, book, plan_c):
     v = sample_batches * BS / t
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
             "n_gpus": args.gpus, "steps": len(times), "warmup": min(args.warmup, 1),
-            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64 tokens / f64 loads and stage times",
             "data": "synthetic (PCG64 mixed image+audio stream)",
             "config": {"workload": "BASELINE config 4: global batch 16384, DP 128, PP 1/2/1, "
@@ -230,6 +231,7 @@ def main():
     rank, world, local = dist_init()
     model, cluster, book, plan = workload()
     from paper_2408_04275_b200 import _capi as A
+    from paper_2408_04275_b200 import shard
     from paper_2408_04275_b200.workload import synth_stream
 
     plan_c = plan.to_c()
@@ -246,9 +248,11 @@ def main():
     cm = pl.cost_model(model, cluster, book)
     mode_intra, mode_both = A.ReorderMode(1, 0, 0), A.ReorderMode(1, 1, 0)
 
-    n_batches_total = args.samples // BS
-    my_batches = n_batches_total // world + (1 if rank < n_batches_total % world else 0)
-    first_batch = rank * (n_batches_total // world) + min(rank, n_batches_total % world)
+    # Weak scaling: every rank reorders its own 16M-sample shard (1,024
+    # global batches) of a world x 16M stream — global batches are
+    # independent, so there is no data-path collective.
+    my_batches = args.samples // BS
+    first_batch = rank * my_batches
     samples = synth_stream(my_batches * BS, seed=1000 + first_batch, family="mixed")
     n = samples.n
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
@@ -266,10 +270,10 @@ def main():
     sh = C.c_void_p(stream.cuda_stream)
     ptr = lambda t: C.c_void_p(t.data_ptr())
 
-    def step(mode):
-        pl._check(lib.reorder_stream_dev(pl.ctx, cm.h, C.byref(plan_c), C.byref(mode), C.byref(ds),
-                                         my_batches, ptr(out_order), ptr(lb), ptr(la), ptr(tb),
-                                         ptr(ta), ptr(kept), sh))
+    def step(mode, sub=None, nb=my_batches):
+        pl._check(lib.reorder_stream_dev(pl.ctx, cm.h, C.byref(plan_c), C.byref(mode),
+                                         C.byref(sub or ds), nb, ptr(out_order), ptr(lb),
+                                         ptr(la), ptr(tb), ptr(ta), ptr(kept), sh))
 
     def sort_partition():
         pl._check(lib.intra_stream_dev(pl.ctx, BS, DP, 0, C.byref(ds), my_batches,
@@ -298,15 +302,17 @@ def main():
     with Clocks(local) as clk:
         ms_local = timed(lambda: step(mode_intra), args.steps, args.warmup)
     ms = max_over_ranks(ms_local, world)
-    total = n_batches_total * BS
+    total = my_batches * BS * world
     out = {"metric": METRIC, "value": total / (ms / 1e3), "unit": "samples/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "int32 tokens / int64 loads / f64 stage times (u16 sort keys)",
            "data": "synthetic (PCG64 mixed image+audio stream; desk-shaped cost profile)",
-           "config": {"workload": "BASELINE config 4: 16M-sample stream, global batch 16384, "
-                                  "DP 128, PP 1/2/1, disaggregated_reorder ReorderMode{intra}",
-                      "samples": total, "global_batch": BS, "dp": DP,
+           "config": {"workload": "BASELINE config 4: 16M-sample stream per GPU, global batch "
+                                  "16384, DP 128, PP 1/2/1, disaggregated_reorder "
+                                  "ReorderMode{intra}",
+                      "samples": total, "samples_per_gpu": my_batches * BS, "global_batch": BS,
+                      "dp": DP,
                       "parallelism": f"global-batch-range sharding over {world} GPU(s), "
                                      "no data-path collective",
                       "l2": "256 MiB buffer written between timed steps (inputs also > L2)"},
@@ -331,22 +337,72 @@ def main():
     out["roofline"] = {
         "bound": "hbm", "kernel": "token_keys_kernel + intra_fused_kernel (sort/partition path)",
         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-        "traffic": (tr["bytes_per_launch_16M"] * my_batches / n_batches_total) if tr else None,
+        "traffic": tr.get("bytes_per_step_16M") if tr else None,
         "algorithmic_bytes_per_launch": algo, "ms_per_launch": sp_local,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650"}
 
     if world > 1:
+        # strong-scaling view: ONE 16M stream split by batch range, plus the
         # concatenated ordering on every rank (NCCL all-gather over NVLink)
         import torch.distributed as dist
-        full = torch.empty(n * world, dtype=torch.int32, device="cuda")
-        if n_batches_total % world == 0:
+        first, count = shard.batch_range(my_batches, rank, world)
+        io = samples.image_offsets
+        sub = A.Samples(count * BS, None,
+                        C.cast(d_csr[0].data_ptr() + 4 * first * BS, C.POINTER(C.c_int32)),
+                        C.cast(d_csr[1].data_ptr(), C.POINTER(C.c_int32)),
+                        C.cast(d_csr[2].data_ptr() + 4 * first * BS, C.POINTER(C.c_int32)),
+                        C.cast(d_csr[3].data_ptr(), C.POINTER(C.c_int32)))
+        s_ms = max_over_ranks(timed(lambda: step(mode_intra, sub, count), args.steps,
+                                    args.warmup), world)
+        out["strong"] = {"samples": my_batches * BS, "ms_per_step": s_ms,
+                         "value": my_batches * BS / (s_ms / 1e3), "unit": "samples/s"}
+        if my_batches % world == 0:
+            full = torch.empty(my_batches * BS, dtype=torch.int32, device="cuda")
+            part = out_order[:count * BS]
+
             def gather():
-                step(mode_intra)
+                step(mode_intra, sub, count)
                 with torch.cuda.stream(stream):
-                    dist.all_gather_into_tensor(full, out_order)
+                    dist.all_gather_into_tensor(full, part)
             g_ms = max_over_ranks(timed(gather, max(2, args.steps // 2), 1), world)
-            out["gather"] = {"ms_per_step": g_ms, "value": total / (g_ms / 1e3),
-                             "unit": "samples/s", "collective": "all_gather_into_tensor(int32)"}
+            out["strong"]["with_gather"] = {
+                "ms_per_step": g_ms, "value": my_batches * BS / (g_ms / 1e3),
+                "collective": "all_gather_into_tensor(int32 output orders)"}
+
+    if not args.no_extras:
+        # e2e on every rank: host CSR (pinned) -> device -> results back,
+        # through the public C ABI (dtb_reorder_stream, copy/compute pipelined)
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_csr = [pin(samples.image_offsets), pin(samples.image_tokens),
+                 pin(samples.audio_offsets), pin(samples.audio_tokens)]
+        hs = A.Samples(n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32)) for x in h_csr])
+        h_order = torch.empty(n, dtype=torch.int32).pin_memory()
+        h_lb = torch.empty(my_batches * DP, dtype=torch.float64).pin_memory()
+        h_la = torch.empty_like(h_lb).pin_memory()
+        h_tb = torch.empty(my_batches, dtype=torch.float64).pin_memory()
+        h_ta = torch.empty_like(h_tb).pin_memory()
+        h_kept = torch.empty(my_batches, dtype=torch.uint8).pin_memory()
+        P = lambda t, ct: C.cast(t.data_ptr(), C.POINTER(ct))
+
+        def e2e():
+            pl._check(lib.reorder_stream(pl.ctx, cm.h, C.byref(plan_c), C.byref(mode_intra),
+                                         C.byref(hs), my_batches, P(h_order, C.c_int32),
+                                         P(h_lb, C.c_double), P(h_la, C.c_double),
+                                         P(h_tb, C.c_double), P(h_ta, C.c_double),
+                                         P(h_kept, C.c_uint8)))
+        e2e()
+        reps = max(3, args.steps // 2)
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e()
+        e_dt = max_over_ranks((time.perf_counter() - t0) / reps, world)
+        h2d = sum(x.numel() * x.element_size() for x in h_csr)
+        d2h = sum(x.numel() * x.element_size() for x in (h_order, h_lb, h_la, h_tb, h_ta, h_kept))
+        out["e2e"] = {"value": total / e_dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h, "ms_per_step": e_dt * 1e3,
+                      "path": "dtb_reorder_stream (host pointers, pinned; per-rank bytes, "
+                              "max over ranks)"}
 
     if not args.no_extras and rank == 0 and world == 1:
         # full default mode (intra + inter)
@@ -373,36 +429,6 @@ def main():
                          "ms_per_search": s_dt * 1e3, "candidates": res.candidates_evaluated,
                          "timing": "host wall clock around the C-ABI call (includes "
                                    "enumeration, solve, reduce, D2H)"}
-        # e2e: host CSR (pinned) -> device -> result back, through the public C ABI
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        h_csr = [pin(samples.image_offsets), pin(samples.image_tokens),
-                 pin(samples.audio_offsets), pin(samples.audio_tokens)]
-        hs = A.Samples(n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32)) for x in h_csr])
-        h_order = torch.empty(n, dtype=torch.int32).pin_memory()
-        h_lb = torch.empty(my_batches * DP, dtype=torch.float64).pin_memory()
-        h_la = torch.empty_like(h_lb).pin_memory()
-        h_tb = torch.empty(my_batches, dtype=torch.float64).pin_memory()
-        h_ta = torch.empty_like(h_tb).pin_memory()
-        h_kept = torch.empty(my_batches, dtype=torch.uint8).pin_memory()
-        P = lambda t, ct: C.cast(t.data_ptr(), C.POINTER(ct))
-
-        def e2e():
-            pl._check(lib.reorder_stream(pl.ctx, cm.h, C.byref(plan_c), C.byref(mode_intra),
-                                         C.byref(hs), my_batches, P(h_order, C.c_int32),
-                                         P(h_lb, C.c_double), P(h_la, C.c_double),
-                                         P(h_tb, C.c_double), P(h_ta, C.c_double),
-                                         P(h_kept, C.c_uint8)))
-        e2e()
-        reps = max(3, args.steps // 2)
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            e2e()
-        e_dt = (time.perf_counter() - t0) / reps
-        h2d = sum(x.numel() * x.element_size() for x in h_csr)
-        d2h = sum(x.numel() * x.element_size() for x in (h_order, h_lb, h_la, h_tb, h_ta, h_kept))
-        out["e2e"] = {"value": n / e_dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
-                      "d2h_bytes_per_step": d2h, "ms_per_step": e_dt * 1e3,
-                      "path": "dtb_reorder_stream (host pointers, pinned)"}
         # CPU baseline: the compiled reference on this host's cores
         threads = os.cpu_count() or 1
         sample_batches = max(1, min(my_batches, 2 * threads))
