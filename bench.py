@@ -57,6 +57,7 @@ def parse():
 
 
 def dist_init():
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries exactly one JSON line
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -448,6 +449,10 @@ def main():
             out["search"]["cpu_baseline"] = {"error": str(ex)}
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -941,6 +941,10 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   CU(tok32s.alloc(4ull * total, s));
   CU(wflag.alloc(4ull * n_batches, s));
   CU(wide.alloc(fused_wide_scratch_bytes(n_batches), s));
+  // Separate streaming cost pass.  (FusedArgs::fuse_cost runs it inside the
+  // fused kernel instead; measured slower on B200 — 409 vs 304 us for the
+  // 16M stream: with two 112 KB CTAs per SM too few CSR loads are in flight,
+  // profiles/r01_summary.md.)
   CU(launch_token_keys(io, it, ao, at, total, n, tok16.as<unsigned short>(),
                        wflag.as<unsigned int>(), s));
   FusedArgs fa{};

@@ -281,11 +281,8 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   const bool desc = a.order == DTB_DESCENDING;
 
   if (a.prof && tid == 0) a.prof[b * 8 + 0] = globaltimer();
-  // ---- 1. token keys of the batch from the cost pass: 8 samples per
-  // 128-bit load, all loads issued before use.  cost_size = 2 * tokens.
-  // Batches with a saturated token (or outside the 16-bit layout's limits)
-  // take the 32-bit path straight from the CSR.
-  if (a.wide_flag[b] || m > kNarrowMaxM || n > kFusedMaxN || (n & 7)) {
+  // Batches outside the 16-bit layout's limits take the 32-bit path.
+  if (m > kNarrowMaxM || n > kFusedMaxN || (n & 7) || (!a.fuse_cost && a.wide_flag[b])) {
     // consumers (TokSrc) then read this batch's 32-bit token copies
     if (tid == 0) a.wide_flag[b] = 1u;
     fused_wide(a, b, S);
@@ -299,7 +296,99 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   __syncthreads();
   unsigned int kand = ~0u, kor = 0u;
   int zeros = 0;
-  {
+  // ---- 1. modality tokens of the batch.  cost_size = 2 * tokens.
+  // Per sample: kbi (sort key), identity block loads, zero count, the bit
+  // window of the keys.
+  auto take_sample = [&](int i, unsigned tok) {
+    const unsigned key = desc ? 0x7fffu - tok : tok;
+    kand &= key;
+    kor |= key;
+    zeros += tok == 0;
+    S.kbi[i] = static_cast<unsigned short>(key);
+    S.idx16[i] = static_cast<unsigned short>(i);
+  };
+  if (a.fuse_cost) {
+    // Fused cost pass (Sample::cost_size, core.hpp:160-167) straight from
+    // the CSR: 4 consecutive samples per item, two items per thread in
+    // flight — all offset loads, then the first 3 image / 1 audio
+    // subsequence of each sample, before any is consumed.
+    constexpr int KI = 3, KA = 1, U = 1;
+    const int n_items = n >> 2;
+    const int* io = a.img_off + first;
+    const int* ao = a.aud_off != nullptr ? a.aud_off + first : nullptr;
+    bool wide = false;
+    for (int it0 = tid; it0 < n_items; it0 += kFusedT * U) {
+      int ib[U][5], ab[U][5];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int item = it0 + u * kFusedT;
+        const bool ok = item < n_items;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          ib[u][j] = ok ? __ldg(io + item * 4 + j) : 0;
+          ab[u][j] = ok && ao != nullptr ? __ldg(ao + item * 4 + j) : 0;
+        }
+      }
+      int tv[U][4][KI + KA];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+          for (int q = 0; q < KI; ++q)
+            tv[u][j][q] = ib[u][j] + q < ib[u][j + 1] ? __ldg(a.img_tok + ib[u][j] + q) : 0;
+#pragma unroll
+          for (int q = 0; q < KA; ++q)
+            tv[u][j][KI + q] = ab[u][j] + q < ab[u][j + 1] ? __ldg(a.aud_tok + ab[u][j] + q) : 0;
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int item = it0 + u * kFusedT;
+        if (item >= n_items) break;
+        unsigned short out[4];
+        const int i0 = item * 4;
+        const unsigned blk0 = min(a.div_pg.div(static_cast<unsigned>(i0)), static_cast<unsigned>(m - 1));
+        const unsigned blk3 = min(a.div_pg.div(static_cast<unsigned>(i0 + 3)), static_cast<unsigned>(m - 1));
+        unsigned run = 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          long long t = 0;
+#pragma unroll
+          for (int q = 0; q < KI + KA; ++q) t += tv[u][j][q];
+          for (int x = ib[u][j] + KI; x < ib[u][j + 1]; ++x) t += __ldg(a.img_tok + x);
+          for (int x = ab[u][j] + KA; x < ab[u][j + 1]; ++x) t += __ldg(a.aud_tok + x);
+          if (t < 0 || t > 0x7fff) wide = true;
+          const unsigned tok = t < 0 || t > 0x7fff ? 0x7fffu : static_cast<unsigned>(t);
+          out[j] = static_cast<unsigned short>(tok);
+          take_sample(i0 + j, tok);
+          if (blk0 == blk3) {
+            run += 2u * tok;
+          } else {
+            const unsigned qd = a.div_pg.div(static_cast<unsigned>(i0 + j));
+            atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2u * tok);
+          }
+        }
+        if (blk0 == blk3) atomicAdd(&S.blk_ident[blk0], run);
+        if (a.tok16_w != nullptr) {
+          uint2 pk;
+          pk.x = static_cast<unsigned>(out[0]) | (static_cast<unsigned>(out[1]) << 16);
+          pk.y = static_cast<unsigned>(out[2]) | (static_cast<unsigned>(out[3]) << 16);
+          *reinterpret_cast<uint2*>(a.tok16_w + first + i0) = pk;
+        }
+      }
+    }
+    // a saturated or negative token sum: the whole batch takes the 32-bit
+    // path (which re-reads the CSR)
+    const unsigned any_wide = block_or<kFusedT>(wide ? 1u : 0u, reinterpret_cast<unsigned*>(S.tmp));
+    if (tid == 0) a.wide_flag[b] = any_wide;
+    if (any_wide) {
+      __syncthreads();
+      fused_wide(a, b, S);
+      return;
+    }
+  } else {
+    // tokens from the separate cost pass (launch_token_keys): 8 samples per
+    // 128-bit load, all loads issued before use
     constexpr int V = (kFusedMaxN / 8 + kFusedT - 1) / kFusedT;  // 128-bit loads per thread
     const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
     const int nv = n >> 3;
@@ -322,12 +411,7 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
       for (int j = 0; j < 8; ++j) {
         const int i = i0 + j;
         const unsigned tok = (words[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-        const unsigned key = desc ? 0x7fffu - tok : tok;
-        kand &= key;
-        kor |= key;
-        zeros += tok == 0;
-        S.kbi[i] = static_cast<unsigned short>(key);
-        S.idx16[i] = static_cast<unsigned short>(i);
+        take_sample(i, tok);
         if (blk0 == blk7) {
           run += 2u * tok;
         } else {

@@ -39,6 +39,11 @@ struct FusedArgs {
   // (that batch then takes the 32-bit path from the CSR).
   const unsigned short* tok16;
   unsigned int* wide_flag;  // set by the kernel for every batch it runs on the 32-bit path
+  // fuse_cost: the kernel runs the cost pass itself from the CSR (tok16 and
+  // the cost-pass flags are not read); it writes wide_flag[b] (0/1) and, when
+  // tok16_w != null, the input-order u16 tokens for later consumers.
+  int fuse_cost;
+  unsigned short* tok16_w;
   FastDiv div_pg;
   DevErr* err;
 };
