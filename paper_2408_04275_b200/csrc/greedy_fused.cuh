@@ -54,9 +54,13 @@ __device__ __forceinline__ unsigned block_incl_scan_u32(unsigned v, int* s, unsi
 }
 
 // sizes(k): size of sorted item k; emit(k, g, slot).  Zero run = [z0, z1).
+// prof (debug, may be null): [0] globaltimer after the zero run, [1] round
+// counts (full-round segments << 32 | general rounds).
 template <int T, bool ASC, typename SizeFn, typename EmitFn>
 __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn& sizes,
-                             const EmitFn& emit, FusedGreedySmem& G, int* tmp) {
+                             const EmitFn& emit, FusedGreedySmem& G, int* tmp,
+                             unsigned long long* prof = nullptr) {
+  unsigned long long n_full = 0, n_general = 0;
   static_assert(T >= 2 * kFG && T % kFG == 0, "one entry per thread, two in a merge");
   const int tid = threadIdx.x;
   if (tid < m) {
@@ -110,6 +114,11 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
       r -= nfull;
       k = z1;
       __syncthreads();
+      if (prof && tid == 0) {
+        unsigned long long tnow;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+        prof[0] = tnow;
+      }
       continue;
     }
     const int lim = k < z0 ? min(n, z0) : n;  // non-zero items [k, lim)
@@ -163,6 +172,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
           if (j < r && part) atomicAdd(&G.AL[j], part);
           if (tid < r) G.AC[tid] += tstar;
           k += tstar * r;
+          ++n_full;
           __syncthreads();
           continue;
         }
@@ -263,8 +273,10 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
     }
     r = nkeep + (r - R);
     k += R;
+    ++n_general;
     __syncthreads();
   }
+  if (prof && tid == 0) prof[1] = (n_full << 32) | n_general;
   if (tid < r) {
     G.gload[G.AG[tid]] = G.AL[tid];
     G.gcnt[G.AG[tid]] = G.AC[tid];

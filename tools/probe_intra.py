@@ -58,6 +58,15 @@ def main():
     for k, nm in enumerate(names):
         dt = (p[:, k + 1] - p[:, k]) / 1e3
         print(f"  {nm:18s} median {np.median(dt):8.1f} us  max {dt.max():8.1f}")
+    pi = prof.view(args.batches, 8).cpu().numpy()
+    z = (p[:, 6] - p[:, 2]) / 1e3
+    ok = pi[:, 6] > 0
+    if ok.any():
+        print(f"  greedy: zero run median {np.median(z[ok]):.1f} us; rest "
+              f"{np.median(((p[:, 3] - p[:, 6]) / 1e3)[ok]):.1f} us")
+    cnt = pi[:, 7]
+    print(f"  greedy rounds: full segments median {np.median(cnt >> 32):.0f}, "
+          f"general median {np.median(cnt & 0xffffffff):.0f} max {(cnt & 0xffffffff).max()}")
     start = p[:, 0] - p[:, 0].min()
     print(f"  CTA start spread: {start.max() / 1e3:.1f} us (waves)")
     if args.check:
