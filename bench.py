@@ -145,14 +145,14 @@ class Clocks:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_reference(samples, plan_c, mode, n_batches, steps, warmup, threads, cm):
+def cpu_reference(samples, plan_c, mode, n_batches, steps, warmup, threads, cm, bs=BS):
     """The reference's own disaggregated_reorder (oracle/_ref) over n_batches
     global batches, fanned out over `threads` host threads.  Samples are
     converted to std::vector<Sample> outside the timed region."""
     import oracle
     pl, kind = oracle.best()
     lib = pl.lib
-    sub = samples.slice(0, n_batches * BS)
+    sub = samples.slice(0, n_batches * bs)
     s = sub.to_c()
     h = C.c_void_p()
     pl._check(lib.stream_prepare(C.byref(s), n_batches, C.byref(h)))
@@ -411,6 +411,40 @@ def main():
         out["modes"] = {"intra+inter": {"ms_per_step": both_ms,
                                         "value": my_batches * BS / (both_ms / 1e3),
                                         "unit": "samples/s"}}
+        # BASELINE config 2: LLaVA-style ViT-L + 7B backbone, PP 1/2/1 (4
+        # devices), 32 microbatches per iteration, 10K independent iterations
+        # — one global batch of 32 samples per iteration (DP 1), default
+        # mode (intra + inter), on the same stream entry point
+        import helpers as H
+        c2_iters, c2_l = 10000, 32
+        c2_model, c2_cluster, c2_book = H.llava_model(), H.a800_cluster(64), H.llava_book()
+        c2_cm = pl.cost_model(c2_model, c2_cluster, c2_book)
+        c2_plan = H.plan((1, 1, 1), (1, 1, 2), (1, 1, 1), c2_l).to_c()
+        c2_s = synth_stream(c2_iters * c2_l, seed=2024, family="skewed")
+        c2_d = [dev(c2_s.image_offsets), dev(c2_s.image_tokens), dev(c2_s.audio_offsets),
+                dev(c2_s.audio_tokens)]
+        c2_ds = A.Samples(c2_s.n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32))
+                                           for x in c2_d])
+        c2_out = [torch.empty(c2_s.n, dtype=torch.int32, device="cuda")] + \
+                 [torch.empty(c2_iters, dtype=torch.float64, device="cuda") for _ in range(4)] + \
+                 [torch.empty(c2_iters, dtype=torch.uint8, device="cuda")]
+
+        def c2_step():
+            pl._check(lib.reorder_stream_dev(pl.ctx, c2_cm.h, C.byref(c2_plan),
+                                             C.byref(mode_both), C.byref(c2_ds), c2_iters,
+                                             *[ptr(x) for x in c2_out], sh))
+        c2_ms = timed(c2_step, max(2, args.steps // 3), 1)
+        c2_threads = os.cpu_count() or 1
+        c2_sample = min(c2_iters, 2000)
+        kind2, times2 = cpu_reference(c2_s, c2_plan, mode_both, c2_sample, 2, 0, c2_threads,
+                                      (c2_model, c2_cluster, c2_book), bs=c2_l)
+        out["config2"] = {
+            "metric": "inter-reordered iterations/s (disaggregated_reorder default mode, LLaVA "
+                      "ViT-L + 7B, PP 1/2/1, 32 microbatches/iteration, 10K iterations)",
+            "value": c2_iters / (c2_ms / 1e3), "unit": "iterations/s", "ms_per_step": c2_ms,
+            "cpu_baseline": {"value": c2_sample / float(np.median(times2)),
+                             "unit": "iterations/s", "cores": c2_threads, "kind": kind2,
+                             "sample": f"first {c2_sample} iterations"}}
         # orchestration search, BASELINE config 3
         smodel, scluster, sbook, sbs, sstats = search_workload()
         scm = pl.cost_model(smodel, scluster, sbook)

@@ -252,6 +252,7 @@ STREAM_CASES = [  # (n_batches, bs, dp_lm, dp_me, pp triple, inter)
     (4, 2048, 16, 4, (1, 2, 1), True),     # span 4: assembled microbatch sums
     (3, 1024, 8, 8, (2, 1, 1), True),
     (2, 16384, 128, 128, (1, 2, 1), False),  # BASELINE config 4 batch shape
+    (40, 32, 1, 1, (1, 2, 1), True),      # BASELINE config 2 shape: one group of 32 per batch
 ]
 
 
