@@ -445,6 +445,20 @@ def main():
             "cpu_baseline": {"value": c2_sample / float(np.median(times2)),
                              "unit": "iterations/s", "cores": c2_threads, "kind": kind2,
                              "sample": f"first {c2_sample} iterations"}}
+        # exhaustive ordering scorer: every ordering of
+        # l = 10 microbatches, p = 4, scored by the 1F1B makespan
+        rng_x = np.random.default_rng(10)
+        fx, bx = H.skewed_times(rng_x.lognormal(0, 0.5, 10), 4, 0.4)
+        pl.exhaustive_order(fx, bx, 1)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            bt_x, _o, _a = pl.exhaustive_order(fx, bx, 1)
+        ex_dt = (time.perf_counter() - t0) / 3
+        out["exhaustive_orders"] = {"metric": "orderings scored/s (exhaustive 1F1B makespan, "
+                                              "l = 10, p = 4; tests/test_reorder.cpp:215-239)",
+                                    "value": 3628800 / ex_dt, "unit": "orderings/s",
+                                    "ms_per_call": ex_dt * 1e3,
+                                    "timing": "host wall clock around the C-ABI call"}
         # orchestration search, BASELINE config 3
         smodel, scluster, sbook, sbs, sstats = search_workload()
         scm = pl.cost_model(smodel, scluster, sbook)

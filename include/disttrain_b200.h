@@ -355,6 +355,18 @@ dtb_status dtb_schedule_batch_dev(dtb_context* ctx, int64_t batch,
                                   double* iteration_time, double* device_busy,
                                   void* stream);
 
+/* Exhaustive ordering scorer — the reference's small-instance optimality
+ * oracle for inter_reorder (tests/test_reorder.cpp:215-239 `sim_time` over
+ * every std::next_permutation from the identity): the makespan
+ * of StageTimes::permuted(order) (src/pipeline_sim.cpp:201-212) scheduled by
+ * schedule_1f1b / schedule_interleaved for all l! orders, l <= 12.  Writes
+ * the minimum makespan, the FIRST order (in next_permutation order) attaining
+ * it, and, when all_times != NULL, every makespan in that order (l! doubles).
+ * Same validation and errors as dtb_schedule. */
+dtb_status dtb_exhaustive_order(dtb_context* ctx, const double* fwd, const double* bwd,
+                                int32_t l, int32_t p, int32_t vpp, double* best_time,
+                                int32_t* best_order, double* all_times);
+
 /* simulate_iteration (src/simulate.cpp:23-48) over n_groups coupled groups;
  * group g owns microbatches [group_offsets[g], group_offsets[g+1]).
  * group_times[n_groups] may be NULL. */

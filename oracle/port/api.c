@@ -241,6 +241,69 @@ dtb_status API(schedule_batch)(dtb_context* ctx, int64_t batch,
   return DTB_OK;
 }
 
+/* std::next_permutation over ints (lexicographic successor; 0 at the end). */
+static int next_perm(int32_t* a, int n) {
+  int i = n - 2;
+  while (i >= 0 && a[i] >= a[i + 1]) --i;
+  if (i < 0) {
+    for (int x = 0, y = n - 1; x < y; ++x, --y) {
+      const int32_t t = a[x];
+      a[x] = a[y];
+      a[y] = t;
+    }
+    return 0;
+  }
+  int j = n - 1;
+  while (a[j] <= a[i]) --j;
+  int32_t t = a[i];
+  a[i] = a[j];
+  a[j] = t;
+  for (int x = i + 1, y = n - 1; x < y; ++x, --y) {
+    t = a[x];
+    a[x] = a[y];
+    a[y] = t;
+  }
+  return 1;
+}
+
+/* tests/test_reorder.cpp:215-239: sim_time of every ordering. */
+dtb_status API(exhaustive_order)(dtb_context* ctx, const double* fwd, const double* bwd,
+                                 int32_t l, int32_t p, int32_t vpp, double* best_time,
+                                 int32_t* best_order, double* all_times) {
+  if (l < 1 || l > 12) return port_fail(DTB_ERR_INTERNAL, "exhaustive_order needs 1 <= l <= 12");
+  const size_t cells = (size_t)l * p;
+  int32_t perm[12];
+  double* pf = malloc(sizeof(double) * cells);
+  double* pb = malloc(sizeof(double) * cells);
+  for (int i = 0; i < l; ++i) perm[i] = i;
+  double best = 1e300;
+  int64_t k = 0;
+  dtb_status st = DTB_OK;
+  do {
+    for (int i = 0; i < l; ++i)
+      for (int s = 0; s < p; ++s) {
+        pf[(size_t)i * p + s] = fwd[(size_t)perm[i] * p + s];
+        pb[(size_t)i * p + s] = bwd[(size_t)perm[i] * p + s];
+      }
+    port_timeline tl;
+    st = port_schedule(pf, pb, l, p, vpp, &tl);
+    if (st != DTB_OK) break;
+    const double it = tl.iteration_time;
+    port_timeline_free(&tl);
+    if (all_times) all_times[k] = it;
+    if (it < best) {
+      best = it;
+      memcpy(best_order, perm, sizeof(int32_t) * l);
+    }
+    ++k;
+  } while (next_perm(perm, l));
+  free(pf);
+  free(pb);
+  if (st != DTB_OK) return st;
+  *best_time = best;
+  return DTB_OK;
+}
+
 dtb_status API(simulate_iteration)(dtb_context* ctx, const port_cm* cm,
                                    const dtb_plan* plan, int32_t n_groups,
                                    const int64_t* goff,

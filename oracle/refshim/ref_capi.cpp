@@ -9,6 +9,7 @@
 // Every function is a thin marshalling layer: CSR / POD -> mmplan types ->
 // the reference call -> POD.  No algorithmic code lives here.
 #include <algorithm>
+#include <numeric>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -488,6 +489,34 @@ dtb_status API(schedule_batch)(dtb_context*, int64_t batch, const double* fwd,
                   device_busy + b * tl.device_busy.size());
       }
     });
+  });
+}
+
+dtb_status API(exhaustive_order)(dtb_context*, const double* fwd, const double* bwd,
+                                 int32_t l, int32_t p, int32_t vpp, double* best_time,
+                                 int32_t* best_order, double* all_times) {
+  return guarded([&] {
+    if (l < 1 || l > 12) throw InternalError("exhaustive_order needs 1 <= l <= 12");
+    const StageTimes t = to_times(fwd, bwd, l, p);
+    // tests/test_reorder.cpp:55-59 (sim_time) + :226-232 (the permutation loop)
+    std::vector<int> perm(l);
+    std::iota(perm.begin(), perm.end(), 0);
+    double best = 1e300;
+    std::vector<int> arg = perm;
+    int64_t k = 0;
+    do {
+      const StageTimes permuted = t.permuted(perm);
+      const double it = vpp > 1 ? schedule_interleaved(permuted, vpp).iteration_time
+                                : schedule_1f1b(permuted).iteration_time;
+      if (all_times) all_times[k] = it;
+      if (it < best) {
+        best = it;
+        arg = perm;
+      }
+      ++k;
+    } while (std::next_permutation(perm.begin(), perm.end()));
+    *best_time = best;
+    std::copy(arg.begin(), arg.end(), best_order);
   });
 }
 

@@ -148,6 +148,8 @@ _SIGS = {
                               P(c_f64), P(c_f64), P(c_i64), P(c_i32)]),
     "interval_windows": (c_i32, [VP, P(c_f64), P(c_f64), c_i32, c_i32,
                                  P(c_f64)]),
+    "exhaustive_order": (c_i32, [VP, P(c_f64), P(c_f64), c_i32, c_i32, c_i32, P(c_f64),
+                                 P(c_i32), P(c_f64)]),
     "schedule_batch": (c_i32, [VP, c_i64, P(c_f64), P(c_f64), c_i32, c_i32,
                                c_i32, P(c_f64), P(c_f64)]),
     "schedule_batch_dev": (c_i32, [VP, c_i64, VP, VP, c_i32, c_i32, c_i32,

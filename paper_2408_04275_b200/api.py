@@ -10,6 +10,7 @@ class to the reference/port libraries for parity checks.
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -539,6 +540,21 @@ class Planner:
         self._check(self.lib.interval_windows(self.ctx, ptr(fwd, C.c_double), ptr(bwd, C.c_double),
                                               l, p, ptr(out, C.c_double)))
         return out
+
+    def exhaustive_order(self, fwd, bwd, vpp=1, with_all=False):
+        """Makespan of every ordering of the rows (tests/test_reorder.cpp:215-239):
+        returns (best makespan, first order attaining it, all makespans in
+        std::next_permutation order or None)."""
+        fwd = np.ascontiguousarray(fwd, dtype=np.float64)
+        bwd = np.ascontiguousarray(bwd, dtype=np.float64)
+        l, p = fwd.shape
+        best = C.c_double()
+        order = np.zeros(l, dtype=np.int32)
+        allt = np.zeros(math.factorial(l)) if with_all else None
+        self._check(self.lib.exhaustive_order(self.ctx, ptr(fwd, C.c_double), ptr(bwd, C.c_double),
+                                              l, p, vpp, C.byref(best), ptr(order, C.c_int32),
+                                              ptr(allt, C.c_double)))
+        return best.value, order.tolist(), allt
 
     def schedule_batch(self, fwd, bwd, vpp=1, with_busy=False):
         fwd, bwd = _f64(fwd), _f64(bwd)

@@ -727,6 +727,42 @@ dtb_status dtb_schedule_batch_dev(dtb_context* ctx, int64_t batch, const double*
   return DTB_OK;
 }
 
+dtb_status dtb_exhaustive_order(dtb_context* ctx, const double* fwd, const double* bwd,
+                                int32_t l, int32_t p, int32_t vpp, double* best_time,
+                                int32_t* best_order, double* all_times) {
+  TRY(set_device(ctx));
+  if (l < 1 || l > exhaustive_max_l())
+    return fail(DTB_ERR_INTERNAL, "exhaustive_order needs 1 <= l <= %d", exhaustive_max_l());
+  if (p < 1 || p > exhaustive_max_p())
+    return fail(DTB_ERR_INVALID_ARGUMENT, "exhaustive_order supports 1 <= p <= %d",
+                exhaustive_max_p());
+  TRY(check_vpp(l, p, vpp));
+  long long total = 1;
+  for (int i = 2; i <= l; ++i) total *= i;
+  if (all_times != nullptr && total > (1ll << 26))
+    return fail(DTB_ERR_INVALID_ARGUMENT, "all_times of %lld orderings not supported", total);
+  const size_t cells = static_cast<size_t>(l) * p;
+  cudaStream_t s = ctx->stream;
+  TRY(reset_err(ctx));
+  DBuf df, db, all, bt, bo, scr;
+  TRY(upload(df, fwd, cells, s));
+  TRY(upload(db, bwd, cells, s));
+  CU(launch_check_times(df.as<double>(), db.as<double>(), static_cast<long long>(cells), ctx->err,
+                        s));
+  if (all_times != nullptr) CU(all.alloc(8ull * total, s));
+  CU(bt.alloc(8, s));
+  CU(bo.alloc(4ull * l, s));
+  const int n_blocks = static_cast<int>(std::min<long long>(148 * 16, (total + 127) / 128));
+  CU(scr.alloc(exhaustive_scratch(n_blocks), s));
+  CU(launch_exhaustive(df.as<double>(), db.as<double>(), l, p, vpp,
+                       all_times ? all.as<double>() : nullptr, bt.as<double>(), bo.as<int>(),
+                       scr.p, n_blocks, ctx->err, s));
+  TRY(download(best_time, bt, 1, s));
+  TRY(download(best_order, bo, l, s));
+  if (all_times != nullptr) TRY(download(all_times, all, total, s));
+  return sync_and_check(ctx);
+}
+
 dtb_status dtb_schedule_batch(dtb_context* ctx, int64_t batch, const double* fwd,
                               const double* bwd, int32_t l, int32_t p, int32_t vpp,
                               double* iteration_time, double* device_busy) {

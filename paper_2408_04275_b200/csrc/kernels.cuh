@@ -189,6 +189,14 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
                               cudaStream_t stream);
 size_t group_sims_scratch(const GroupSimArgs& a);
 
+// ------------------------------------------------- exhaustive orderings
+int exhaustive_max_l();
+int exhaustive_max_p();
+size_t exhaustive_scratch(int n_blocks);
+cudaError_t launch_exhaustive(const double* fwd, const double* bwd, int l, int p, int vpp,
+                              double* all, double* best_t, int* best_order, void* scratch,
+                              int n_blocks, DevErr* err, cudaStream_t stream);
+
 // --------------------------------------------------------- inter reorder
 struct InterArgs {
   long long batch;       // independent problems

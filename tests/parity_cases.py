@@ -120,6 +120,25 @@ def check_schedule(impl, oracle, rng):
         assert_same(ba, bb, "batch busy")
 
 
+def check_exhaustive(impl, oracle, rng):
+    """Every ordering's makespan (the reference's small-instance optimality
+    oracle, tests/test_reorder.cpp:215-239), vpp 1 and 2, ties included."""
+    cases = [(H.skewed_times(rng.lognormal(0, 0.5, 6), 3, 0.4), 1),
+             (H.random_times(rng, 5, 4), 1),
+             ((np.full((4, 2), 0.5), np.full((4, 2), 1.0)), 1),   # all orders tie
+             (H.random_times(rng, 4, 4), 2),
+             (H.random_times(rng, 1, 3), 1)]
+    for (f, b), vpp in cases:
+        ta, oa, aa = impl.exhaustive_order(f, b, vpp, with_all=True)
+        tb, ob, ab = oracle.exhaustive_order(f, b, vpp, with_all=True)
+        assert ta == tb and oa == ob, (f.shape, vpp, ta, tb, oa, ob)
+        assert_same(aa, ab, "all orderings")
+    f, b = H.skewed_times(rng.lognormal(0, 0.5, 8), 3, 0.4)   # 40,320 orderings
+    ta, oa, _ = impl.exhaustive_order(f, b, 1)
+    tb, ob, _ = oracle.exhaustive_order(f, b, 1)
+    assert ta == tb and oa == ob
+
+
 # ------------------------------------------------------------------- inter
 def inter_cases(rng):
     for _ in range(30):
