@@ -477,6 +477,27 @@ dtb_status dtb_model_orchestration(dtb_context* ctx, const dtb_cost_model* cm,
                                    dtb_candidate* candidates,
                                    int64_t capacity);
 
+/* brute_force_oracle (src/orchestrator.cpp:433-491): exhaustive integer
+ * search over every tuple of enumerate_parallelism and every PP triple with
+ * q_me*pp_me + q_lm*pp_lm + q_mg*pp_mg <= total_gpus, memory_check,
+ * predict_times, BestTracker order; candidates_evaluated counts the
+ * memory-feasible plans.  CapExceededError ("exhaustive search capped at
+ * <cap> GPUs, got <n>") when total_gpus > gpu_cap (the reference's
+ * BruteForceOptions default is 32; the GPU search accepts larger caps). */
+dtb_status dtb_brute_force_oracle(dtb_context* ctx, const dtb_cost_model* cm,
+                                  const dtb_workload_stats* stats, int64_t global_batch,
+                                  int32_t vpp, int32_t gpu_cap,
+                                  dtb_orchestration_result* result);
+
+/* rigid_baseline (src/orchestrator.cpp:407-431): Megatron-style rigid
+ * orchestration — encoder/generator share the backbone's TP and DP with one
+ * pipeline stage each, the backbone takes every remaining GPU; the best by
+ * predicted time (BestTracker order).  InfeasibleError "no feasible rigid
+ * configuration". */
+dtb_status dtb_rigid_baseline(dtb_context* ctx, const dtb_cost_model* cm,
+                              const dtb_workload_stats* stats, int64_t global_batch,
+                              int32_t vpp, dtb_plan* plan);
+
 /* One shard of the search for multi-GPU runs: evaluates the tuples whose
  * sorted index i satisfies i % shard_count == shard_index and writes the
  * shard's BestTracker winner (feasible == 0 when none) to *best_dev, a

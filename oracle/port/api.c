@@ -403,6 +403,102 @@ dtb_status API(solve_subproblem)(dtb_context* ctx, const port_cm* cm,
 
 int port_offer(int has, dtb_candidate* best, const dtb_candidate* cand);
 
+static dtb_plan plan_of(const dtb_tuple* t, int pe, int pl, int pg, int64_t bs, int vpp) {
+  dtb_plan p;
+  p.unit[0].tp = t->tp_me;
+  p.unit[0].dp = t->dp_me;
+  p.unit[0].pp = pe;
+  p.unit[1].tp = t->tp_lm;
+  p.unit[1].dp = t->dp_lm;
+  p.unit[1].pp = pl;
+  p.unit[2].tp = t->tp_mg;
+  p.unit[2].dp = t->dp_mg;
+  p.unit[2].pp = pg;
+  p.vpp = vpp;
+  p.global_batch = bs;
+  return p;
+}
+
+/* brute_force_oracle — src/orchestrator.cpp:433-491. */
+dtb_status API(brute_force_oracle)(dtb_context* ctx, const port_cm* cm,
+                                   const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                                   int32_t gpu_cap, dtb_orchestration_result* res) {
+  const int n = cm->cluster.total_gpus;
+  if (n > gpu_cap)
+    return port_fail(DTB_ERR_CAP_EXCEEDED, "exhaustive search capped at %d GPUs, got %d",
+                     gpu_cap, n);
+  dtb_tuple* v;
+  const int64_t nt = port_enumerate(&cm->cluster, bs, &v);
+  int has = 0;
+  int64_t evaluated = 0;
+  dtb_candidate best, c;
+  for (int64_t i = 0; i < nt; ++i) {
+    const dtb_tuple* t = &v[i];
+    const int q_me = t->tp_me * t->dp_me, q_lm = t->tp_lm * t->dp_lm, q_mg = t->tp_mg * t->dp_mg;
+    for (int pe = 1; q_me * pe + q_lm + q_mg <= n; ++pe)
+      for (int pl = 1; q_me * pe + q_lm * pl + q_mg <= n; ++pl)
+        for (int pg = 1; q_me * pe + q_lm * pl + q_mg * pg <= n; ++pg) {
+          const dtb_plan plan = plan_of(t, pe, pl, pg, bs, vpp);
+          if (vpp > 1 && (bs / t->dp_lm) % (pe + pl + pg) != 0) continue;
+          dtb_memory_report mem;
+          port_memory_check(&plan, &cm->model, &cm->cluster, &mem);
+          if (!mem.pass) continue;
+          memset(&c, 0, sizeof c);
+          c.tuple = *t;
+          c.feasible = 1;
+          c.plan = plan;
+          if (port_predict_times(cm, &plan, stats, &c.times) != 0) {
+            free(v);
+            return port_status;
+          }
+          ++evaluated;
+          has = port_offer(has, &best, &c);
+        }
+  }
+  free(v);
+  res->candidates_evaluated = evaluated;
+  res->solve_seconds = 0.0;
+  if (!has) return port_fail(DTB_ERR_INFEASIBLE, "no feasible plan in the exhaustive search");
+  res->best = best.plan;
+  res->times = best.times;
+  return DTB_OK;
+}
+
+/* rigid_baseline — src/orchestrator.cpp:407-431 (validate_plan reduces to
+ * the memory check here: every other rule holds by construction). */
+dtb_status API(rigid_baseline)(dtb_context* ctx, const port_cm* cm,
+                               const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                               dtb_plan* out) {
+  static const int tps[4] = {1, 2, 4, 8};
+  int64_t divs[4096];
+  int64_t nd = 0;
+  for (int64_t d = 1; d <= bs && nd < 4096; ++d)
+    if (bs % d == 0) divs[nd++] = d;
+  int has = 0;
+  dtb_candidate best, c;
+  for (int a = 0; a < 4; ++a)
+    for (int64_t j = 0; j < nd; ++j) {
+      const long q = (long)tps[a] * divs[j];
+      const int pl = (int)((cm->cluster.total_gpus - 2 * q) / q);
+      if (pl < 1) continue;
+      dtb_tuple t = {tps[a], (int32_t)divs[j], tps[a], (int32_t)divs[j], tps[a], (int32_t)divs[j]};
+      const dtb_plan plan = plan_of(&t, 1, pl, 1, bs, vpp);
+      if (vpp > 1 && (bs / divs[j]) % (pl + 2) != 0) continue;
+      dtb_memory_report mem;
+      port_memory_check(&plan, &cm->model, &cm->cluster, &mem);
+      if (!mem.pass) continue;
+      memset(&c, 0, sizeof c);
+      c.tuple = t;
+      c.feasible = 1;
+      c.plan = plan;
+      if (port_predict_times(cm, &plan, stats, &c.times) != 0) return port_status;
+      has = port_offer(has, &best, &c);
+    }
+  if (!has) return port_fail(DTB_ERR_INFEASIBLE, "no feasible rigid configuration");
+  *out = best.plan;
+  return DTB_OK;
+}
+
 /* model_orchestration — src/orchestrator.cpp:380-405. */
 dtb_status API(model_orchestration)(dtb_context* ctx, const port_cm* cm,
                                     const dtb_workload_stats* stats,

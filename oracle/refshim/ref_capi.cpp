@@ -747,6 +747,27 @@ dtb_status API(model_orchestration)(dtb_context*, const dtb_cost_model* cm,
   });
 }
 
+dtb_status API(brute_force_oracle)(dtb_context*, const dtb_cost_model* cm,
+                                   const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                                   int32_t gpu_cap, dtb_orchestration_result* result) {
+  return guarded([&] {
+    BruteForceOptions opts;
+    opts.vpp = vpp;
+    opts.gpu_cap = gpu_cap;
+    const OrchestrationResult r = brute_force_oracle(*cm->cm, to_stats(*stats), bs, opts);
+    result->best = from_plan(r.best);
+    result->times = {r.times.t_warm, r.times.t_steady, r.times.t_iter};
+    result->candidates_evaluated = static_cast<int64_t>(r.candidates_evaluated);
+    result->solve_seconds = r.solve_seconds;
+  });
+}
+
+dtb_status API(rigid_baseline)(dtb_context*, const dtb_cost_model* cm,
+                               const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                               dtb_plan* plan) {
+  return guarded([&] { *plan = from_plan(rigid_baseline(*cm->cm, to_stats(*stats), bs, vpp)); });
+}
+
 // Multi-threaded CPU baseline of model_orchestration: the reference's own
 // enumerate_parallelism + solve_subproblem per tuple, fanned out over
 // set_threads(n) host threads, folded with the reference's tie-break order

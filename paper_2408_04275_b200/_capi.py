@@ -179,6 +179,9 @@ _SIGS = {
                                       P(Tuple), c_i64]),
     "solve_subproblem": (c_i32, [VP, VP, P(WorkloadStats), P(Tuple), c_i64,
                                  c_i64, c_i32, P(Candidate)]),
+    "brute_force_oracle": (c_i32, [VP, VP, P(WorkloadStats), c_i64, c_i32, c_i32,
+                                   P(OrchestrationResult)]),
+    "rigid_baseline": (c_i32, [VP, VP, P(WorkloadStats), c_i64, c_i32, P(Plan)]),
     "model_orchestration": (c_i32, [VP, VP, P(WorkloadStats), c_i64, c_i32,
                                     P(OrchestrationResult), P(Candidate),
                                     c_i64]),

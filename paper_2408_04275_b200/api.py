@@ -673,6 +673,22 @@ class Planner:
                                               global_batch, vpp, out))
         return [Candidate.from_c(c) for c in out[:len(tuples)]]
 
+    def brute_force_oracle(self, cm, stats, global_batch, vpp=1, gpu_cap=32):
+        """brute_force_oracle (src/orchestrator.cpp:433-491)."""
+        res = A.OrchestrationResult()
+        self._check(self.lib.brute_force_oracle(self.ctx, cm.h, C.byref(stats), global_batch, vpp,
+                                                gpu_cap, C.byref(res)))
+        return dict(best=PlanSpec.from_c(res.best),
+                    times=(res.times.t_warm, res.times.t_steady, res.times.t_iter),
+                    candidates_evaluated=res.candidates_evaluated)
+
+    def rigid_baseline(self, cm, stats, global_batch, vpp=1):
+        """rigid_baseline (src/orchestrator.cpp:407-431)."""
+        plan = A.Plan()
+        self._check(self.lib.rigid_baseline(self.ctx, cm.h, C.byref(stats), global_batch, vpp,
+                                            C.byref(plan)))
+        return PlanSpec.from_c(plan)
+
     def model_orchestration(self, cm, stats, global_batch, vpp=1, keep_candidates=False):
         res = A.OrchestrationResult()
         cands, cap = None, 0

@@ -6,6 +6,7 @@
 // run on the context stream and synchronise; `_dev` entry points enqueue on
 // the caller's stream.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -1458,6 +1459,105 @@ dtb_status dtb_model_orchestration(dtb_context* ctx, const dtb_cost_model* cm,
   if (!b.feasible) return fail(DTB_ERR_INFEASIBLE, "no feasible plan for this model and cluster");
   result->best = b.plan;
   result->times = b.times;
+  return DTB_OK;
+}
+
+dtb_status dtb_brute_force_oracle(dtb_context* ctx, const dtb_cost_model* cm,
+                                  const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                                  int32_t gpu_cap, dtb_orchestration_result* result) {
+  TRY(set_device(ctx));
+  const int n_gpus = cm->cluster.total_gpus;
+  if (n_gpus > gpu_cap)
+    return fail(DTB_ERR_CAP_EXCEEDED, "exhaustive search capped at %d GPUs, got %d", gpu_cap,
+                n_gpus);
+  const auto t0 = std::chrono::steady_clock::now();
+  TRY(reset_err(ctx));
+  cudaStream_t s = ctx->stream;
+  DBuf scr, cnt, tuples, ev, bb, best;
+  CU(scr.alloc(enumerate_scratch(bs), s));
+  CU(cnt.alloc(8, s));
+  CU(launch_enumerate(cm->cluster, bs, nullptr, 0, cnt.as<long long>(), nullptr, 0, scr.p, s));
+  long long n = 0;
+  CU(cudaMemcpyAsync(&n, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  CU(tuples.alloc(sizeof(dtb_tuple) * (n > 0 ? n : 1), s));
+  CU(launch_enumerate(cm->cluster, bs, nullptr, 0, cnt.as<long long>(), tuples.as<dtb_tuple>(),
+                      n, scr.p, s));
+  int grid = static_cast<int>(std::min<long long>((n + 127) / 128, 148 * 16));
+  if (grid < 1) grid = 1;
+  CU(ev.alloc(8, s));
+  CU(cudaMemsetAsync(ev.p, 0, 8, s));
+  CU(bb.alloc(sizeof(dtb_candidate) * grid, s));
+  CU(best.alloc(sizeof(dtb_candidate), s));
+  OrchArgs a{};
+  a.cm = cm->dev;
+  a.stats = *stats;
+  a.bs = bs;
+  a.vpp = vpp;
+  a.tuples = tuples.as<dtb_tuple>();
+  a.n = n;
+  a.shard_index = 0;
+  a.shard_count = 1;
+  a.block_best = bb.as<dtb_candidate>();
+  a.err = ctx->err;
+  CU(launch_brute(a, grid, reinterpret_cast<unsigned long long*>(ev.p), s));
+  CU(launch_best_reduce(bb.as<dtb_candidate>(), grid, best.as<dtb_candidate>(), s));
+  DevErr e;
+  CU(cudaMemcpyAsync(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost, s));
+  dtb_candidate b;
+  unsigned long long evaluated = 0;
+  CU(cudaMemcpyAsync(&b, best.p, sizeof b, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&evaluated, ev.p, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  TRY(orch_error(ctx, cm, e, tuples.as<dtb_tuple>()));
+  result->candidates_evaluated = static_cast<int64_t>(evaluated);
+  result->solve_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (!b.feasible) return fail(DTB_ERR_INFEASIBLE, "no feasible plan in the exhaustive search");
+  result->best = b.plan;
+  result->times = b.times;
+  return DTB_OK;
+}
+
+dtb_status dtb_rigid_baseline(dtb_context* ctx, const dtb_cost_model* cm,
+                              const dtb_workload_stats* stats, int64_t bs, int32_t vpp,
+                              dtb_plan* plan) {
+  TRY(set_device(ctx));
+  TRY(reset_err(ctx));
+  cudaStream_t s = ctx->stream;
+  std::vector<long long> divs;
+  for (long long d = 1; d * d <= bs; ++d)
+    if (bs % d == 0) {
+      divs.push_back(d);
+      if (d != bs / d) divs.push_back(bs / d);
+    }
+  std::sort(divs.begin(), divs.end());
+  const int nd = static_cast<int>(divs.size());
+  DBuf dd, c, best;
+  TRY(upload(dd, divs.data(), divs.size(), s));
+  CU(c.alloc(sizeof(dtb_candidate) * (4 * nd > 0 ? 4 * nd : 1), s));
+  CU(best.alloc(sizeof(dtb_candidate), s));
+  CU(launch_rigid(cm->dev, *stats, bs, vpp, dd.as<long long>(), nd, c.as<dtb_candidate>(),
+                  ctx->err, s));
+  CU(launch_best_reduce(c.as<dtb_candidate>(), 4 * nd, best.as<dtb_candidate>(), s));
+  DevErr e;
+  dtb_candidate b;
+  CU(cudaMemcpyAsync(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&b, best.p, sizeof b, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (e.code != 0) {
+    if (e.code != -1) return dev_status(e);
+    const long long x = static_cast<long long>(e.ordered >> 8);
+    const int tp = std::array<int, 4>{1, 2, 4, 8}[x / nd];
+    for (int u = 0; u < 3; ++u) {
+      TRY(check_fwd_query(cm, u, tp));
+      TRY(check_bwd_query(cm, u, tp));
+    }
+    const int tps[3] = {tp, tp, tp};
+    return dev_status(e, tps);
+  }
+  if (!b.feasible) return fail(DTB_ERR_INFEASIBLE, "no feasible rigid configuration");
+  *plan = b.plan;
   return DTB_OK;
 }
 

@@ -440,6 +440,101 @@ cudaError_t launch_orchestration(const OrchArgs& a, int grid, cudaStream_t strea
   return cudaGetLastError();
 }
 
+// brute_force_oracle (orchestrator.cpp:433-491): one thread per tuple walks
+// every PP triple that fits the cluster; memory_check, predict_times and a
+// private BestTracker; then the same block/grid lexicographic reduction.
+// (Work per tuple grows with (n / q)^3; the reference caps n at 32.)
+__global__ void __launch_bounds__(kOrchT)
+brute_kernel(OrchArgs a, unsigned long long* evaluated) {
+  __shared__ dtb_candidate s_best[kOrchT];
+  const long long stride = static_cast<long long>(gridDim.x) * kOrchT;
+  const int n = a.cm.cluster.total_gpus;
+  dtb_candidate mine;
+  mine.feasible = 0;
+  unsigned long long count = 0;
+  for (long long idx = blockIdx.x * static_cast<long long>(kOrchT) + threadIdx.x; idx < a.n;
+       idx += stride) {
+    const dtb_tuple t = a.tuples[idx];
+    const int q_me = t.tp_me * t.dp_me, q_lm = t.tp_lm * t.dp_lm, q_mg = t.tp_mg * t.dp_mg;
+    const long long mbs = a.bs / t.dp_lm;
+    bool failed = false;
+    for (int pe = 1; !failed && q_me * pe + q_lm + q_mg <= n; ++pe)
+      for (int pl = 1; !failed && q_me * pe + q_lm * pl + q_mg <= n; ++pl)
+        for (int pg = 1; q_me * pe + q_lm * pl + q_mg * pg <= n; ++pg) {
+          if (a.vpp > 1 && mbs % (pe + pl + pg) != 0) continue;
+          dtb_candidate c;
+          c.tuple = t;
+          c.feasible = 1;
+          c.reason = DTB_REASON_NONE;
+          c.plan = plan_from(t, pe, pl, pg, a.bs, a.vpp);
+          if (!dev_memory_pass(a.cm, c.plan, nullptr)) continue;
+          const int e = dev_predict(a.cm, c.plan, a.stats, &c.times);
+          if (e) {
+            dev_fail_ordered(a.err, static_cast<unsigned long long>(idx * 3), e);
+            failed = true;
+            break;
+          }
+          ++count;
+          if (cand_better(c, mine)) mine = c;
+        }
+  }
+  atomicAdd(evaluated, count);
+  s_best[threadIdx.x] = mine;
+  __syncthreads();
+  for (int w = kOrchT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w && cand_better(s_best[threadIdx.x + w], s_best[threadIdx.x]))
+      s_best[threadIdx.x] = s_best[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.block_best[blockIdx.x] = s_best[0];
+}
+
+cudaError_t launch_brute(const OrchArgs& a, int grid, unsigned long long* evaluated,
+                         cudaStream_t stream) {
+  brute_kernel<<<grid, kOrchT, 0, stream>>>(a, evaluated);
+  return cudaGetLastError();
+}
+
+// rigid_baseline (orchestrator.cpp:407-431): one thread per (tp, dp divisor);
+// validate_plan reduces to memory_check for these plans (every other rule
+// holds by construction).  Writes one candidate per pair (feasible = 0 when
+// skipped) for the BestTracker reduction.
+__global__ void rigid_kernel(DevCM cm, dtb_workload_stats stats, long long bs, int vpp,
+                             const long long* divs, int n_divs, dtb_candidate* out,
+                             DevErr* err) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= 4 * n_divs) return;
+  const int tp = kTpc[x / n_divs];
+  const long long dp = divs[x % n_divs];
+  dtb_candidate c;
+  c.feasible = 0;
+  c.reason = DTB_REASON_NONE;
+  const long q = static_cast<long>(tp) * dp;
+  const int pl = static_cast<int>((cm.cluster.total_gpus - 2 * q) / q);
+  if (pl >= 1) {
+    const dtb_tuple t = {tp, static_cast<int>(dp), tp, static_cast<int>(dp), tp,
+                         static_cast<int>(dp)};
+    c.tuple = t;
+    c.plan = plan_from(t, 1, pl, 1, bs, vpp);
+    const bool vpp_ok = vpp == 1 || (bs / dp) % (pl + 2) == 0;
+    if (vpp_ok && dev_memory_pass(cm, c.plan, nullptr)) {
+      const int e = dev_predict(cm, c.plan, stats, &c.times);
+      if (e) dev_fail_ordered(err, static_cast<unsigned long long>(x), e);
+      else c.feasible = 1;
+    }
+  }
+  out[x] = c;
+}
+
+cudaError_t launch_rigid(const DevCM& cm, const dtb_workload_stats& stats, long long bs, int vpp,
+                         const long long* divs, int n_divs, dtb_candidate* out, DevErr* err,
+                         cudaStream_t stream) {
+  if (n_divs < 1) return cudaSuccess;
+  rigid_kernel<<<(4 * n_divs + 127) / 128, 128, 0, stream>>>(cm, stats, bs, vpp, divs, n_divs,
+                                                             out, err);
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(kOrchT)
 best_reduce_kernel(const dtb_candidate* in, long long n, dtb_candidate* out) {
   __shared__ dtb_candidate s_best[kOrchT];

@@ -246,6 +246,11 @@ cudaError_t launch_enumerate(const dtb_cluster_spec& c, long long bs,
                              cudaStream_t stream);
 cudaError_t launch_orchestration(const OrchArgs& a, int grid,
                                  cudaStream_t stream);
+cudaError_t launch_brute(const OrchArgs& a, int grid, unsigned long long* evaluated,
+                         cudaStream_t stream);
+cudaError_t launch_rigid(const DevCM& cm, const dtb_workload_stats& stats, long long bs, int vpp,
+                         const long long* divs, int n_divs, dtb_candidate* out, DevErr* err,
+                         cudaStream_t stream);
 cudaError_t launch_best_reduce(const dtb_candidate* in, long long n,
                                dtb_candidate* out, cudaStream_t stream);
 cudaError_t launch_predict(const DevCM& cm, const dtb_workload_stats& stats,

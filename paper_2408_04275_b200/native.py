@@ -33,7 +33,8 @@ REQUIRED = [
     "cost_model_destroy", "cost_sizes", "unit_times", "memory_check", "build_stage_times",
     "microbatch_fwd_keys", "compute_stats", "intra_partition", "block_group_loads",
     "select_min", "select_closest", "schedule", "get_intervals", "interval_windows",
-    "schedule_batch", "schedule_batch_dev", "exhaustive_order", "simulate_iteration", "inter_reorder",
+    "schedule_batch", "schedule_batch_dev", "exhaustive_order", "brute_force_oracle",
+    "rigid_baseline", "simulate_iteration", "inter_reorder",
     "inter_reorder_batch", "inter_reorder_batch_dev", "disaggregated_reorder", "reorder_stream",
     "reorder_stream_dev", "intra_stream_dev", "predict_times", "enumerate_parallelism", "solve_subproblem",
     "model_orchestration", "orchestration_shard_dev", "best_reduce_dev",

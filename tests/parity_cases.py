@@ -311,6 +311,45 @@ def orch_cases():
     yield H.mllm72b_model(), H.a800_cluster(112), H.mllm72b_book(), 240, 1
 
 
+def outcome(fn, *args):
+    """Result, or (error class, message) — both sides must agree on either."""
+    try:
+        return fn(*args)
+    except Exception as e:  # noqa: BLE001 — the error itself is the outcome
+        return (type(e).__name__, str(e))
+
+
+def check_brute(impl, oracle, rng):
+    """brute_force_oracle and rigid_baseline (src/orchestrator.cpp:407-491):
+    plan, times and the evaluated count; the cap and infeasible errors."""
+    from paper_2408_04275_b200.api import CapExceededError
+    cases = [(H.toy_model(), H.quiet_cluster(12), H.flat_book(1.0, 1.0, 1.0), 8, 1),
+             (H.toy_model(), H.quiet_cluster(16), H.tp_scaled_book(0.3, 1.7, 0.9), 4, 1),
+             (H.toy_model(), H.quiet_cluster(24), H.tp_scaled_book(0.4, 2.0, 0.6), 8, 2),
+             (H.desk_model(), H.desk_cluster(32), H.desk_book(), 64, 1)]
+    for model, cluster, book, bs, vpp in cases:
+        ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
+        stats = stats_to_c(model.seq_len, 1000.0, 1000.0)
+        a = outcome(impl.brute_force_oracle, ci, stats, bs, vpp)
+        b = outcome(oracle.brute_force_oracle, co, stats, bs, vpp)
+        assert a == b, (a, b)
+        a = outcome(impl.rigid_baseline, ci, stats, bs, vpp)
+        b = outcome(oracle.rigid_baseline, co, stats, bs, vpp)
+        assert a == b, (a, b)
+    # the cap: same error class and text
+    model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
+    ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
+    stats = stats_to_c(model.seq_len, 1000.0, 1000.0)
+    msgs = []
+    for pl, c in ((impl, ci), (oracle, co)):
+        try:
+            pl.brute_force_oracle(c, stats, 64)
+            raise AssertionError("cap not enforced")
+        except CapExceededError as e:
+            msgs.append(str(e))
+    assert msgs[0] == msgs[1], msgs
+
+
 def check_orchestration(impl, oracle, rng):
     for model, cluster, book, bs, vpp in orch_cases():
         ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)

@@ -9,7 +9,7 @@ import parity_cases as P
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["intra", "select", "schedule", "exhaustive", "inter", "cost",
+@pytest.mark.parametrize("name", ["intra", "select", "schedule", "exhaustive", "brute", "inter", "cost",
                                   "simulate", "disaggregated", "stream", "orchestration"])
 def test_gpu_matches_oracle(name, gpu, oracle_best):
     rng = np.random.default_rng(4321 + len(name))
