@@ -1483,11 +1483,15 @@ dtb_status dtb_brute_force_oracle(dtb_context* ctx, const dtb_cost_model* cm,
   CU(tuples.alloc(sizeof(dtb_tuple) * (n > 0 ? n : 1), s));
   CU(launch_enumerate(cm->cluster, bs, nullptr, 0, cnt.as<long long>(), tuples.as<dtb_tuple>(),
                       n, scr.p, s));
-  int grid = static_cast<int>(std::min<long long>((n + 127) / 128, 148 * 16));
-  if (grid < 1) grid = 1;
+  const int grid = 148 * 16;
   CU(ev.alloc(8, s));
   CU(cudaMemsetAsync(ev.p, 0, 8, s));
   CU(bb.alloc(sizeof(dtb_candidate) * grid, s));
+  const size_t bscr = brute_scratch(n);
+  DBuf bs_scr;
+  CU(bs_scr.alloc(bscr, s));
+  // records of blocks that get no pairs must read as infeasible
+  CU(cudaMemsetAsync(bb.p, 0, sizeof(dtb_candidate) * grid, s));
   CU(best.alloc(sizeof(dtb_candidate), s));
   OrchArgs a{};
   a.cm = cm->dev;
@@ -1500,7 +1504,7 @@ dtb_status dtb_brute_force_oracle(dtb_context* ctx, const dtb_cost_model* cm,
   a.shard_count = 1;
   a.block_best = bb.as<dtb_candidate>();
   a.err = ctx->err;
-  CU(launch_brute(a, grid, reinterpret_cast<unsigned long long*>(ev.p), s));
+  CU(launch_brute(a, grid, reinterpret_cast<unsigned long long*>(ev.p), bs_scr.p, bscr, s));
   CU(launch_best_reduce(bb.as<dtb_candidate>(), grid, best.as<dtb_candidate>(), s));
   DevErr e;
   CU(cudaMemcpyAsync(&e, ctx->err, sizeof e, cudaMemcpyDeviceToHost, s));

@@ -440,43 +440,71 @@ cudaError_t launch_orchestration(const OrchArgs& a, int grid, cudaStream_t strea
   return cudaGetLastError();
 }
 
-// brute_force_oracle (orchestrator.cpp:433-491): one thread per tuple walks
-// every PP triple that fits the cluster; memory_check, predict_times and a
-// private BestTracker; then the same block/grid lexicographic reduction.
-// (Work per tuple grows with (n / q)^3; the reference caps n at 32.)
+// brute_force_oracle (orchestrator.cpp:433-491).  The work per tuple grows
+// like (n / q)^3, so tuples are split into (tuple, pp_me, pp_lm) PAIRS — a
+// count pass and a scan give each tuple its pair range — and one thread per
+// pair walks pp_mg; memory_check, predict_times and a private BestTracker,
+// then the same block/grid lexicographic reduction (a total order: the
+// split does not change the winner).
+__device__ __forceinline__ long long brute_pairs_of(const dtb_tuple& t, int n) {
+  const int q_me = t.tp_me * t.dp_me, q_lm = t.tp_lm * t.dp_lm, q_mg = t.tp_mg * t.dp_mg;
+  long long c = 0;
+  for (int pe = 1; q_me * pe + q_lm + q_mg <= n; ++pe) c += (n - q_me * pe - q_mg) / q_lm;
+  return c;
+}
+
+__global__ void brute_count_kernel(const dtb_tuple* tuples, long long n_tuples, int n,
+                                   long long* counts) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < n_tuples) counts[i] = brute_pairs_of(tuples[i], n);
+}
+
 __global__ void __launch_bounds__(kOrchT)
-brute_kernel(OrchArgs a, unsigned long long* evaluated) {
+brute_kernel(OrchArgs a, const long long* offsets, long long total,
+             unsigned long long* evaluated) {
   __shared__ dtb_candidate s_best[kOrchT];
   const long long stride = static_cast<long long>(gridDim.x) * kOrchT;
   const int n = a.cm.cluster.total_gpus;
   dtb_candidate mine;
   mine.feasible = 0;
   unsigned long long count = 0;
-  for (long long idx = blockIdx.x * static_cast<long long>(kOrchT) + threadIdx.x; idx < a.n;
-       idx += stride) {
+  for (long long x = blockIdx.x * static_cast<long long>(kOrchT) + threadIdx.x; x < total;
+       x += stride) {
+    // tuple: last offset <= x
+    long long lo = 0, hi = a.n - 1;
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) >> 1;
+      if (offsets[mid] <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    const long long idx = lo;
     const dtb_tuple t = a.tuples[idx];
     const int q_me = t.tp_me * t.dp_me, q_lm = t.tp_lm * t.dp_lm, q_mg = t.tp_mg * t.dp_mg;
+    long long r = x - offsets[idx];
+    int pe = 1;
+    for (;; ++pe) {
+      const long long c = (n - q_me * pe - q_mg) / q_lm;
+      if (r < c) break;
+      r -= c;
+    }
+    const int pl = static_cast<int>(r) + 1;
     const long long mbs = a.bs / t.dp_lm;
-    bool failed = false;
-    for (int pe = 1; !failed && q_me * pe + q_lm + q_mg <= n; ++pe)
-      for (int pl = 1; !failed && q_me * pe + q_lm * pl + q_mg <= n; ++pl)
-        for (int pg = 1; q_me * pe + q_lm * pl + q_mg * pg <= n; ++pg) {
-          if (a.vpp > 1 && mbs % (pe + pl + pg) != 0) continue;
-          dtb_candidate c;
-          c.tuple = t;
-          c.feasible = 1;
-          c.reason = DTB_REASON_NONE;
-          c.plan = plan_from(t, pe, pl, pg, a.bs, a.vpp);
-          if (!dev_memory_pass(a.cm, c.plan, nullptr)) continue;
-          const int e = dev_predict(a.cm, c.plan, a.stats, &c.times);
-          if (e) {
-            dev_fail_ordered(a.err, static_cast<unsigned long long>(idx * 3), e);
-            failed = true;
-            break;
-          }
-          ++count;
-          if (cand_better(c, mine)) mine = c;
-        }
+    for (int pg = 1; q_me * pe + q_lm * pl + q_mg * pg <= n; ++pg) {
+      if (a.vpp > 1 && mbs % (pe + pl + pg) != 0) continue;
+      dtb_candidate c;
+      c.tuple = t;
+      c.feasible = 1;
+      c.reason = DTB_REASON_NONE;
+      c.plan = plan_from(t, pe, pl, pg, a.bs, a.vpp);
+      if (!dev_memory_pass(a.cm, c.plan, nullptr)) continue;
+      const int e = dev_predict(a.cm, c.plan, a.stats, &c.times);
+      if (e) {
+        dev_fail_ordered(a.err, static_cast<unsigned long long>(idx * 3), e);
+        break;
+      }
+      ++count;
+      if (cand_better(c, mine)) mine = c;
+    }
   }
   atomicAdd(evaluated, count);
   s_best[threadIdx.x] = mine;
@@ -489,9 +517,38 @@ brute_kernel(OrchArgs a, unsigned long long* evaluated) {
   if (threadIdx.x == 0) a.block_best[blockIdx.x] = s_best[0];
 }
 
-cudaError_t launch_brute(const OrchArgs& a, int grid, unsigned long long* evaluated,
-                         cudaStream_t stream) {
-  brute_kernel<<<grid, kOrchT, 0, stream>>>(a, evaluated);
+size_t brute_scratch(long long n_tuples) {
+  size_t temp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<long long*>(nullptr),
+                                static_cast<long long*>(nullptr), static_cast<int>(n_tuples));
+  return 16 * static_cast<size_t>(n_tuples) + temp + 512;
+}
+
+// Counts, scans and returns (via *total_out, host) the pair count; then the
+// search.  scratch: brute_scratch(n) bytes.
+cudaError_t launch_brute(const OrchArgs& a, int max_grid, unsigned long long* evaluated,
+                         void* scratch, size_t bytes, cudaStream_t stream) {
+  auto* counts = static_cast<long long*>(scratch);
+  auto* offsets = counts + a.n;
+  char* temp = reinterpret_cast<char*>(offsets + a.n + 1);
+  size_t temp_bytes = bytes - 16 * static_cast<size_t>(a.n) - 16;
+  const int n = a.cm.cluster.total_gpus;
+  if (a.n == 0) return cudaSuccess;
+  brute_count_kernel<<<static_cast<unsigned>((a.n + 127) / 128), 128, 0, stream>>>(a.tuples, a.n,
+                                                                                    n, counts);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offsets,
+                                                static_cast<int>(a.n), stream);
+  if (e != cudaSuccess) return e;
+  long long last_off = 0, last_cnt = 0;
+  cudaMemcpyAsync(&last_off, offsets + a.n - 1, 8, cudaMemcpyDeviceToHost, stream);
+  cudaMemcpyAsync(&last_cnt, counts + a.n - 1, 8, cudaMemcpyDeviceToHost, stream);
+  e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return e;
+  const long long total = last_off + last_cnt;
+  long long grid = (total + kOrchT - 1) / kOrchT;
+  if (grid > max_grid) grid = max_grid;
+  if (grid < 1) grid = 1;
+  brute_kernel<<<static_cast<unsigned>(grid), kOrchT, 0, stream>>>(a, offsets, total, evaluated);
   return cudaGetLastError();
 }
 

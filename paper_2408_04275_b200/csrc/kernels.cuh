@@ -246,8 +246,11 @@ cudaError_t launch_enumerate(const dtb_cluster_spec& c, long long bs,
                              cudaStream_t stream);
 cudaError_t launch_orchestration(const OrchArgs& a, int grid,
                                  cudaStream_t stream);
-cudaError_t launch_brute(const OrchArgs& a, int grid, unsigned long long* evaluated,
-                         cudaStream_t stream);
+size_t brute_scratch(long long n_tuples);
+// block_best must hold max_grid records; the launcher synchronises `stream`
+// once (pair count).
+cudaError_t launch_brute(const OrchArgs& a, int max_grid, unsigned long long* evaluated,
+                         void* scratch, size_t bytes, cudaStream_t stream);
 cudaError_t launch_rigid(const DevCM& cm, const dtb_workload_stats& stats, long long bs, int vpp,
                          const long long* divs, int n_divs, dtb_candidate* out, DevErr* err,
                          cudaStream_t stream);
