@@ -11,6 +11,9 @@
 //  (t_iter, total_gpus, tuple, pp triple) picks the plan
 //  (orchestrator.cpp:211-233).  All arithmetic mirrors the reference op by
 //  op (compiled with -fmad=false), so t_iter and the plan are bit-exact.
+#include <algorithm>
+#include <vector>
+
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
@@ -91,15 +94,24 @@ cudaError_t launch_enumerate(const dtb_cluster_spec& c, long long bs,
                              long long* count_dev, dtb_tuple* out,
                              long long capacity, void* scratch,
                              cudaStream_t stream) {
-  // scratch: divs[4096] | n_divs | counts[] | offsets[] | cub temp
+  // scratch: divs[4096] | n_divs | counts[] | offsets[] | cub temp.  The
+  // ascending divisors of the global batch (orchestrator.cpp:30-40) are
+  // formed on the host — a single-thread device kernel plus a readback cost
+  // ~50 us per search.
   char* p = static_cast<char*>(scratch);
   long long* divs = reinterpret_cast<long long*>(p);
-  int* n_divs = reinterpret_cast<int*>(p + 4096 * 8);
-  divisors_kernel<<<1, 1, 0, stream>>>(bs, divs, n_divs);
-  int D = 0;
-  cudaError_t e = cudaMemcpyAsync(&D, n_divs, sizeof(int), cudaMemcpyDeviceToHost, stream);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamSynchronize(stream);
+  std::vector<long long> hd;
+  for (long long d = 1; d * d <= bs; ++d)
+    if (bs % d == 0) {
+      hd.push_back(d);
+      if (d != bs / d) hd.push_back(bs / d);
+    }
+  std::sort(hd.begin(), hd.end());
+  const int D = static_cast<int>(hd.size());
+  if (D > 4096) return cudaErrorInvalidValue;
+  // pageable source: the copy is staged before this call returns
+  cudaError_t e = cudaMemcpyAsync(divs, hd.data(), sizeof(long long) * D,
+                                  cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) return e;
   const long long n_prefix = 16LL * D * D * 4;
   long long* counts = reinterpret_cast<long long*>(p + 4096 * 8 + 256);
