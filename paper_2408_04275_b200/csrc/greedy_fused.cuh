@@ -59,7 +59,7 @@ __device__ __forceinline__ unsigned block_incl_scan_u32(unsigned v, int* s, unsi
 template <int T, bool ASC, typename SizeFn, typename EmitFn>
 __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn& sizes,
                              const EmitFn& emit, FusedGreedySmem& G, int* tmp,
-                             unsigned long long* prof = nullptr) {
+                             long long* tmpll, unsigned long long* prof = nullptr) {
   unsigned long long n_full = 0, n_general = 0;
   static_assert(T >= 2 * kFG && T % kFG == 0, "one entry per thread, two in a merge");
   const int tid = threadIdx.x;
@@ -96,14 +96,24 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
       }
       int nfull;  // filled entries are a prefix of A
       block_excl_scan<T>(full ? 1 : 0, tmp, &nfull);
-      for (int q = tid; q < z; q += T) {
-        int lo = 0, hi = r - 1;  // last entry whose capacity prefix is <= q
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (G.pre[mid] <= q) lo = mid;
-          else hi = mid - 1;
+      if (k == 0) {
+        // first run of the batch: every entry is empty (capacity cap, in gid
+        // order), so the entry of item q is q / cap — no search
+        const unsigned ucap = static_cast<unsigned>(cap);
+        for (int q = tid; q < z; q += T) {
+          const int j = static_cast<int>(static_cast<unsigned>(q) / ucap);
+          emit(k + q, G.AG[j], q - j * cap);
         }
-        emit(k + q, G.AG[lo], G.TC[lo] + (q - G.pre[lo]));
+      } else {
+        for (int q = tid; q < z; q += T) {
+          int lo = 0, hi = r - 1;  // last entry whose capacity prefix is <= q
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (G.pre[mid] <= q) lo = mid;
+            else hi = mid - 1;
+          }
+          emit(k + q, G.AG[lo], G.TC[lo] + (q - G.pre[lo]));
+        }
       }
       __syncthreads();
       if (tid < r && tid >= nfull) {
@@ -140,9 +150,15 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
             const bool ok = t < Tr;
             const unsigned s0 = ok ? sizes(k + t * r) : 0u;
             const unsigned sl = ok ? sizes(k + t * r + r - 1) : 0u;
-            unsigned tot0, totl;
-            const unsigned inc0 = block_incl_scan_u32<T>(s0, tmp, &tot0);
-            const unsigned incl = block_incl_scan_u32<T>(sl, tmp, &totl);
+            // both columns in one 64-bit scan: each half's sum stays < 2^31
+            // (loads of <= 16384 items of <= 65534), so no carry crosses
+            long long tot;
+            const unsigned long long inc = static_cast<unsigned long long>(block_incl_scan_ll<T>(
+                static_cast<long long>((static_cast<unsigned long long>(sl) << 32) | s0),
+                tmpll, &tot));
+            const unsigned inc0 = static_cast<unsigned>(inc), incl = static_cast<unsigned>(inc >> 32);
+            const unsigned tot0 = static_cast<unsigned>(tot),
+                           totl = static_cast<unsigned>(static_cast<unsigned long long>(tot) >> 32);
             const unsigned new0 = l0 + c0 + inc0;
             const unsigned last = ll + cl + (incl - sl);
             const int f = ok && !fkey_lt(last, gl, new0, g0) ? t : 0x7fffffff;

@@ -466,10 +466,10 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
       S.out16[g * capP + slot] = static_cast<unsigned short>(k);
     };
     if (desc)
-      greedy_fused<kFusedT, false>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp,
+      greedy_fused<kFusedT, false>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll,
                                    a.prof ? a.prof + b * 8 + 6 : nullptr);
     else
-      greedy_fused<kFusedT, true>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp,
+      greedy_fused<kFusedT, true>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll,
                                   a.prof ? a.prof + b * 8 + 6 : nullptr);
     if (a.prof && tid == 0) a.prof[b * 8 + 3] = globaltimer();
     // ---- 4. group offsets of the flat order and the greedy block loads
