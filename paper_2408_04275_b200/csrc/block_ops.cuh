@@ -198,183 +198,12 @@ __device__ void tile_radix_sort(K* keys, V* vals, int n, int lo_bit,
   }
 }
 
-// Lanes of the warp whose digit equals this lane's, among lanes with `ok`
-// set.  MATCH.ANY measured on B200 (tools/bench_match.cu): ~2.4 SM-cycles
-// per warp-op versus ~21 for the 7-ballot restatement.
-template <int RB>
-__device__ __forceinline__ unsigned digit_peers(unsigned d, bool ok) {
-  const unsigned peers = __match_any_sync(kFull, ok ? d : 0xffffffffu);
-  return ok ? peers : 0u;
-}
-
-// One stable counting pass over n <= T*ITEMS 32-bit items in place, digit
-// given by digit(pos, item) in [0, 1 << RB).  Same warp-striped ranking as
-// tile_radix_sort; used both for the cost-key passes (digit = key bits) and
-// for the group partition after the greedy (digit = group id).
-template <int T, int ITEMS, int RB, typename DigitFn>
-__device__ void tile_pass_u32(unsigned int* items, int n, const DigitFn& digit, int* cnt,
-                              int* scan_tmp) {
-  constexpr int W = T / 32;
-  constexpr int D = 1 << RB;
-  const int lane = lane_id(), w = warp_id();
-  const unsigned lt = lanemask_lt();
-  for (int i = threadIdx.x; i < D * W; i += T) cnt[i] = 0;
-  static_assert(ITEMS % 2 == 0, "ranks are packed in pairs");
-  unsigned int k[ITEMS];
-  unsigned int rk[ITEMS / 2];  // two 16-bit ranks per register; digits recomputed
-  // all item loads first: the ranking chain below then only waits on the
-  // per-digit counters, not on item loads
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int pos = w * 32 * ITEMS + i * 32 + lane;
-    k[i] = pos < n ? items[pos] : 0u;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int pos = w * 32 * ITEMS + i * 32 + lane;
-    const bool ok = pos < n;
-    const unsigned d = ok ? static_cast<unsigned>(digit(pos, k[i])) : 0u;
-    const unsigned peers = digit_peers<RB>(d, ok);
-    int before = 0;
-    if (ok) before = cnt[w * D + d];
-    __syncwarp();
-    if (ok && (peers & lt) == 0) cnt[w * D + d] = before + __popc(peers);
-    __syncwarp();
-    const unsigned r = static_cast<unsigned>(before + __popc(peers & lt));
-    if (i & 1) rk[i >> 1] |= r << 16;
-    else rk[i >> 1] = r;
-  }
-  __syncthreads();
-  constexpr int PER = (D * W + T - 1) / T;
-  int local[PER];
-  int sum = 0;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const int idx = threadIdx.x * PER + j;
-    local[j] = idx < D * W ? cnt[(idx % W) * D + idx / W] : 0;
-    sum += local[j];
-  }
-  int total;
-  int base = block_excl_scan<T>(sum, scan_tmp, &total);
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const int idx = threadIdx.x * PER + j;
-    if (idx < D * W) cnt[(idx % W) * D + idx / W] = base;
-    base += local[j];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int pos = w * 32 * ITEMS + i * 32 + lane;
-    if (pos < n) {
-      const unsigned d = static_cast<unsigned>(digit(pos, k[i]));
-      const unsigned r = (i & 1) ? (rk[i >> 1] >> 16) : (rk[i >> 1] & 0xffffu);
-      items[cnt[w * D + d] + r] = k[i];
-    }
-  }
-  __syncthreads();
-}
-
 // Bijective in-block swizzle of sorted positions (stays inside its 32-item
 // block): strided gathers of sorted items (stride r = active groups in the
 // greedy, consecutive slots of one group in the write-out) spread over banks.
 __device__ __forceinline__ int swz(int k) {
   const int x = k >> 5;
   return k ^ ((x ^ (x >> 2) ^ (x >> 4)) & 31);
-}
-
-// One stable counting pass of a block radix sort of u16 sample indices by
-// the u16 keys key[idx], in place, over ALL T * ITEMS slots (the caller pads
-// past n with indices whose key has the largest digit in every pass, so they
-// stay at the end and no per-item bounds predicates are needed).  Only the
-// indices stay live across the block scan, two per register (ITEMS / 2
-// registers); keys are re-read from shared memory and per-item ranks are
-// parked there (u16 `ranks`).  Warp-striped ranking as in tile_pass_u32
-// keeps equal digits in input order.  SWZ: write swizzled positions.
-// key[v] for a shared-memory u16 array, address formed inside the asm so the
-// compiler cannot keep ITEMS addresses alive between the two phases of a
-// pass (it would rather spill them than recompute one shift-add).
-__device__ __forceinline__ unsigned lds_u16_at(unsigned base, unsigned v) {
-  unsigned short x;
-  asm volatile("{\n\t.reg .u32 a;\n\tmad.lo.u32 a, %1, 2, %2;\n\tld.shared.u16 %0, [a];\n\t}"
-               : "=h"(x)
-               : "r"(v), "r"(base));
-  return x;
-}
-
-template <int T, int ITEMS, int RB, bool SWZ, typename DigitFn>
-__device__ void tile_pass_idx16(unsigned short* idx, const unsigned short* key,
-                                const DigitFn& digit, int* cnt, int* scan_tmp,
-                                unsigned short* ranks) {
-  constexpr int W = T / 32;
-  constexpr int D = 1 << RB;
-  constexpr int PAIRS = (ITEMS + 1) / 2;
-  // counters are digit-major (cnt[d * W + w]): the stable (digit, warp)
-  // order is then a contiguous scan
-  const int lane = lane_id(), w = warp_id();
-  const unsigned lt = lanemask_lt();
-  for (int i = threadIdx.x; i < D * W; i += T) cnt[i] = 0;
-  unsigned int k2[PAIRS];
-  const int base_pos = w * 32 * ITEMS + lane;
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const unsigned v = idx[base_pos + i * 32];
-    if (i & 1) k2[i >> 1] |= v << 16;
-    else k2[i >> 1] = v;
-  }
-  // opaque: the compiler would otherwise keep ITEMS unpacked registers
-#pragma unroll
-  for (int q = 0; q < PAIRS; ++q) asm volatile("" : "+r"(k2[q]));
-  auto item = [&](int i) -> unsigned { return (i & 1) ? (k2[i >> 1] >> 16) : (k2[i >> 1] & 0xffffu); };
-  const unsigned key_base = static_cast<unsigned>(__cvta_generic_to_shared(key));
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    // peers by MATCH.ANY; the lowest peer reserves the group's ranks with
-    // one shared atomic whose return value is the count before this slot:
-    // no load -> add -> store chain between consecutive slots of a warp
-    // (same-address atomics of a warp retire in program order)
-    const unsigned d = static_cast<unsigned>(digit(lds_u16_at(key_base, item(i))));
-    const unsigned peers = __match_any_sync(kFull, d);
-    const int leader = __ffs(peers) - 1;
-    int old = 0;
-    if (lane == leader) old = atomicAdd(cnt + d * W + w, __popc(peers));
-    const int before = __shfl_sync(kFull, old, leader);
-    ranks[base_pos + i * 32] = static_cast<unsigned short>(before + __popc(peers & lt));
-  }
-  __syncthreads();
-  constexpr int PER = (D * W + T - 1) / T;
-  int local[PER];
-  int sum = 0;
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const int x = threadIdx.x * PER + j;
-    local[j] = x < D * W ? cnt[x] : 0;
-    sum += local[j];
-  }
-  int total;
-  int base = block_excl_scan<T>(sum, scan_tmp, &total);
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const int x = threadIdx.x * PER + j;
-    if (x < D * W) cnt[x] = base;
-    base += local[j];
-  }
-  // the key base address for the scatter phase comes back from memory, so
-  // ptxas cannot prove the key addresses equal to the ranking phase's and
-  // keep them (spilled) across the scan instead of recomputing them
-  if (threadIdx.x == 0) cnt[D * W] = static_cast<int>(key_base);
-  __syncthreads();
-  const unsigned key_base2 = static_cast<unsigned>(*static_cast<volatile int*>(cnt + D * W));
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const unsigned v = item(i);
-    const unsigned d = static_cast<unsigned>(digit(lds_u16_at(key_base2, v)));
-    const int dst = cnt[d * W + w] + ranks[base_pos + i * 32];
-    idx[SWZ ? swz(dst) : dst] = static_cast<unsigned short>(v);
-  }
-  __syncthreads();
 }
 
 // One stable counting pass (per-THREAD counters, blocked arrangement) of a
