@@ -57,7 +57,10 @@ def parse():
 
 
 def dist_init():
-    os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries exactly one JSON line
+    # stdout carries exactly one JSON line: NCCL's INFO/VERSION banner
+    # ("NCCL version ...") would precede it on rank 0
+    if not os.environ.get("DTB_KEEP_NCCL_DEBUG"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
