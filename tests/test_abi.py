@@ -42,3 +42,12 @@ def test_oracles_export_the_same_abi(ref, port):
             continue
         assert ref.lib.has(name), "mmref_" + name
         assert port.lib.has(name), "mmport_" + name
+
+
+def test_product_path_fails_loudly_without_the_library(tmp_path, monkeypatch):
+    """No CPU fallback: a missing libdisttrain_b200.so is an error."""
+    from paper_2408_04275_b200 import native
+    monkeypatch.setattr(native, "LIB_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(native, "_lib", None)
+    with pytest.raises(FileNotFoundError):
+        native.library()
