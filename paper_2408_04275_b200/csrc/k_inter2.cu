@@ -61,8 +61,16 @@ __device__ __noinline__ Row4 inter_row_direct(const InterArgs* a, long long te, 
 constexpr int kBRing = 16;
 
 // Shared memory per thread (bytes).
+// Pending list row stride (bytes): l rounded up to whole words, plus one
+// word so the stride in words is odd (bank-conflict-free row starts).
+__host__ __device__ inline int inter_pl_stride(int l) {
+  int w = (l + 3) / 4;
+  if ((w & 1) == 0) ++w;
+  return 4 * w;
+}
+
 __host__ __device__ inline size_t inter_tok_bytes_per_thread(int l) {
-  return static_cast<size_t>(l) * (3 * 8 + 2 + 1) + 2 * 8 * kBRing;
+  return static_cast<size_t>(l) * (3 * 8 + 2 + 1) + 2 * 8 * kBRing + inter_pl_stride(l);
 }
 
 template <int PE, int PB, int PG>
@@ -83,6 +91,10 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
       (reinterpret_cast<size_t>(colT + static_cast<size_t>(l) * T) + 7) & ~size_t(7));
   double* colBG = colBE + static_cast<size_t>(kBRing) * T;
   unsigned char* colR = reinterpret_cast<unsigned char*>(colBG + static_cast<size_t>(kBRing) * T);
+  // per-thread pending list (ascending indices), row-contiguous: [T][stride]
+  const int pls = inter_pl_stride(l);
+  unsigned char* colPL = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<size_t>(colR + static_cast<size_t>(l) * T) + 3) & ~size_t(3));
 
   UnitEval ub;
   ub.init(a.cm, a.plan, DTB_BACKBONE);
@@ -165,6 +177,23 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     pend[w] = lo >= l ? 0u : (l - lo >= 32 ? 0xffffffffu : ((1u << (l - lo)) - 1u));
   }
   int npend = l;
+  // the same set as a compacted ascending list: the hot O(npend) loops then
+  // run exactly npend iterations in every lane (npend is uniform across the
+  // warp) instead of l predicated ones
+  unsigned char* PL = colPL + static_cast<size_t>(t) * pls;
+  for (int q = 0; q < l; ++q) PL[q] = static_cast<unsigned char>(q);
+  auto list_remove = [&](int pos) {
+    for (int q = pos; q + 1 < npend; ++q) PL[q] = PL[q + 1];
+  };
+  auto list_find = [&](int idx) -> int {  // position of idx (ascending list)
+    int lo = 0, hi = npend - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (PL[mid] < idx) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
   auto pend_word = [&](int w) -> unsigned {
     unsigned r = 0u;
 #pragma unroll
@@ -196,28 +225,26 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     }
     return best;
   };
-  // select_closest, one pick: smallest (|r - key|, key > r, index).  A
-  // uniform loop over all indices (lanes of a warp hold different problems
-  // whose pending sets differ; bit-scan loops would diverge)
-  auto pick_closest = [&](double residual) -> int {
-    int best = -1;
+  // select_closest, one pick: smallest (|r - key|, key > r, index) over the
+  // pending list (ascending, so the incumbent always has the lower index);
+  // *pos gets the list position of the pick
+  auto pick_closest = [&](double residual, int* pos) -> int {
+    int best = -1, bq = 0;
     double db = 0.0;
     bool bover = false;
-    for (int w = 0; w * 32 < l; ++w) {
-      const unsigned m = pend_word(w);
-      const int hi = min(32, l - w * 32);
 #pragma unroll 4
-      for (int b = 0; b < hi; ++b) {
-        const int idx = w * 32 + b;
-        const double k = K(idx);
-        const double da = fabs(residual - k);
-        const bool over = !(k <= residual);
-        const bool take = ((m >> b) & 1u) && (best < 0 || da < db || (da == db && !over && bover));
-        best = take ? idx : best;
-        db = take ? da : db;
-        bover = take ? over : bover;
-      }
+    for (int q = 0; q < npend; ++q) {
+      const int idx = PL[q];
+      const double k = K(idx);
+      const double da = fabs(residual - k);
+      const bool over = !(k <= residual);
+      const bool take = best < 0 || da < db || (da == db && !over && bover);
+      best = take ? idx : best;
+      bq = take ? q : bq;
+      db = take ? da : db;
+      bover = take ? over : bover;
     }
+    *pos = bq;
     return best;
   };
 
@@ -232,6 +259,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   const int first = pick_min();
   place(first);
   clear(first);
+  list_remove(list_find(first));
   --npend;
   const int tail_n = min(DEV - 1, npend);
   int rear[DEV > 1 ? DEV - 1 : 1];
@@ -243,6 +271,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     for (int z = 0; z < (DEV > 1 ? DEV - 1 : 1); ++z)
       if (z == q) rear[z] = r;
     clear(r);
+    list_remove(list_find(r));
     --npend;
   }
 
@@ -355,21 +384,13 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     const int t_target = 2 * wi + 2 * P - 1;  // tick of B(wi, 0)
     // pending means per unit: sequential sums in ascending index order
     {
-      // x + 0.0 == x for every partial sum here (never -0.0: all terms are
-      // >= +0), so non-pending rows contribute an exact +0.0 and the loop
-      // is uniform across the warp
+      // sequential over the ascending pending list (src/reorder.cpp:191-201)
       double sE = 0.0, sG = 0.0;
-      for (int w = 0; w * 32 < l; ++w) {
-        const unsigned m = pend_word(w);
-        const int hi = min(32, l - w * 32);
 #pragma unroll 4
-        for (int b = 0; b < hi; ++b) {
-          const bool on = (m >> b) & 1u;
-          const int idx = w * 32 + b;
-          const double f = F(idx), g = G(idx);
-          sE += on ? f : 0.0;
-          sG += on ? g : 0.0;
-        }
+      for (int q = 0; q < npend; ++q) {
+        const int idx = PL[q];
+        sE += F(idx);
+        sG += G(idx);
       }
       const double c = static_cast<double>(npend);
       meanE = sE / c;
@@ -399,10 +420,12 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     const int take = step == 1 ? min(DEV - 1, npend) : 1;
     double residual = target;
     for (int q = 0; q < take; ++q) {
-      const int pick = pick_closest(residual);
+      int ppos;
+      const int pick = pick_closest(residual, &ppos);
       residual -= K(pick);
       place(pick);
       clear(pick);
+      list_remove(ppos);
       --npend;
     }
     np = nret;
@@ -456,7 +479,7 @@ cudaError_t launch_inter_tok(const InterArgs& a, cudaStream_t stream) {
   int dev = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t fixed = 8 * static_cast<size_t>(a.l + 1) + 64;
+  const size_t fixed = 8 * static_cast<size_t>(a.l + 1) + 64 + 8;
   const size_t per = inter_tok_bytes_per_thread(a.l);
   int T = 128;
   while (T > 1 && fixed + per * T + 64 > static_cast<size_t>(max_smem)) --T;
