@@ -177,22 +177,32 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     pend[w] = lo >= l ? 0u : (l - lo >= 32 ? 0xffffffffu : ((1u << (l - lo)) - 1u));
   }
   int npend = l;
-  // the same set as a compacted ascending list: the hot O(npend) loops then
-  // run exactly npend iterations in every lane (npend is uniform across the
-  // warp) instead of l predicated ones
+  // the same set as an ascending list with lazy deletion: removed entries
+  // become holes (0xff) and the list is compacted every kCompact removals,
+  // so the hot loops run `plen` iterations in every lane (removals are
+  // uniform across the warp: one per step) instead of l predicated ones,
+  // and no lane shifts bytes on its own schedule
+  constexpr int kCompact = 8;
   unsigned char* PL = colPL + static_cast<size_t>(t) * pls;
   for (int q = 0; q < l; ++q) PL[q] = static_cast<unsigned char>(q);
+  int plen = l, holes = 0;
   auto list_remove = [&](int pos) {
-    for (int q = pos; q + 1 < npend; ++q) PL[q] = PL[q + 1];
-  };
-  auto list_find = [&](int idx) -> int {  // position of idx (ascending list)
-    int lo = 0, hi = npend - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (PL[mid] < idx) lo = mid + 1;
-      else hi = mid;
+    PL[pos] = 0xff;
+    if (++holes == kCompact) {
+      int w = 0;
+      for (int q = 0; q < plen; ++q) {
+        const unsigned char v = PL[q];
+        PL[w] = v;
+        w += v != 0xff;
+      }
+      plen = w;
+      holes = 0;
     }
-    return lo;
+  };
+  auto list_find = [&](int idx) -> int {  // position of idx (linear; start-up only)
+    int q = 0;
+    while (PL[q] != idx) ++q;
+    return q;
   };
   auto pend_word = [&](int w) -> unsigned {
     unsigned r = 0u;
@@ -233,12 +243,14 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     double db = 0.0;
     bool bover = false;
 #pragma unroll 4
-    for (int q = 0; q < npend; ++q) {
-      const int idx = PL[q];
+    for (int q = 0; q < plen; ++q) {
+      const int raw = PL[q];
+      const bool live = raw != 0xff;
+      const int idx = live ? raw : 0;
       const double k = K(idx);
       const double da = fabs(residual - k);
       const bool over = !(k <= residual);
-      const bool take = best < 0 || da < db || (da == db && !over && bover);
+      const bool take = live && (best < 0 || da < db || (da == db && !over && bover));
       best = take ? idx : best;
       bq = take ? q : bq;
       db = take ? da : db;
@@ -386,11 +398,15 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     {
       // sequential over the ascending pending list (src/reorder.cpp:191-201)
       double sE = 0.0, sG = 0.0;
+      // holes add an exact +0.0 (no partial sum is -0.0: every term >= +0)
 #pragma unroll 4
-      for (int q = 0; q < npend; ++q) {
-        const int idx = PL[q];
-        sE += F(idx);
-        sG += G(idx);
+      for (int q = 0; q < plen; ++q) {
+        const int raw = PL[q];
+        const bool live = raw != 0xff;
+        const int idx = live ? raw : 0;
+        const double f = F(idx), g = G(idx);
+        sE += live ? f : 0.0;
+        sG += live ? g : 0.0;
       }
       const double c = static_cast<double>(npend);
       meanE = sE / c;
