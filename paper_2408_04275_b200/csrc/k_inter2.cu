@@ -70,7 +70,7 @@ __host__ __device__ inline int inter_pl_stride(int l) {
 }
 
 __host__ __device__ inline size_t inter_tok_bytes_per_thread(int l) {
-  return static_cast<size_t>(l) * (3 * 8 + 2 + 1) + 2 * 8 * kBRing + inter_pl_stride(l);
+  return static_cast<size_t>(l) * (3 * 8 + 2 + 1) + 4 * 8 * kBRing + inter_pl_stride(l);
 }
 
 template <int PE, int PB, int PG>
@@ -90,7 +90,9 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   double* colBE = reinterpret_cast<double*>(
       (reinterpret_cast<size_t>(colT + static_cast<size_t>(l) * T) + 7) & ~size_t(7));
   double* colBG = colBE + static_cast<size_t>(kBRing) * T;
-  unsigned char* colR = reinterpret_cast<unsigned char*>(colBG + static_cast<size_t>(kBRing) * T);
+  double* colFE = colBG + static_cast<size_t>(kBRing) * T;  // placed rows' forward values
+  double* colFG = colFE + static_cast<size_t>(kBRing) * T;
+  unsigned char* colR = reinterpret_cast<unsigned char*>(colFG + static_cast<size_t>(kBRing) * T);
   // per-thread pending list (ascending indices), row-contiguous: [T][stride]
   const int pls = inter_pl_stride(l);
   unsigned char* colPL = reinterpret_cast<unsigned char*>(
@@ -112,13 +114,18 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   const long long prob = blockIdx.x * static_cast<long long>(T) + t;
   if (prob >= a.batch) return;
   int* out = a.orders + prob * l;
-  auto F = [&](int i) -> double& { return colF[static_cast<size_t>(i) * T + t]; };
-  auto G = [&](int i) -> double& { return colG[static_cast<size_t>(i) * T + t]; };
-  auto K = [&](int i) -> double& { return colK[static_cast<size_t>(i) * T + t]; };
+  // F/G/K are indexed by PENDING-LIST POSITION (not sample index): the hot
+  // loops then read the same address offset in every lane (conflict-free,
+  // no dependent index load); placed rows keep theirs in rings
+  auto F = [&](int q) -> double& { return colF[static_cast<size_t>(q) * T + t]; };
+  auto G = [&](int q) -> double& { return colG[static_cast<size_t>(q) * T + t]; };
+  auto K = [&](int q) -> double& { return colK[static_cast<size_t>(q) * T + t]; };
   auto TK = [&](int i) -> unsigned short& { return colT[static_cast<size_t>(i) * T + t]; };
   auto RET = [&](int i) -> unsigned char& { return colR[static_cast<size_t>(i) * T + t]; };
   auto BE = [&](int pos) -> double& { return colBE[static_cast<size_t>(pos % kBRing) * T + t]; };
   auto BG = [&](int pos) -> double& { return colBG[static_cast<size_t>(pos % kBRing) * T + t]; };
+  auto FE = [&](int pos) -> double& { return colFE[static_cast<size_t>(pos % kBRing) * T + t]; };
+  auto FG = [&](int pos) -> double& { return colFG[static_cast<size_t>(pos % kBRing) * T + t]; };
 
   // ---- fill: rows of the problem's microbatches (staged order)
   const long long bb = prob / a.groups;
@@ -165,6 +172,22 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     }
   };
 
+  // forward values of a row by sample index (cold path)
+  auto fwd_row = [&](int idx, double* ef, double* gf) {
+    if (!direct_rows) {
+      const double4 r = ld_row(a.table.eg + TK(idx));
+      *ef = r.x;
+      *gf = r.z;
+    } else {
+      const long long v = a.span == 1 ? a.tok.get(bb, grp * l + idx, true)
+                                      : a.mbsum[prob * static_cast<long long>(l) + idx];
+      double key;
+      int e2 = 0;
+      const Row4 r = inter_row_direct(&a, v, &key, &e2);
+      *ef = r.ef;
+      *gf = r.gf;
+    }
+  };
   for (int i = 0; i < l; ++i) out[i] = i;
   if (l <= 1 || DEV == 1) return;
 
@@ -192,17 +215,16 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
       int w = 0;
       for (int q = 0; q < plen; ++q) {
         const unsigned char v = PL[q];
+        const double f = F(q), g = G(q), k = K(q);
         PL[w] = v;
+        F(w) = f;
+        G(w) = g;
+        K(w) = k;
         w += v != 0xff;
       }
       plen = w;
       holes = 0;
     }
-  };
-  auto list_find = [&](int idx) -> int {  // position of idx (linear; start-up only)
-    int q = 0;
-    while (PL[q] != idx) ++q;
-    return q;
   };
   auto pend_word = [&](int w) -> unsigned {
     unsigned r = 0u;
@@ -216,23 +238,22 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     for (int w = 0; w < MW; ++w)
       if (w == (idx >> 5)) pend[w] &= ~(1u << (idx & 31));
   };
-  // select_min, one pick: smallest (key, index)
-  auto pick_min = [&]() -> int {
-    int best = -1;
+  // select_min, one pick: smallest (key, index) over the pending list;
+  // *pos gets its list position
+  auto pick_min = [&](int* pos) -> int {
+    int best = -1, bq = 0;
     double kb = 0.0;
-#pragma unroll
-    for (int w = 0; w < MW; ++w) {
-      unsigned m = pend[w];
-      while (m) {
-        const int idx = w * 32 + __ffs(m) - 1;
-        m &= m - 1;
-        const double k = K(idx);
-        if (best < 0 || k < kb) {
-          best = idx;
-          kb = k;
-        }
+    for (int q = 0; q < plen; ++q) {
+      const int raw = PL[q];
+      if (raw == 0xff) continue;
+      const double k = K(q);
+      if (best < 0 || k < kb) {
+        best = raw;
+        bq = q;
+        kb = k;
       }
     }
+    *pos = bq;
     return best;
   };
   // select_closest, one pick: smallest (|r - key|, key > r, index) over the
@@ -246,8 +267,8 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     for (int q = 0; q < plen; ++q) {
       const int raw = PL[q];
       const bool live = raw != 0xff;
-      const int idx = live ? raw : 0;
-      const double k = K(idx);
+      const int idx = raw;
+      const double k = K(q);
       const double da = fabs(residual - k);
       const bool over = !(k <= residual);
       const bool take = live && (best < 0 || da < db || (da == db && !over && bover));
@@ -261,29 +282,43 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   };
 
   int nret = 0;
-  auto place = [&](int idx) {
+  auto place = [&](int idx, int q) {
     double eb, gb;
     bwd_row(idx, &eb, &gb);
     BE(nret) = eb;
     BG(nret) = gb;
+    FE(nret) = F(q);
+    FG(nret) = G(q);
     RET(nret++) = static_cast<unsigned char>(idx);
   };
-  const int first = pick_min();
-  place(first);
+  int fpos;
+  const int first = pick_min(&fpos);
+  place(first, fpos);
   clear(first);
-  list_remove(list_find(first));
+  list_remove(fpos);
   --npend;
   const int tail_n = min(DEV - 1, npend);
-  int rear[DEV > 1 ? DEV - 1 : 1];
+  constexpr int NR = DEV > 1 ? DEV - 1 : 1;
+  int rear[NR];
+  double rearF[NR], rearG[NR];
 #pragma unroll
-  for (int q = 0; q < (DEV > 1 ? DEV - 1 : 1); ++q) rear[q] = 0;
+  for (int q = 0; q < NR; ++q) {
+    rear[q] = 0;
+    rearF[q] = rearG[q] = 0.0;
+  }
   for (int q = 0; q < tail_n; ++q) {
-    const int r = pick_min();
+    int rpos;
+    const int r = pick_min(&rpos);
+    const double rf = F(rpos), rg = G(rpos);
 #pragma unroll
-    for (int z = 0; z < (DEV > 1 ? DEV - 1 : 1); ++z)
-      if (z == q) rear[z] = r;
+    for (int z = 0; z < NR; ++z)
+      if (z == q) {
+        rear[z] = r;
+        rearF[z] = rf;
+        rearG[z] = rg;
+      }
     clear(r);
-    list_remove(list_find(r));
+    list_remove(rpos);
     --npend;
   }
 
@@ -314,12 +349,19 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     }
     const bool enc = s < PE;
     if (r < np) {
-      const int row = RET(r);
-      return enc ? F(row) : G(row);
+      if (r + kBRing >= nret) return enc ? FE(r) : FG(r);
+      // outside the ring (not reached by the 1F1B windows): from the table
+      double ef, gf;
+      fwd_row(RET(r), &ef, &gf);
+      return enc ? ef : gf;
     }
     if (r < np + npend) return enc ? meanE : meanG;
-    const int row = rear_row(r - np - npend);
-    return enc ? F(row) : G(row);
+    const int q = r - np - npend;
+    double x = 0.0;
+#pragma unroll
+    for (int z = 0; z < NR; ++z)
+      if (z == q) x = enc ? rearF[z] : rearG[z];
+    return x;
   };
   auto candB = [&](int r, int s) -> double {
     if (r >= np && r < np + npend) {
@@ -401,10 +443,8 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
       // holes add an exact +0.0 (no partial sum is -0.0: every term >= +0)
 #pragma unroll 4
       for (int q = 0; q < plen; ++q) {
-        const int raw = PL[q];
-        const bool live = raw != 0xff;
-        const int idx = live ? raw : 0;
-        const double f = F(idx), g = G(idx);
+        const bool live = PL[q] != 0xff;
+        const double f = F(q), g = G(q);
         sE += live ? f : 0.0;
         sG += live ? g : 0.0;
       }
@@ -438,8 +478,8 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     for (int q = 0; q < take; ++q) {
       int ppos;
       const int pick = pick_closest(residual, &ppos);
-      residual -= K(pick);
-      place(pick);
+      residual -= K(ppos);
+      place(pick, ppos);
       clear(pick);
       list_remove(ppos);
       --npend;
