@@ -70,7 +70,7 @@ __host__ __device__ inline int inter_pl_stride(int l) {
 }
 
 __host__ __device__ inline size_t inter_tok_bytes_per_thread(int l) {
-  return static_cast<size_t>(l) * (3 * 8 + 2 + 1) + 4 * 8 * kBRing + inter_pl_stride(l);
+  return static_cast<size_t>(l) * (3 * 8 + 2 + 1) + 2 * 8 * kBRing + inter_pl_stride(l);
 }
 
 template <int PE, int PB, int PG>
@@ -90,9 +90,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   double* colBE = reinterpret_cast<double*>(
       (reinterpret_cast<size_t>(colT + static_cast<size_t>(l) * T) + 7) & ~size_t(7));
   double* colBG = colBE + static_cast<size_t>(kBRing) * T;
-  double* colFE = colBG + static_cast<size_t>(kBRing) * T;  // placed rows' forward values
-  double* colFG = colFE + static_cast<size_t>(kBRing) * T;
-  unsigned char* colR = reinterpret_cast<unsigned char*>(colFG + static_cast<size_t>(kBRing) * T);
+  unsigned char* colR = reinterpret_cast<unsigned char*>(colBG + static_cast<size_t>(kBRing) * T);
   // per-thread pending list (ascending indices), row-contiguous: [T][stride]
   const int pls = inter_pl_stride(l);
   unsigned char* colPL = reinterpret_cast<unsigned char*>(
@@ -114,18 +112,13 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   const long long prob = blockIdx.x * static_cast<long long>(T) + t;
   if (prob >= a.batch) return;
   int* out = a.orders + prob * l;
-  // F/G/K are indexed by PENDING-LIST POSITION (not sample index): the hot
-  // loops then read the same address offset in every lane (conflict-free,
-  // no dependent index load); placed rows keep theirs in rings
-  auto F = [&](int q) -> double& { return colF[static_cast<size_t>(q) * T + t]; };
-  auto G = [&](int q) -> double& { return colG[static_cast<size_t>(q) * T + t]; };
-  auto K = [&](int q) -> double& { return colK[static_cast<size_t>(q) * T + t]; };
+  auto F = [&](int i) -> double& { return colF[static_cast<size_t>(i) * T + t]; };
+  auto G = [&](int i) -> double& { return colG[static_cast<size_t>(i) * T + t]; };
+  auto K = [&](int i) -> double& { return colK[static_cast<size_t>(i) * T + t]; };
   auto TK = [&](int i) -> unsigned short& { return colT[static_cast<size_t>(i) * T + t]; };
   auto RET = [&](int i) -> unsigned char& { return colR[static_cast<size_t>(i) * T + t]; };
   auto BE = [&](int pos) -> double& { return colBE[static_cast<size_t>(pos % kBRing) * T + t]; };
   auto BG = [&](int pos) -> double& { return colBG[static_cast<size_t>(pos % kBRing) * T + t]; };
-  auto FE = [&](int pos) -> double& { return colFE[static_cast<size_t>(pos % kBRing) * T + t]; };
-  auto FG = [&](int pos) -> double& { return colFG[static_cast<size_t>(pos % kBRing) * T + t]; };
 
   // ---- fill: rows of the problem's microbatches (staged order)
   const long long bb = prob / a.groups;
@@ -172,22 +165,6 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     }
   };
 
-  // forward values of a row by sample index (cold path)
-  auto fwd_row = [&](int idx, double* ef, double* gf) {
-    if (!direct_rows) {
-      const double4 r = ld_row(a.table.eg + TK(idx));
-      *ef = r.x;
-      *gf = r.z;
-    } else {
-      const long long v = a.span == 1 ? a.tok.get(bb, grp * l + idx, true)
-                                      : a.mbsum[prob * static_cast<long long>(l) + idx];
-      double key;
-      int e2 = 0;
-      const Row4 r = inter_row_direct(&a, v, &key, &e2);
-      *ef = r.ef;
-      *gf = r.gf;
-    }
-  };
   for (int i = 0; i < l; ++i) out[i] = i;
   if (l <= 1 || DEV == 1) return;
 
@@ -200,31 +177,22 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     pend[w] = lo >= l ? 0u : (l - lo >= 32 ? 0xffffffffu : ((1u << (l - lo)) - 1u));
   }
   int npend = l;
-  // the same set as an ascending list with lazy deletion: removed entries
-  // become holes (0xff) and the list is compacted every kCompact removals,
-  // so the hot loops run `plen` iterations in every lane (removals are
-  // uniform across the warp: one per step) instead of l predicated ones,
-  // and no lane shifts bytes on its own schedule
-  constexpr int kCompact = 8;
+  // the same set as a compacted ascending list: the hot O(npend) loops then
+  // run exactly npend iterations in every lane (npend is uniform across the
+  // warp) instead of l predicated ones
   unsigned char* PL = colPL + static_cast<size_t>(t) * pls;
   for (int q = 0; q < l; ++q) PL[q] = static_cast<unsigned char>(q);
-  int plen = l, holes = 0;
   auto list_remove = [&](int pos) {
-    PL[pos] = 0xff;
-    if (++holes == kCompact) {
-      int w = 0;
-      for (int q = 0; q < plen; ++q) {
-        const unsigned char v = PL[q];
-        const double f = F(q), g = G(q), k = K(q);
-        PL[w] = v;
-        F(w) = f;
-        G(w) = g;
-        K(w) = k;
-        w += v != 0xff;
-      }
-      plen = w;
-      holes = 0;
+    for (int q = pos; q + 1 < npend; ++q) PL[q] = PL[q + 1];
+  };
+  auto list_find = [&](int idx) -> int {  // position of idx (ascending list)
+    int lo = 0, hi = npend - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (PL[mid] < idx) lo = mid + 1;
+      else hi = mid;
     }
+    return lo;
   };
   auto pend_word = [&](int w) -> unsigned {
     unsigned r = 0u;
@@ -238,22 +206,23 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     for (int w = 0; w < MW; ++w)
       if (w == (idx >> 5)) pend[w] &= ~(1u << (idx & 31));
   };
-  // select_min, one pick: smallest (key, index) over the pending list;
-  // *pos gets its list position
-  auto pick_min = [&](int* pos) -> int {
-    int best = -1, bq = 0;
+  // select_min, one pick: smallest (key, index)
+  auto pick_min = [&]() -> int {
+    int best = -1;
     double kb = 0.0;
-    for (int q = 0; q < plen; ++q) {
-      const int raw = PL[q];
-      if (raw == 0xff) continue;
-      const double k = K(q);
-      if (best < 0 || k < kb) {
-        best = raw;
-        bq = q;
-        kb = k;
+#pragma unroll
+    for (int w = 0; w < MW; ++w) {
+      unsigned m = pend[w];
+      while (m) {
+        const int idx = w * 32 + __ffs(m) - 1;
+        m &= m - 1;
+        const double k = K(idx);
+        if (best < 0 || k < kb) {
+          best = idx;
+          kb = k;
+        }
       }
     }
-    *pos = bq;
     return best;
   };
   // select_closest, one pick: smallest (|r - key|, key > r, index) over the
@@ -264,14 +233,12 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     double db = 0.0;
     bool bover = false;
 #pragma unroll 4
-    for (int q = 0; q < plen; ++q) {
-      const int raw = PL[q];
-      const bool live = raw != 0xff;
-      const int idx = raw;
-      const double k = K(q);
+    for (int q = 0; q < npend; ++q) {
+      const int idx = PL[q];
+      const double k = K(idx);
       const double da = fabs(residual - k);
       const bool over = !(k <= residual);
-      const bool take = live && (best < 0 || da < db || (da == db && !over && bover));
+      const bool take = best < 0 || da < db || (da == db && !over && bover);
       best = take ? idx : best;
       bq = take ? q : bq;
       db = take ? da : db;
@@ -282,43 +249,29 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   };
 
   int nret = 0;
-  auto place = [&](int idx, int q) {
+  auto place = [&](int idx) {
     double eb, gb;
     bwd_row(idx, &eb, &gb);
     BE(nret) = eb;
     BG(nret) = gb;
-    FE(nret) = F(q);
-    FG(nret) = G(q);
     RET(nret++) = static_cast<unsigned char>(idx);
   };
-  int fpos;
-  const int first = pick_min(&fpos);
-  place(first, fpos);
+  const int first = pick_min();
+  place(first);
   clear(first);
-  list_remove(fpos);
+  list_remove(list_find(first));
   --npend;
   const int tail_n = min(DEV - 1, npend);
-  constexpr int NR = DEV > 1 ? DEV - 1 : 1;
-  int rear[NR];
-  double rearF[NR], rearG[NR];
+  int rear[DEV > 1 ? DEV - 1 : 1];
 #pragma unroll
-  for (int q = 0; q < NR; ++q) {
-    rear[q] = 0;
-    rearF[q] = rearG[q] = 0.0;
-  }
+  for (int q = 0; q < (DEV > 1 ? DEV - 1 : 1); ++q) rear[q] = 0;
   for (int q = 0; q < tail_n; ++q) {
-    int rpos;
-    const int r = pick_min(&rpos);
-    const double rf = F(rpos), rg = G(rpos);
+    const int r = pick_min();
 #pragma unroll
-    for (int z = 0; z < NR; ++z)
-      if (z == q) {
-        rear[z] = r;
-        rearF[z] = rf;
-        rearG[z] = rg;
-      }
+    for (int z = 0; z < (DEV > 1 ? DEV - 1 : 1); ++z)
+      if (z == q) rear[z] = r;
     clear(r);
-    list_remove(rpos);
+    list_remove(list_find(r));
     --npend;
   }
 
@@ -349,19 +302,12 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     }
     const bool enc = s < PE;
     if (r < np) {
-      if (r + kBRing >= nret) return enc ? FE(r) : FG(r);
-      // outside the ring (not reached by the 1F1B windows): from the table
-      double ef, gf;
-      fwd_row(RET(r), &ef, &gf);
-      return enc ? ef : gf;
+      const int row = RET(r);
+      return enc ? F(row) : G(row);
     }
     if (r < np + npend) return enc ? meanE : meanG;
-    const int q = r - np - npend;
-    double x = 0.0;
-#pragma unroll
-    for (int z = 0; z < NR; ++z)
-      if (z == q) x = enc ? rearF[z] : rearG[z];
-    return x;
+    const int row = rear_row(r - np - npend);
+    return enc ? F(row) : G(row);
   };
   auto candB = [&](int r, int s) -> double {
     if (r >= np && r < np + npend) {
@@ -440,13 +386,11 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     {
       // sequential over the ascending pending list (src/reorder.cpp:191-201)
       double sE = 0.0, sG = 0.0;
-      // holes add an exact +0.0 (no partial sum is -0.0: every term >= +0)
 #pragma unroll 4
-      for (int q = 0; q < plen; ++q) {
-        const bool live = PL[q] != 0xff;
-        const double f = F(q), g = G(q);
-        sE += live ? f : 0.0;
-        sG += live ? g : 0.0;
+      for (int q = 0; q < npend; ++q) {
+        const int idx = PL[q];
+        sE += F(idx);
+        sG += G(idx);
       }
       const double c = static_cast<double>(npend);
       meanE = sE / c;
@@ -478,8 +422,8 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     for (int q = 0; q < take; ++q) {
       int ppos;
       const int pick = pick_closest(residual, &ppos);
-      residual -= K(ppos);
-      place(pick, ppos);
+      residual -= K(pick);
+      place(pick);
       clear(pick);
       list_remove(ppos);
       --npend;
