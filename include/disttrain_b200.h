@@ -49,6 +49,7 @@ typedef enum dtb_status {
   DTB_ERR_EMPTY_PROFILE = 6,       /* EmptyProfileError    errors.hpp:28   */
   DTB_ERR_INFEASIBLE = 7,          /* InfeasibleError      errors.hpp:46   */
   DTB_ERR_CAP_EXCEEDED = 8,        /* CapExceededError     errors.hpp:64   */
+  DTB_ERR_TRACE = 9,               /* TraceError           errors.hpp:35   */
   DTB_ERR_INVALID_ARGUMENT = 100,  /* null pointer / ABI limit exceeded    */
   DTB_ERR_CUDA = 101               /* device failure (no reference analogue) */
 } dtb_status;
@@ -497,6 +498,51 @@ dtb_status dtb_brute_force_oracle(dtb_context* ctx, const dtb_cost_model* cm,
 dtb_status dtb_rigid_baseline(dtb_context* ctx, const dtb_cost_model* cm,
                               const dtb_workload_stats* stats, int64_t global_batch,
                               int32_t vpp, dtb_plan* plan);
+
+/* ------------------------------------------------------------ trace ingest
+ * ingest_trace (src/workload.cpp:115-153): JSONL records
+ * {"text_tokens": int, "image_subseqs": [int...], "audio_subseqs": [int...]}
+ * one per line -> the sample CSR of dtb_samples.  Same line splitting
+ * (std::getline), blank-line rule, JSON grammar (nlohmann 3.11.3, last
+ * duplicate key wins), int64 conversion and Sample::valid checks as the
+ * reference; a failure is DTB_ERR_TRACE with TraceError's kind() and line()
+ * in dtb_trace_result; the message is "<kind> at line <n>: <why>".  ABI limits
+ * (nesting deeper than 1024, token counts that do not fit int32, lines over
+ * 2^31 bytes) are DTB_ERR_INVALID_ARGUMENT with the line. */
+typedef struct dtb_trace_csr {
+  int64_t cap_samples;     /* text_tokens holds cap_samples, the offsets cap_samples + 1 */
+  int64_t cap_image;       /* image_tokens capacity */
+  int64_t cap_audio;       /* audio_tokens capacity */
+  int32_t* text_tokens;
+  int32_t* image_offsets;
+  int32_t* image_tokens;
+  int32_t* audio_offsets;
+  int32_t* audio_tokens;
+} dtb_trace_csr;
+
+enum { DTB_TRACE_NONE = 0, DTB_TRACE_PARSE_ERROR = 1, DTB_TRACE_INVARIANT_VIOLATION = 2 };
+
+typedef struct dtb_trace_result {
+  int64_t n_samples;       /* produced — or required, when a capacity is short */
+  int64_t n_image;
+  int64_t n_audio;
+  int64_t n_lines;         /* getline lines, blank ones included */
+  int32_t error_kind;      /* DTB_TRACE_*: TraceError::kind() */
+  int32_t error_line;      /* TraceError::line(), 1-based */
+  int32_t error_reason;    /* detail code (csrc/jsonl.cuh JReason) */
+  int32_t reserved;
+} dtb_trace_result;
+
+/* Host bytes -> host CSR.  out == NULL (or out->text_tokens == NULL): sizes
+ * only.  A short capacity returns DTB_ERR_INVALID_ARGUMENT with the required
+ * sizes in res. */
+dtb_status dtb_ingest_trace(dtb_context* ctx, const char* bytes, int64_t len,
+                            int64_t seq_len_cap, const dtb_trace_csr* out,
+                            dtb_trace_result* res);
+/* Device bytes -> device CSR (all pointers device pointers; ctx stream). */
+dtb_status dtb_ingest_trace_dev(dtb_context* ctx, const char* bytes, int64_t len,
+                                int64_t seq_len_cap, const dtb_trace_csr* out,
+                                dtb_trace_result* res);
 
 /* One shard of the search for multi-GPU runs: evaluates the tuples whose
  * sorted index i satisfies i % shard_count == shard_index and writes the

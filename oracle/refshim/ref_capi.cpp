@@ -15,6 +15,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -819,6 +820,64 @@ dtb_status API(model_orchestration_mt)(dtb_context*, const dtb_cost_model* cm,
                                 std::chrono::steady_clock::now() - t0)
                                 .count();
   });
+}
+
+// ingest_trace (src/workload.cpp:115-153) over an istringstream of the
+// bytes; CSR marshalling only.
+dtb_status API(ingest_trace)(dtb_context*, const char* bytes, int64_t len, int64_t seq_len_cap,
+                             const dtb_trace_csr* out, dtb_trace_result* res) {
+  *res = dtb_trace_result{};
+  std::string text(bytes ? bytes : "", static_cast<size_t>(len));
+  {
+    std::istringstream lines(text);
+    std::string line;
+    while (std::getline(lines, line)) ++res->n_lines;
+  }
+  std::vector<Sample> samples;
+  try {
+    std::istringstream in(text);
+    samples = ingest_trace(in, seq_len_cap);
+  } catch (const TraceError& e) {
+    res->error_kind = e.kind() == "ParseError" ? DTB_TRACE_PARSE_ERROR
+                                               : DTB_TRACE_INVARIANT_VIOLATION;
+    res->error_line = e.line();
+    return fail(DTB_ERR_TRACE, e.what());
+  } catch (const std::exception& e) {
+    return fail(DTB_ERR_INTERNAL, e.what());
+  }
+  int64_t ni = 0, na = 0;
+  for (const Sample& smp : samples) {
+    ni += static_cast<int64_t>(smp.image_subseqs.size());
+    na += static_cast<int64_t>(smp.audio_subseqs.size());
+  }
+  res->n_samples = static_cast<int64_t>(samples.size());
+  res->n_image = ni;
+  res->n_audio = na;
+  for (size_t k = 0; k < samples.size(); ++k) {
+    const Sample& smp = samples[k];
+    bool big = smp.text_tokens > 0x7fffffff;
+    for (auto v : smp.image_subseqs) big |= v > 0x7fffffff;
+    for (auto v : smp.audio_subseqs) big |= v > 0x7fffffff;
+    if (big) {
+      res->error_line = 0;
+      return fail(DTB_ERR_INVALID_ARGUMENT, "token count beyond the int32 CSR");
+    }
+  }
+  if (out == nullptr || out->text_tokens == nullptr) return DTB_OK;
+  if (res->n_samples > out->cap_samples || ni > out->cap_image || na > out->cap_audio)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "CSR capacity too small");
+  int64_t oi = 0, oa = 0;
+  for (size_t k = 0; k < samples.size(); ++k) {
+    const Sample& smp = samples[k];
+    out->text_tokens[k] = static_cast<int32_t>(smp.text_tokens);
+    out->image_offsets[k] = static_cast<int32_t>(oi);
+    out->audio_offsets[k] = static_cast<int32_t>(oa);
+    for (auto v : smp.image_subseqs) out->image_tokens[oi++] = static_cast<int32_t>(v);
+    for (auto v : smp.audio_subseqs) out->audio_tokens[oa++] = static_cast<int32_t>(v);
+  }
+  out->image_offsets[samples.size()] = static_cast<int32_t>(oi);
+  out->audio_offsets[samples.size()] = static_cast<int32_t>(oa);
+  return DTB_OK;
 }
 
 }  // extern "C"

@@ -108,6 +108,19 @@ class MemoryReport(C.Structure):
                 ("pass_", c_i32), ("capacity_bytes", c_f64)]
 
 
+class TraceCsr(C.Structure):
+    _fields_ = [("cap_samples", C.c_int64), ("cap_image", C.c_int64), ("cap_audio", C.c_int64),
+                ("text_tokens", C.c_void_p), ("image_offsets", C.c_void_p),
+                ("image_tokens", C.c_void_p), ("audio_offsets", C.c_void_p),
+                ("audio_tokens", C.c_void_p)]
+
+
+class TraceResult(C.Structure):
+    _fields_ = [("n_samples", C.c_int64), ("n_image", C.c_int64), ("n_audio", C.c_int64),
+                ("n_lines", C.c_int64), ("error_kind", C.c_int32), ("error_line", C.c_int32),
+                ("error_reason", C.c_int32), ("reserved", C.c_int32)]
+
+
 class ReorderReport(C.Structure):
     _fields_ = [("output_order", P(c_i32)), ("group_load_before", P(c_f64)),
                 ("group_load_after", P(c_f64)), ("t_iter_before", c_f64),
@@ -182,6 +195,8 @@ _SIGS = {
     "brute_force_oracle": (c_i32, [VP, VP, P(WorkloadStats), c_i64, c_i32, c_i32,
                                    P(OrchestrationResult)]),
     "rigid_baseline": (c_i32, [VP, VP, P(WorkloadStats), c_i64, c_i32, P(Plan)]),
+    "ingest_trace": (c_i32, [VP, C.c_char_p, c_i64, c_i64, P(TraceCsr), P(TraceResult)]),
+    "ingest_trace_dev": (c_i32, [VP, VP, c_i64, c_i64, P(TraceCsr), P(TraceResult)]),
     "model_orchestration": (c_i32, [VP, VP, P(WorkloadStats), c_i64, c_i32,
                                     P(OrchestrationResult), P(Candidate),
                                     c_i64]),
@@ -201,7 +216,7 @@ _SIGS = {
 STATUS_NAMES = {
     0: "OK", 1: "InternalError", 2: "KTooLargeError", 3: "IndivisibleVppError",
     4: "BatchSizeMismatchError", 5: "ConfigError", 6: "EmptyProfileError",
-    7: "InfeasibleError", 8: "CapExceededError", 100: "InvalidArgument",
+    7: "InfeasibleError", 8: "CapExceededError", 9: "TraceError", 100: "InvalidArgument",
     101: "CudaError",
 }
 

@@ -66,13 +66,29 @@ class InvalidArgument(MmplanError):
     pass
 
 
+class TraceError(ConfigError):
+    """TraceError (errors.hpp:35-47): kind() "ParseError" or
+    "InvariantViolation" and the 1-based line()."""
+
+    def __init__(self, msg, kind="", line=0):
+        super().__init__(msg)
+        self._kind = kind
+        self._line = line
+
+    def kind(self):
+        return self._kind
+
+    def line(self):
+        return self._line
+
+
 class CudaError(MmplanError):
     pass
 
 
 _ERRORS = {1: InternalError, 2: KTooLargeError, 3: IndivisibleVppError,
            4: BatchSizeMismatchError, 5: ConfigError, 6: EmptyProfileError,
-           7: InfeasibleError, 8: CapExceededError, 100: InvalidArgument,
+           7: InfeasibleError, 8: CapExceededError, 9: TraceError, 100: InvalidArgument,
            101: CudaError}
 
 REASON_TEXT = {
@@ -681,6 +697,33 @@ class Planner:
         return dict(best=PlanSpec.from_c(res.best),
                     times=(res.times.t_warm, res.times.t_steady, res.times.t_iter),
                     candidates_evaluated=res.candidates_evaluated)
+
+    def ingest_trace(self, data: bytes, seq_len_cap: int) -> "SampleBatch":
+        """ingest_trace (src/workload.cpp:115-153): JSONL bytes -> SampleBatch.
+        Raises TraceError with kind()/line() like the reference."""
+        res = A.TraceResult()
+        st = self.lib.ingest_trace(self.ctx, data, len(data), seq_len_cap, None, C.byref(res))
+        self._trace_check(st, res)
+        n, ni, na = res.n_samples, res.n_image, res.n_audio
+        out = SampleBatch(np.zeros(n, np.int32), np.zeros(n + 1, np.int32),
+                          np.zeros(max(ni, 1), np.int32), np.zeros(n + 1, np.int32),
+                          np.zeros(max(na, 1), np.int32))
+        csr = A.TraceCsr(n, ni, na, out.text.ctypes.data, out.image_offsets.ctypes.data,
+                         out.image_tokens.ctypes.data, out.audio_offsets.ctypes.data,
+                         out.audio_tokens.ctypes.data)
+        st = self.lib.ingest_trace(self.ctx, data, len(data), seq_len_cap, C.byref(csr),
+                                   C.byref(res))
+        self._trace_check(st, res)
+        out.image_tokens = out.image_tokens[:ni]
+        out.audio_tokens = out.audio_tokens[:na]
+        return out
+
+    def _trace_check(self, status, res):
+        if status == 9:
+            msg = self.lib.last_error().decode(errors="replace")
+            kind = "ParseError" if res.error_kind == 1 else "InvariantViolation"
+            raise TraceError(msg, kind, res.error_line)
+        self._check(status)
 
     def rigid_baseline(self, cm, stats, global_batch, vpp=1):
         """rigid_baseline (src/orchestrator.cpp:407-431)."""

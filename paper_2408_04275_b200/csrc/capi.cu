@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "jsonl.cuh"
 #include "kernels.cuh"
 
 using namespace dtb;
@@ -1590,6 +1591,172 @@ dtb_status dtb_best_reduce_dev(dtb_context* ctx, const dtb_candidate* records, i
                                dtb_candidate* best_dev, void* stream) {
   TRY(set_device(ctx));
   CU(launch_best_reduce(records, n, best_dev, static_cast<cudaStream_t>(stream)));
+  return DTB_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ trace ingest
+namespace {
+
+const char* trace_why(int reason) {
+  switch (reason) {
+    case JR_SYNTAX: return "syntax error while parsing value";
+    case JR_NUMBER_OVERFLOW: return "number overflow";
+    case JR_NOT_RECORD: return "record must be an object with text_tokens";
+    case JR_TEXT_TYPE: return "text_tokens: type must be number";
+    case JR_IMAGE_TYPE: return "image_subseqs: type must be an array of numbers";
+    case JR_AUDIO_TYPE: return "audio_subseqs: type must be an array of numbers";
+    case JR_NEG_TEXT: return "negative text token count";          // src/core.cpp:102
+    case JR_NEG_SUBSEQ: return "negative subsequence token count"; // src/core.cpp:105
+    case JR_NO_TOKENS: return "sample has no tokens";              // src/core.cpp:108
+    case JR_OVER_CAP: return "sample exceeds the sequence length cap";  // src/core.cpp:110
+    case JR_TOO_DEEP: return "nesting deeper than 1024 levels";
+    case JR_INT32: return "token count or line length beyond the int32 CSR";
+    default: return "unknown";
+  }
+}
+
+// Parses the device byte buffer; on success leaves the CSR in device
+// buffers `o` (allocated here when dev_out is null) and the sizes in res.
+dtb_status ingest_impl(dtb_context* ctx, const unsigned char* b, long long len, long long cap,
+                       const dtb_trace_csr* dev_out, dtb_trace_result* res, DBuf* own) {
+  cudaStream_t s = ctx->stream;
+  *res = dtb_trace_result{};
+  DBuf scratch, nl, st, tx, ia, aa, cn, sc, bad;
+  const size_t sb = ingest_lines_scratch(len);
+  CU(scratch.alloc(sb, s));
+  long long n_nl = 0;
+  CU(launch_nl_count(b, len, scratch.p, sb, &n_nl, s));
+  long long n_lines = n_nl;
+  if (len > 0) {
+    unsigned char last = 0;
+    CU(cudaMemcpyAsync(&last, b + len - 1, 1, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (last != '\n') ++n_lines;
+  }
+  res->n_lines = n_lines;
+  CU(nl.alloc(8ull * (n_nl > 0 ? n_nl : 1), s));
+  if (n_nl > 0) CU(launch_nl_write(b, len, scratch.p, nl.as<long long>(), s));
+  const size_t nL = static_cast<size_t>(n_lines);
+  CU(st.alloc(4 * nL, s));
+  CU(tx.alloc(8 * nL, s));
+  CU(ia.alloc(4 * nL, s));
+  CU(aa.alloc(4 * nL, s));
+  CU(cn.alloc(12 * (nL + 1), s));
+  CU(sc.alloc(12 * (nL + 1), s));
+  CU(bad.alloc(8, s));
+  CU(cudaMemsetAsync(bad.p, 0xff, 8, s));
+  IngestLines L{st.as<int>(), tx.as<long long>(), ia.as<int>(), aa.as<int>(), cn.as<int>(),
+                sc.as<int>()};
+  CU(launch_ingest_parse(b, len, nl.as<long long>(), n_nl, n_lines, cap, L,
+                         bad.as<unsigned long long>(), scratch.p, sb, s));
+  unsigned long long first_bad = 0;
+  int tot[3] = {0, 0, 0};
+  CU(cudaMemcpyAsync(&first_bad, bad.p, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(tot, sc.as<int>() + 3 * nL, 12, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (first_bad != ~0ull) {
+    int code = 0;
+    CU(cudaMemcpyAsync(&code, st.as<int>() + first_bad, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const int status = code & 0xff, reason = code >> 8;
+    const int line = static_cast<int>(first_bad + 1);
+    res->error_line = line;
+    res->error_reason = reason;
+    if (status == J_UNSUPPORTED)
+      return fail(DTB_ERR_INVALID_ARGUMENT, "line %d: %s", line, trace_why(reason));
+    const bool parse = status == J_PARSE;
+    res->error_kind = parse ? DTB_TRACE_PARSE_ERROR : DTB_TRACE_INVARIANT_VIOLATION;
+    return fail(DTB_ERR_TRACE, "%s at line %d: %s", parse ? "ParseError" : "InvariantViolation",
+                line, trace_why(reason));
+  }
+  res->n_samples = tot[0];
+  res->n_image = tot[1];
+  res->n_audio = tot[2];
+  if (dev_out == nullptr) return DTB_OK;
+  IngestOut o{};
+  if (own != nullptr) {  // library-owned device CSR (host entry point)
+    CU(own[0].alloc(4ull * tot[0], s));
+    CU(own[1].alloc(4ull * (tot[0] + 1), s));
+    CU(own[2].alloc(4ull * tot[1], s));
+    CU(own[3].alloc(4ull * (tot[0] + 1), s));
+    CU(own[4].alloc(4ull * tot[2], s));
+    o = IngestOut{own[0].as<int>(), own[1].as<int>(), own[2].as<int>(), own[3].as<int>(),
+                  own[4].as<int>()};
+  } else {
+    o = IngestOut{dev_out->text_tokens, dev_out->image_offsets, dev_out->image_tokens,
+                  dev_out->audio_offsets, dev_out->audio_tokens};
+  }
+  CU(launch_ingest_write(b, len, nl.as<long long>(), n_nl, n_lines, L, o, s));
+  return DTB_OK;
+}
+
+dtb_status trace_args(dtb_context* ctx, const char* bytes, int64_t len, int64_t cap,
+                      const dtb_trace_csr* out, dtb_trace_result* res, bool* write) {
+  TRY(set_device(ctx));
+  if (res == nullptr || (bytes == nullptr && len > 0) || len < 0)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "null result / byte buffer");
+  *write = out != nullptr && out->text_tokens != nullptr;
+  if (*write && (out->image_offsets == nullptr || out->audio_offsets == nullptr))
+    return fail(DTB_ERR_INVALID_ARGUMENT, "null CSR offsets");
+  (void)cap;
+  return DTB_OK;
+}
+
+dtb_status trace_capacity(const dtb_trace_csr* out, const dtb_trace_result* res) {
+  if (res->n_samples > out->cap_samples || res->n_image > out->cap_image ||
+      res->n_audio > out->cap_audio)
+    return fail(DTB_ERR_INVALID_ARGUMENT,
+                "CSR capacity too small: need %lld samples, %lld image, %lld audio subsequences",
+                static_cast<long long>(res->n_samples), static_cast<long long>(res->n_image),
+                static_cast<long long>(res->n_audio));
+  if ((res->n_image > 0 && out->image_tokens == nullptr) ||
+      (res->n_audio > 0 && out->audio_tokens == nullptr))
+    return fail(DTB_ERR_INVALID_ARGUMENT, "null CSR token buffer");
+  return DTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dtb_status dtb_ingest_trace_dev(dtb_context* ctx, const char* bytes, int64_t len,
+                                int64_t seq_len_cap, const dtb_trace_csr* out,
+                                dtb_trace_result* res) {
+  bool write = false;
+  TRY(trace_args(ctx, bytes, len, seq_len_cap, out, res, &write));
+  // sizes first, then the write into the caller's buffers
+  TRY(ingest_impl(ctx, reinterpret_cast<const unsigned char*>(bytes), len, seq_len_cap, nullptr,
+                  res, nullptr));
+  if (!write) return DTB_OK;
+  TRY(trace_capacity(out, res));
+  TRY(ingest_impl(ctx, reinterpret_cast<const unsigned char*>(bytes), len, seq_len_cap, out, res,
+                  nullptr));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return DTB_OK;
+}
+
+dtb_status dtb_ingest_trace(dtb_context* ctx, const char* bytes, int64_t len,
+                            int64_t seq_len_cap, const dtb_trace_csr* out,
+                            dtb_trace_result* res) {
+  bool write = false;
+  TRY(trace_args(ctx, bytes, len, seq_len_cap, out, res, &write));
+  DBuf db;
+  TRY(upload(db, reinterpret_cast<const unsigned char*>(bytes), static_cast<size_t>(len),
+             ctx->stream));
+  DBuf own[5];
+  dtb_trace_csr dummy{};
+  TRY(ingest_impl(ctx, db.as<unsigned char>(), len, seq_len_cap, write ? &dummy : nullptr, res,
+                  own));
+  if (!write) return DTB_OK;
+  TRY(trace_capacity(out, res));
+  TRY(download(out->text_tokens, own[0], static_cast<size_t>(res->n_samples), ctx->stream));
+  TRY(download(out->image_offsets, own[1], static_cast<size_t>(res->n_samples + 1), ctx->stream));
+  TRY(download(out->image_tokens, own[2], static_cast<size_t>(res->n_image), ctx->stream));
+  TRY(download(out->audio_offsets, own[3], static_cast<size_t>(res->n_samples + 1), ctx->stream));
+  TRY(download(out->audio_tokens, own[4], static_cast<size_t>(res->n_audio), ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
   return DTB_OK;
 }
 

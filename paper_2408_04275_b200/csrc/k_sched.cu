@@ -575,8 +575,10 @@ group_sims_fast(GroupSimArgs a) {
 // reference's operands.  All durations are >= 0 and never NaN (profile times
 // are validated strictly positive, src/cost_model.cpp:37-47; analytic and
 // comm terms are non-negative), so the per-device end times are
-// non-decreasing and (i) std::max == fmax on them, (ii) the iteration time
-// max over all events == max over the devices' last ends.
+// non-decreasing and the iteration time (max over all events) == max over
+// the devices' last ends.  max is smax (std::max's compare + select: one
+// DSETP and two FSEL) — fmax lowers to DSETP.MAX + SEL + FSEL + a NaN-quieting
+// LOP3 and extra moves on sm_100.
 constexpr int kSimT = 128;
 constexpr int kSimChunk = 4;
 
@@ -654,7 +656,7 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
       if (!check || (mb >= 0 && mb < l)) {
         const double x = dur(s, fwd, d);
         const double dep = fwd ? (s > 0 ? pv[s - 1] : 0.0) : (s + 1 < P ? pv[s + 1] : pv[s]);
-        const double start = (s == 0 && fwd) || (s == P - 1 && !fwd) ? av[s] : fmax(av[s], dep);
+        const double start = (s == 0 && fwd) || (s == P - 1 && !fwd) ? av[s] : smax(av[s], dep);
         av[s] = start + x;
         if (BUSY) busy[s] += x;
       }
@@ -670,7 +672,7 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
       if (!check || (mb >= 0 && mb < l)) {
         const double x = dur(s, fwd, d);
         const double dep = fwd ? pv[s - 1] : (s + 1 < P ? pv[s + 1] : pv[s]);
-        const double start = (s == P - 1 && !fwd) ? av[s] : fmax(av[s], dep);
+        const double start = (s == P - 1 && !fwd) ? av[s] : smax(av[s], dep);
         av[s] = start + x;
         if (BUSY) busy[s] += x;
       }
@@ -710,34 +712,53 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
     // cost-table rows are all in flight before its first tick; its token
     // sums were loaded two chunks ahead (vector loads when possible).
     const bool vec = ord == nullptr && (P % 4) == 0 && (l % 4) == 0;
-    auto tokens = [&](int i0, int* tk) {
+    // token sums of a chunk are fetched raw (vector registers) and unpacked
+    // only when the chunk's rows are addressed one chunk later, so the load
+    // latency is covered by a chunk of ticks
+    constexpr int NV = P / 4 > 0 ? P / 4 : 1;
+    uint2 rv16[NV];
+    int4 rv32[NV];
+    int tk[P] = {}, tk_next[P] = {};
+    auto fetch = [&](int i0) {
       if (i0 >= l) return;
 #if DTB_SIM_EXPERIMENT == 2
 #pragma unroll
-      for (int j = 0; j < P; ++j) tk[j] = (i0 + j) & 1023;
+      for (int j = 0; j < P; ++j) tk_next[j] = (i0 + j) & 1023;
       return;
 #endif
       if (vec) {
 #pragma unroll
-        for (int j = 0; j < P; j += 4) {
-          if (t16) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(t16 + i0 + j));
-            tk[j] = v.x & 0xffff;
-            tk[j + 1] = v.x >> 16;
-            tk[j + 2] = v.y & 0xffff;
-            tk[j + 3] = v.y >> 16;
-          } else {
-            const int4 v = __ldg(reinterpret_cast<const int4*>(t32 + i0 + j));
-            tk[j] = v.x;
-            tk[j + 1] = v.y;
-            tk[j + 2] = v.z;
-            tk[j + 3] = v.w;
-          }
+        for (int v = 0; v < NV; ++v) {
+          if (t16) rv16[v] = __ldg(reinterpret_cast<const uint2*>(t16 + i0 + 4 * v));
+          else rv32[v] = __ldg(reinterpret_cast<const int4*>(t32 + i0 + 4 * v));
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < P; ++j) tk[j] = i0 + j < l ? token(i0 + j) : 0;
+        for (int j = 0; j < P; ++j) tk_next[j] = i0 + j < l ? token(i0 + j) : 0;
       }
+    };
+    auto promote = [&]() {
+#if DTB_SIM_EXPERIMENT != 2
+      if (vec) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          if (t16) {
+            tk[4 * v] = rv16[v].x & 0xffff;
+            tk[4 * v + 1] = rv16[v].x >> 16;
+            tk[4 * v + 2] = rv16[v].y & 0xffff;
+            tk[4 * v + 3] = rv16[v].y >> 16;
+          } else {
+            tk[4 * v] = rv32[v].x;
+            tk[4 * v + 1] = rv32[v].y;
+            tk[4 * v + 2] = rv32[v].z;
+            tk[4 * v + 3] = rv32[v].w;
+          }
+        }
+        return;
+      }
+#endif
+#pragma unroll
+      for (int j = 0; j < P; ++j) tk[j] = tk_next[j];
     };
     auto tick_ring = [&](int i, bool check, const double4* cur, const double4* prev, int j) {
       // j is a compile-time constant at every call site (fully unrolled)
@@ -757,7 +778,7 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
         if (!check || (mb >= 0 && mb < l)) {
           const double x = du(s, fwd, d);
           const double dep = fwd ? (s > 0 ? pv[s - 1] : 0.0) : (s + 1 < P ? pv[s + 1] : pv[s]);
-          const double start = (s == 0 && fwd) || (s == P - 1 && !fwd) ? av[s] : fmax(av[s], dep);
+          const double start = (s == 0 && fwd) || (s == P - 1 && !fwd) ? av[s] : smax(av[s], dep);
           av[s] = start + x;
           if (BUSY) busy[s] += x;
         }
@@ -772,7 +793,7 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
         if (!check || (mb >= 0 && mb < l)) {
           const double x = du(s, fwd, d);
           const double dep = fwd ? pv[s - 1] : (s + 1 < P ? pv[s + 1] : pv[s]);
-          const double start = (s == P - 1 && !fwd) ? av[s] : fmax(av[s], dep);
+          const double start = (s == P - 1 && !fwd) ? av[s] : smax(av[s], dep);
           av[s] = start + x;
           if (BUSY) busy[s] += x;
         }
@@ -792,13 +813,9 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
     double4 rA[P], rB[P], nxt[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) rA[j] = rB[j] = make_double4(0.0, 0.0, 0.0, 0.0);
-    // token sums run one chunk ahead of the rows they address
-    int tk[P] = {}, tk_next[P] = {};
-    tokens(0, tk_next);
     auto load_rows = [&](int i0) {
-#pragma unroll
-      for (int j = 0; j < P; ++j) tk[j] = tk_next[j];
-      tokens(i0 + P, tk_next);
+      promote();
+      fetch(i0 + P);
 #pragma unroll
       for (int j = 0; j < P; ++j)
         if (i0 + j < l) {
@@ -810,6 +827,7 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
 #endif
         }
     };
+    fetch(0);
     load_rows(0);
     for (int i0 = 0; i0 < l + P - 1; i0 += 2 * P) {
 #pragma unroll
@@ -824,7 +842,7 @@ __device__ __forceinline__ void sim_group(const GroupSimArgs& a, long long gid) 
   }
   double iter = 0.0;
 #pragma unroll
-  for (int s = 0; s < P; ++s) iter = fmax(iter, av[s]);
+  for (int s = 0; s < P; ++s) iter = smax(iter, av[s]);
   if (a.busy) {
     double bub = 0.0;
     if (iter > 0.0) {

@@ -276,4 +276,36 @@ cudaError_t launch_t_iter_reduce(long long n_batches, int groups,
                                  const double* t_group, double dp_sync,
                                  double* t_iter, cudaStream_t stream);
 
+// ---------------------------------------------------------------- ingest
+// Trace JSONL -> sample CSR (csrc/k_ingest.cu, parser csrc/jsonl.cuh).
+struct IngestLines {     // per line, n_lines (+1 for counts / scan)
+  int* status;           // JStatus | JReason << 8
+  long long* text;
+  int* img_at;
+  int* aud_at;
+  int* counts;           // (sample, image, audio) per line, 3 ints, n_lines + 1
+  int* scan;             // exclusive scan of counts, 3 ints, n_lines + 1
+};
+struct IngestOut {
+  int* text_tokens;
+  int* image_offsets;
+  int* image_tokens;
+  int* audio_offsets;
+  int* audio_tokens;
+};
+size_t ingest_lines_scratch(long long len);
+// newline count (synchronises the stream), then positions in byte order;
+// the write reuses the count's scratch
+cudaError_t launch_nl_count(const unsigned char* bytes, long long len, void* scratch,
+                            size_t scratch_bytes, long long* n_nl, cudaStream_t stream);
+cudaError_t launch_nl_write(const unsigned char* bytes, long long len, void* scratch,
+                            long long* nl, cudaStream_t stream);
+cudaError_t launch_ingest_parse(const unsigned char* bytes, long long len, const long long* nl,
+                                long long n_nl, long long n_lines, long long seq_len_cap,
+                                const IngestLines& lines, unsigned long long* first_bad,
+                                void* scratch, size_t scratch_bytes, cudaStream_t stream);
+cudaError_t launch_ingest_write(const unsigned char* bytes, long long len, const long long* nl,
+                                long long n_nl, long long n_lines, const IngestLines& lines,
+                                const IngestOut& out, cudaStream_t stream);
+
 }  // namespace dtb

@@ -36,12 +36,16 @@ def test_oracles_export_the_same_abi(ref, port):
     names = [s[len("dtb_"):] for s in declared_symbols()]
     device_only = {"schedule_batch_dev", "inter_reorder_batch_dev", "reorder_stream_dev",
                    "orchestration_shard_dev", "best_reduce_dev", "infeasible_reason_text",
-                   "intra_stream_dev"}
+                   "intra_stream_dev", "ingest_trace_dev"}
+    # trace ingest is pinned by the compiled reference and nlohmann itself
+    # (tests/test_ingest.py); the C port does not restate a JSON library
+    ref_only = {"ingest_trace"}
     for name in names:
         if name in device_only:
             continue
         assert ref.lib.has(name), "mmref_" + name
-        assert port.lib.has(name), "mmport_" + name
+        if name not in ref_only:
+            assert port.lib.has(name), "mmport_" + name
 
 
 def test_product_path_fails_loudly_without_the_library(tmp_path, monkeypatch):
