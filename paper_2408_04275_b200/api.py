@@ -718,6 +718,22 @@ class Planner:
         out.audio_tokens = out.audio_tokens[:na]
         return out
 
+    def ingest_trace_dev(self, data_ptr: int, length: int, seq_len_cap: int, out=None):
+        """dtb_ingest_trace_dev: device bytes -> device CSR.  out: None (sizes
+        only) or dict(cap_samples, cap_image, cap_audio, text_tokens,
+        image_offsets, image_tokens, audio_offsets, audio_tokens) of device
+        pointers.  Returns the TraceResult."""
+        res = A.TraceResult()
+        csr = None
+        if out is not None:
+            csr = A.TraceCsr(out["cap_samples"], out["cap_image"], out["cap_audio"],
+                             out["text_tokens"], out["image_offsets"], out["image_tokens"],
+                             out["audio_offsets"], out["audio_tokens"])
+        st = self.lib.ingest_trace_dev(self.ctx, data_ptr, length, seq_len_cap,
+                                       C.byref(csr) if csr is not None else None, C.byref(res))
+        self._trace_check(st, res)
+        return res
+
     def _trace_check(self, status, res):
         if status == 9:
             msg = self.lib.last_error().decode(errors="replace")

@@ -1617,6 +1617,19 @@ const char* trace_why(int reason) {
   }
 }
 
+dtb_status trace_capacity(const dtb_trace_csr* out, const dtb_trace_result* res) {
+  if (res->n_samples > out->cap_samples || res->n_image > out->cap_image ||
+      res->n_audio > out->cap_audio)
+    return fail(DTB_ERR_INVALID_ARGUMENT,
+                "CSR capacity too small: need %lld samples, %lld image, %lld audio subsequences",
+                static_cast<long long>(res->n_samples), static_cast<long long>(res->n_image),
+                static_cast<long long>(res->n_audio));
+  if ((res->n_image > 0 && out->image_tokens == nullptr) ||
+      (res->n_audio > 0 && out->audio_tokens == nullptr))
+    return fail(DTB_ERR_INVALID_ARGUMENT, "null CSR token buffer");
+  return DTB_OK;
+}
+
 // Parses the device byte buffer; on success leaves the CSR in device
 // buffers `o` (allocated here when dev_out is null) and the sizes in res.
 dtb_status ingest_impl(dtb_context* ctx, const unsigned char* b, long long len, long long cap,
@@ -1660,7 +1673,7 @@ dtb_status ingest_impl(dtb_context* ctx, const unsigned char* b, long long len, 
     int code = 0;
     CU(cudaMemcpyAsync(&code, st.as<int>() + first_bad, 4, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
-    const int status = code & 0xff, reason = code >> 8;
+    const int status = code & 0xff, reason = (code >> 8) & 0xff;
     const int line = static_cast<int>(first_bad + 1);
     res->error_line = line;
     res->error_reason = reason;
@@ -1675,6 +1688,7 @@ dtb_status ingest_impl(dtb_context* ctx, const unsigned char* b, long long len, 
   res->n_image = tot[1];
   res->n_audio = tot[2];
   if (dev_out == nullptr) return DTB_OK;
+  if (own == nullptr) TRY(trace_capacity(dev_out, res));
   IngestOut o{};
   if (own != nullptr) {  // library-owned device CSR (host entry point)
     CU(own[0].alloc(4ull * tot[0], s));
@@ -1704,19 +1718,6 @@ dtb_status trace_args(dtb_context* ctx, const char* bytes, int64_t len, int64_t 
   return DTB_OK;
 }
 
-dtb_status trace_capacity(const dtb_trace_csr* out, const dtb_trace_result* res) {
-  if (res->n_samples > out->cap_samples || res->n_image > out->cap_image ||
-      res->n_audio > out->cap_audio)
-    return fail(DTB_ERR_INVALID_ARGUMENT,
-                "CSR capacity too small: need %lld samples, %lld image, %lld audio subsequences",
-                static_cast<long long>(res->n_samples), static_cast<long long>(res->n_image),
-                static_cast<long long>(res->n_audio));
-  if ((res->n_image > 0 && out->image_tokens == nullptr) ||
-      (res->n_audio > 0 && out->audio_tokens == nullptr))
-    return fail(DTB_ERR_INVALID_ARGUMENT, "null CSR token buffer");
-  return DTB_OK;
-}
-
 }  // namespace
 
 extern "C" {
@@ -1726,13 +1727,8 @@ dtb_status dtb_ingest_trace_dev(dtb_context* ctx, const char* bytes, int64_t len
                                 dtb_trace_result* res) {
   bool write = false;
   TRY(trace_args(ctx, bytes, len, seq_len_cap, out, res, &write));
-  // sizes first, then the write into the caller's buffers
-  TRY(ingest_impl(ctx, reinterpret_cast<const unsigned char*>(bytes), len, seq_len_cap, nullptr,
-                  res, nullptr));
-  if (!write) return DTB_OK;
-  TRY(trace_capacity(out, res));
-  TRY(ingest_impl(ctx, reinterpret_cast<const unsigned char*>(bytes), len, seq_len_cap, out, res,
-                  nullptr));
+  TRY(ingest_impl(ctx, reinterpret_cast<const unsigned char*>(bytes), len, seq_len_cap,
+                  write ? out : nullptr, res, nullptr));
   CU(cudaStreamSynchronize(ctx->stream));
   return DTB_OK;
 }

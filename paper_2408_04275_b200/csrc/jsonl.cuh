@@ -493,6 +493,126 @@ DTB_HD inline JLine j_parse_line(const B& at, int len, long long seq_len_cap) {
   return r;
 }
 
+// Fast path for the canonical record layout write_trace produces
+// (src/workload.cpp:157-165, nlohmann dump: no whitespace, keys in order):
+//   {"text_tokens":N[,"image_subseqs":[N,...]][,"audio_subseqs":[N,...]]}
+// with N = 0 | [1-9][0-9]{0,8}.  On such a line the general parser's result
+// is exactly: text = N, the arrays' values, no duplicate keys, nothing else
+// to validate but the token total (no int64 wrap: every N < 1e9).  Any other
+// byte sequence returns false and the caller runs j_parse_line.
+template <class B>
+DTB_HD inline bool j_fast_uint(const B& at, int* p, long long* v) {
+  int c = at(*p);
+  if (c < '0' || c > '9') return false;
+  long long x = c - '0';
+  ++*p;
+  if (x == 0) {
+    c = at(*p);
+    if (c >= '0' && c <= '9') return false;
+    *v = 0;
+    return true;
+  }
+  for (int k = 1;; ++k) {
+    c = at(*p);
+    if (c < '0' || c > '9') break;
+    if (k == 9) return false;
+    x = x * 10 + (c - '0');
+    ++*p;
+  }
+  *v = x;
+  return true;
+}
+
+template <class B>
+DTB_HD inline bool j_fast_lit(const B& at, int* p, const char* lit) {
+  for (int k = 0; lit[k]; ++k)
+    if (at(*p + k) != static_cast<unsigned char>(lit[k])) return false;
+  while (lit[0]) {
+    ++lit;
+    ++*p;
+  }
+  return true;
+}
+
+template <class B>
+DTB_HD inline bool j_fast_list(const B& at, int* p, int* cnt, long long* sum) {
+  if (at(*p) == ']') {
+    ++*p;
+    return true;
+  }
+  for (;;) {
+    long long v;
+    if (!j_fast_uint(at, p, &v)) return false;
+    ++*cnt;
+    *sum += v;
+    const int c = at(*p);
+    ++*p;
+    if (c == ']') return true;
+    if (c != ',') return false;
+  }
+}
+
+template <class B>
+DTB_HD inline bool j_fast_line(const B& at, int len, long long seq_len_cap, JLine* r) {
+  int p = 0;
+  if (!j_fast_lit(at, &p, "{\"text_tokens\":")) return false;
+  long long text, sum = 0;
+  if (!j_fast_uint(at, &p, &text)) return false;
+  int n_img = 0, n_aud = 0, img_at = -1, aud_at = -1;
+  if (at(p) == ',' && at(p + 2) == 'i') {
+    if (!j_fast_lit(at, &p, ",\"image_subseqs\":[")) return false;
+    img_at = p - 1;
+    if (!j_fast_list(at, &p, &n_img, &sum)) return false;
+  }
+  if (at(p) == ',') {
+    if (!j_fast_lit(at, &p, ",\"audio_subseqs\":[")) return false;
+    aud_at = p - 1;
+    if (!j_fast_list(at, &p, &n_aud, &sum)) return false;
+  }
+  if (at(p) != '}' || p + 1 != len) return false;
+  r->text = text;
+  r->n_img = n_img;
+  r->n_aud = n_aud;
+  r->img_at = img_at;
+  r->aud_at = aud_at;
+  const long long tot = text + sum;
+  r->status = J_OK;
+  r->reason = JR_NONE;
+  if (tot < 1) {
+    r->status = J_INVARIANT;
+    r->reason = JR_NO_TOKENS;
+  } else if (tot > seq_len_cap) {
+    r->status = J_INVARIANT;
+    r->reason = JR_OVER_CAP;
+  }
+  return true;
+}
+
+// One line: the canonical fast path, else the general parser.
+template <class B>
+DTB_HD inline JLine j_parse_record(const B& at, int len, long long seq_len_cap, bool* fast) {
+  JLine r;
+  *fast = j_fast_line(at, len, seq_len_cap, &r);
+  if (*fast) return r;
+  return j_parse_line(at, len, seq_len_cap);
+}
+
+// Pass 2 on a fast-path line: plain unsigned digits.
+template <class B>
+DTB_HD inline void j_write_array_fast(const B& at, int a, int* dst) {
+  int q = a + 1, k = 0;
+  if (at(q) == ']') return;
+  for (;;) {
+    int v = 0, c;
+    while ((c = at(q)) >= '0' && c <= '9') {
+      v = v * 10 + (c - '0');
+      ++q;
+    }
+    dst[k++] = v;
+    if (at(q++) == ']') return;
+  }
+}
+
 // Pass 2: the values of a validated array at byte a, as int32.
 template <class B>
 DTB_HD inline void j_write_array(const B& at, int a, int* dst) {

@@ -117,15 +117,79 @@ __device__ __forceinline__ void line_span(const long long* nl, long long n_nl, l
   *e = k < n_nl ? nl[k] : len;
 }
 
-__global__ void __launch_bounds__(128)
+// A block's lines are contiguous in the buffer: the block stages the byte
+// window of its 128 lines in shared memory with coalesced 16-byte loads, and
+// each thread parses its line from there (bytes past the staged window, on
+// rare long lines, are read from global memory).
+constexpr int kPT = 128;
+constexpr int kFastBit = 1 << 16;  // status flag: the line took the canonical fast path
+constexpr int kStage = 16384;
+
+struct JStaged {
+  const unsigned char* sm;  // the line's first byte in the staged window
+  int sn;                   // staged bytes of the line
+  const unsigned char* g;   // the line in global memory
+  int n;
+  __device__ __forceinline__ int operator()(int i) const {
+    return i < sn ? static_cast<int>(sm[i]) : i < n ? static_cast<int>(__ldg(g + i)) : -1;
+  }
+};
+
+struct StageWin {
+  long long w0, wn;
+};
+
+__device__ __forceinline__ StageWin stage_lines(const unsigned char* __restrict__ b, long long len,
+                                                const long long* nl, long long n_nl,
+                                                long long n_lines, unsigned char* sm) {
+  __shared__ long long s_w0, s_wn;
+  const long long k0 = blockIdx.x * static_cast<long long>(kPT);
+  if (threadIdx.x == 0) {
+    long long s, e, s1, e1;
+    line_span(nl, n_nl, len, k0, &s, &e);
+    const long long kl = min(k0 + kPT, n_lines) - 1;
+    line_span(nl, n_nl, len, kl, &s1, &e1);
+    s_w0 = s & ~15ll;
+    s_wn = min(e1 - s_w0, static_cast<long long>(kStage));
+  }
+  __syncthreads();
+  const long long w0 = s_w0, wn = s_wn;
+  if ((reinterpret_cast<uintptr_t>(b) & 15) == 0) {
+    for (long long v = threadIdx.x; 16 * v < wn; v += kPT) {
+      const long long off = w0 + 16 * v;
+      if (off + 16 <= len) {
+        *reinterpret_cast<uint4*>(sm + 16 * v) = __ldg(reinterpret_cast<const uint4*>(b + off));
+      } else {
+        for (long long q = off; q < len; ++q) sm[q - w0] = __ldg(b + q);
+      }
+    }
+  } else {
+    for (long long q = threadIdx.x; q < wn; q += kPT) sm[q] = __ldg(b + w0 + q);
+  }
+  __syncthreads();
+  return StageWin{w0, wn};
+}
+
+__device__ __forceinline__ JStaged staged_line(const unsigned char* b, const unsigned char* sm,
+                                               StageWin w, long long s, long long e) {
+  const long long rel = s - w.w0;
+  long long sn = w.wn - rel;
+  sn = sn < 0 ? 0 : sn > e - s ? e - s : sn;
+  return JStaged{sm + (rel < w.wn ? rel : 0), static_cast<int>(sn), b + s, static_cast<int>(e - s)};
+}
+
+__global__ void __launch_bounds__(kPT)
 ingest_parse_kernel(const unsigned char* __restrict__ b, long long len,
                     const long long* __restrict__ nl, long long n_nl, long long n_lines,
                     long long cap, IngestLines L, unsigned long long* __restrict__ first_bad) {
-  const long long k = blockIdx.x * 128ll + threadIdx.x;
+  __shared__ alignas(16) unsigned char sm[kStage];
+  const StageWin w = stage_lines(b, len, nl, n_nl, n_lines, sm);
+  const long long k = blockIdx.x * static_cast<long long>(kPT) + threadIdx.x;
   if (k >= n_lines) return;
   long long s, e;
   line_span(nl, n_nl, len, k, &s, &e);
   JLine r;
+  bool fast = false;
   if (e - s > 0x7fffffffll) {
     r.status = J_UNSUPPORTED;
     r.reason = JR_INT32;
@@ -133,9 +197,9 @@ ingest_parse_kernel(const unsigned char* __restrict__ b, long long len,
     r.n_img = r.n_aud = 0;
     r.img_at = r.aud_at = -1;
   } else {
-    r = j_parse_line(JDev{b + s, static_cast<int>(e - s)}, static_cast<int>(e - s), cap);
+    r = j_parse_record(staged_line(b, sm, w, s, e), static_cast<int>(e - s), cap, &fast);
   }
-  L.status[k] = r.status | (r.reason << 8);
+  L.status[k] = r.status | (r.reason << 8) | (fast ? kFastBit : 0);
   const bool ok = r.status == J_OK;
   L.text[k] = r.text;
   L.img_at[k] = r.img_at;
@@ -144,27 +208,36 @@ ingest_parse_kernel(const unsigned char* __restrict__ b, long long len,
   if (r.status >= J_PARSE) atomicMin(first_bad, static_cast<unsigned long long>(k));
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kPT)
 ingest_write_kernel(const unsigned char* __restrict__ b, long long len,
                     const long long* __restrict__ nl, long long n_nl, long long n_lines,
                     IngestLines L, IngestOut o) {
-  const long long k = blockIdx.x * 128ll + threadIdx.x;
+  __shared__ alignas(16) unsigned char sm[kStage];
+  const long long k = blockIdx.x * static_cast<long long>(kPT) + threadIdx.x;
   const Tri* sc = reinterpret_cast<const Tri*>(L.scan);
   if (k == 0) {
     const Tri t = sc[n_lines];
     o.image_offsets[t.s] = t.i;
     o.audio_offsets[t.s] = t.a;
   }
-  if (k >= n_lines || L.status[k] != J_OK) return;
+  if (n_lines == 0) return;
+  const StageWin w = stage_lines(b, len, nl, n_nl, n_lines, sm);
+  if (k >= n_lines || (L.status[k] & 0xffff) != J_OK) return;
+  const bool fast = (L.status[k] & kFastBit) != 0;
   long long s, e;
   line_span(nl, n_nl, len, k, &s, &e);
-  const JDev at{b + s, static_cast<int>(e - s)};
+  const JStaged at = staged_line(b, sm, w, s, e);
   const Tri t = sc[k];
   o.text_tokens[t.s] = static_cast<int>(L.text[k]);
   o.image_offsets[t.s] = t.i;
   o.audio_offsets[t.s] = t.a;
-  if (L.img_at[k] >= 0) j_write_array(at, L.img_at[k], o.image_tokens + t.i);
-  if (L.aud_at[k] >= 0) j_write_array(at, L.aud_at[k], o.audio_tokens + t.a);
+  if (fast) {
+    if (L.img_at[k] >= 0) j_write_array_fast(at, L.img_at[k], o.image_tokens + t.i);
+    if (L.aud_at[k] >= 0) j_write_array_fast(at, L.aud_at[k], o.audio_tokens + t.a);
+  } else {
+    if (L.img_at[k] >= 0) j_write_array(at, L.img_at[k], o.image_tokens + t.i);
+    if (L.aud_at[k] >= 0) j_write_array(at, L.aud_at[k], o.audio_tokens + t.a);
+  }
 }
 
 }  // namespace
@@ -229,9 +302,9 @@ cudaError_t launch_ingest_parse(const unsigned char* b, long long len, const lon
                                 long long n_nl, long long n_lines, long long cap,
                                 const IngestLines& L, unsigned long long* first_bad, void* scratch,
                                 size_t scratch_bytes, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>((n_lines + 127) / 128);
+  const unsigned grid = static_cast<unsigned>((n_lines + kPT - 1) / kPT);
   if (n_lines > 0)
-    ingest_parse_kernel<<<grid, 128, 0, st>>>(b, len, nl, n_nl, n_lines, cap, L, first_bad);
+    ingest_parse_kernel<<<grid, kPT, 0, st>>>(b, len, nl, n_nl, n_lines, cap, L, first_bad);
   // counts[n_lines] = 0, so scan[n_lines] = totals
   cudaError_t e = cudaMemsetAsync(reinterpret_cast<Tri*>(L.counts) + n_lines, 0, sizeof(Tri), st);
   if (e != cudaSuccess) return e;
@@ -246,8 +319,8 @@ cudaError_t launch_ingest_parse(const unsigned char* b, long long len, const lon
 cudaError_t launch_ingest_write(const unsigned char* b, long long len, const long long* nl,
                                 long long n_nl, long long n_lines, const IngestLines& L,
                                 const IngestOut& o, cudaStream_t st) {
-  const long long grid = (n_lines + 127) / 128;
-  ingest_write_kernel<<<static_cast<unsigned>(grid > 0 ? grid : 1), 128, 0, st>>>(
+  const long long grid = (n_lines + kPT - 1) / kPT;
+  ingest_write_kernel<<<static_cast<unsigned>(grid > 0 ? grid : 1), kPT, 0, st>>>(
       b, len, nl, n_nl, n_lines, L, o);
   return cudaGetLastError();
 }

@@ -12,19 +12,26 @@ struct JHost {
 };
 }  // namespace
 
-// out: status, reason, text, n_img, n_aud; vals: image then audio values
+// out: status, reason, text, n_img, n_aud, fast; vals: image then audio values
 extern "C" int jh_parse(const char* b, int len, long long cap, long long* out, int* vals,
                         int cap_vals) {
   const JHost at{reinterpret_cast<const unsigned char*>(b), len};
-  const dtb::JLine r = dtb::j_parse_line(at, len, cap);
+  bool fast = false;
+  const dtb::JLine r = dtb::j_parse_record(at, len, cap, &fast);
   out[0] = r.status;
   out[1] = r.reason;
   out[2] = r.text;
   out[3] = r.n_img;
   out[4] = r.n_aud;
+  out[5] = fast ? 1 : 0;
   if (r.status == dtb::J_OK && r.n_img + r.n_aud <= cap_vals) {
-    if (r.img_at >= 0) dtb::j_write_array(at, r.img_at, vals);
-    if (r.aud_at >= 0) dtb::j_write_array(at, r.aud_at, vals + r.n_img);
+    if (fast) {
+      if (r.img_at >= 0) dtb::j_write_array_fast(at, r.img_at, vals);
+      if (r.aud_at >= 0) dtb::j_write_array_fast(at, r.aud_at, vals + r.n_img);
+    } else {
+      if (r.img_at >= 0) dtb::j_write_array(at, r.img_at, vals);
+      if (r.aud_at >= 0) dtb::j_write_array(at, r.aud_at, vals + r.n_img);
+    }
   }
   return r.status;
 }

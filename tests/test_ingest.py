@@ -66,7 +66,7 @@ J_OK, J_BLANK, J_PARSE, J_INVARIANT, J_UNSUPPORTED = range(5)
 
 
 def host_parse(lib, line: bytes, cap: int):
-    out = (C.c_longlong * 5)()
+    out = (C.c_longlong * 6)()
     vals = (C.c_int * 4096)()
     st = lib.jh_parse(line, len(line), cap, out, vals, 4096)
     if st != J_OK:

@@ -97,6 +97,20 @@ def random_record(rng: random.Random) -> str:
     return body
 
 
+def canonical_record(rng: random.Random) -> str:
+    """write_trace's layout (the ingest fast path), with boundary values."""
+    def num():
+        return rng.choice([str(rng.randint(0, 3000)), "0", "00", "05", "999999999", "1000000000",
+                           "2147483647", "-1", "1.0", str(rng.randint(0, 10 ** 12))])
+    s = '{"text_tokens":' + (num() if rng.random() < 0.3 else str(rng.randint(0, 2000)))
+    if rng.random() < 0.9:
+        s += ',"image_subseqs":[' + ",".join(num() if rng.random() < 0.2 else str(v)
+                                              for v in _int_list(rng)) + "]"
+    if rng.random() < 0.4:
+        s += ',"audio_subseqs":[' + ",".join(str(v) for v in _int_list(rng)) + "]"
+    return s + "}"
+
+
 def mutate(rng: random.Random, line: bytes) -> bytes:
     b = bytearray(line)
     for _ in range(rng.randint(1, 3)):
@@ -115,7 +129,7 @@ def random_lines(seed: int, n: int) -> list:
     rng = random.Random(seed)
     out = []
     for _ in range(n):
-        line = random_record(rng).encode("utf-8")
+        line = (canonical_record(rng) if rng.random() < 0.3 else random_record(rng)).encode("utf-8")
         if rng.random() < 0.2:
             line = mutate(rng, line)
         out.append(line)
