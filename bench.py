@@ -462,6 +462,67 @@ def main():
                                     "value": 3628800 / ex_dt, "unit": "orderings/s",
                                     "ms_per_call": ex_dt * 1e3,
                                     "timing": "host wall clock around the C-ABI call"}
+        # trace ingest: write_trace JSONL of a 16M-sample
+        # stream -> sample CSR; device-resident bytes, and the host API
+        from paper_2408_04275_b200.workload import write_trace
+        import torch
+        tr_base_n = 1 << 20
+        tr_base = write_trace(synth_stream(tr_base_n, seed=7))
+        tr_reps = 16
+        tr_bytes = tr_base * tr_reps
+        tr_n = tr_base_n * tr_reps
+        d_tr = torch.frombuffer(bytearray(tr_bytes), dtype=torch.uint8).cuda()
+        tr_res = pl.ingest_trace_dev(d_tr.data_ptr(), len(tr_bytes), 8192)
+        tr_out = {"text_tokens": torch.empty(tr_n, dtype=torch.int32, device="cuda"),
+                  "image_offsets": torch.empty(tr_n + 1, dtype=torch.int32, device="cuda"),
+                  "image_tokens": torch.empty(max(1, tr_res.n_image), dtype=torch.int32,
+                                              device="cuda"),
+                  "audio_offsets": torch.empty(tr_n + 1, dtype=torch.int32, device="cuda"),
+                  "audio_tokens": torch.empty(max(1, tr_res.n_audio), dtype=torch.int32,
+                                              device="cuda")}
+        tr_o = dict(cap_samples=tr_n, cap_image=tr_res.n_image, cap_audio=tr_res.n_audio,
+                    **{k: v.data_ptr() for k, v in tr_out.items()})
+        for _ in range(2):
+            pl.ingest_trace_dev(d_tr.data_ptr(), len(tr_bytes), 8192, tr_o)
+        torch.cuda.synchronize()
+        tr_ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            pl.ingest_trace_dev(d_tr.data_ptr(), len(tr_bytes), 8192, tr_o)
+            torch.cuda.synchronize()
+            tr_ts.append(time.perf_counter() - t0)
+        tr_dt = float(np.median(tr_ts))
+        t0 = time.perf_counter()
+        tr_host = pl.ingest_trace(tr_bytes, 8192)
+        tr_e2e = time.perf_counter() - t0
+        assert tr_host.n == tr_n
+        del d_tr, tr_out
+        tr_cpu = {}
+        try:
+            import oracle
+            if oracle.ref_available():
+                sl = tr_base[: len(tr_base) // 8]
+                sl = sl[: sl.rindex(b"\n") + 1]
+                t0 = time.perf_counter()
+                r_cpu = oracle.ref().ingest_trace(sl, 8192)
+                tr_cpu = {"value": r_cpu.n / (time.perf_counter() - t0), "unit": "samples/s",
+                          "cores": 1, "kind": "reference",
+                          "sample": f"first {r_cpu.n} lines ({len(sl)} bytes); ingest_trace "
+                                    "reads one std::istream sequentially"}
+        except Exception as ex:  # pragma: no cover
+            tr_cpu = {"error": str(ex)}
+        out["ingest"] = {"metric": "trace samples ingested/s (ingest_trace, write_trace JSONL "
+                                   "of the 16M-sample mixed stream -> sample CSR)",
+                         "value": tr_n / tr_dt, "unit": "samples/s", "ms_per_call": tr_dt * 1e3,
+                         "bytes": len(tr_bytes), "gb_per_s": len(tr_bytes) / tr_dt / 1e9,
+                         "timing": "host wall clock around dtb_ingest_trace_dev (device "
+                                   "bytes -> device CSR, includes its internal syncs)",
+                         "e2e": {"value": tr_n / tr_e2e, "unit": "samples/s",
+                                 "h2d_bytes_per_step": len(tr_bytes),
+                                 "d2h_bytes_per_step": 4 * (3 * tr_n + 2 + tr_res.n_image +
+                                                            tr_res.n_audio),
+                                 "path": "dtb_ingest_trace (pageable host bytes -> host CSR)"},
+                         "cpu_baseline": tr_cpu}
         # orchestration search, BASELINE config 3
         smodel, scluster, sbook, sbs, sstats = search_workload()
         scm = pl.cost_model(smodel, scluster, sbook)

@@ -76,3 +76,20 @@ def synth_stream(n: int, seed: int = 1, family: str = "mixed",
         raise ValueError("stream exceeds the int32 CSR offset limit")
     return SampleBatch(text.astype(np.int32), img_off.astype(np.int32), img_tokens,
                        aud_off.astype(np.int32), aud_tokens)
+
+
+def write_trace(batch: SampleBatch) -> bytes:
+    """write_trace (src/workload.cpp:157-165) of a SampleBatch: one nlohmann
+    ordered_json dump per line — compact separators, keys text_tokens,
+    image_subseqs, then audio_subseqs only when non-empty."""
+    import json
+    io, it = batch.image_offsets, batch.image_tokens
+    ao, at = batch.audio_offsets, batch.audio_tokens
+    text = batch.text.tolist()
+    lines = []
+    for i in range(batch.n):
+        rec = {"text_tokens": text[i], "image_subseqs": it[io[i]:io[i + 1]].tolist()}
+        if ao[i + 1] > ao[i]:
+            rec["audio_subseqs"] = at[ao[i]:ao[i + 1]].tolist()
+        lines.append(json.dumps(rec, separators=(",", ":")))
+    return ("\n".join(lines) + "\n").encode()

@@ -137,17 +137,8 @@ def random_lines(seed: int, n: int) -> list:
 
 
 def write_trace(batch) -> bytes:
-    """write_trace (src/workload.cpp:157-165) of a SampleBatch: nlohmann
-    ordered_json dump — compact separators, audio_subseqs only if non-empty."""
-    lines = []
-    for i in range(batch.n):
-        img = batch.image_tokens[batch.image_offsets[i]:batch.image_offsets[i + 1]].tolist()
-        aud = batch.audio_tokens[batch.audio_offsets[i]:batch.audio_offsets[i + 1]].tolist()
-        rec = {"text_tokens": int(batch.text[i]), "image_subseqs": img}
-        if aud:
-            rec["audio_subseqs"] = aud
-        lines.append(json.dumps(rec, separators=(",", ":")))
-    return ("\n".join(lines) + "\n").encode()
+    from paper_2408_04275_b200.workload import write_trace as wt
+    return wt(batch)
 
 
 def synth_trace(n: int, seed: int = 1) -> bytes:
