@@ -523,14 +523,13 @@ DTB_HD inline bool j_fast_uint(const B& at, int* p, long long* v) {
   return true;
 }
 
-template <class B>
-DTB_HD inline bool j_fast_lit(const B& at, int* p, const char* lit) {
-  for (int k = 0; lit[k]; ++k)
+// literal match, unrolled so every character is an immediate
+template <class B, int N>
+DTB_HD inline bool j_fast_lit(const B& at, int* p, const char (&lit)[N]) {
+#pragma unroll
+  for (int k = 0; k < N - 1; ++k)
     if (at(*p + k) != static_cast<unsigned char>(lit[k])) return false;
-  while (lit[0]) {
-    ++lit;
-    ++*p;
-  }
+  *p += N - 1;
   return true;
 }
 

@@ -170,6 +170,15 @@ __device__ __forceinline__ StageWin stage_lines(const unsigned char* __restrict_
   return StageWin{w0, wn};
 }
 
+// a line entirely inside the staged window
+struct JSmem {
+  const unsigned char* sm;
+  int n;
+  __device__ __forceinline__ int operator()(int i) const {
+    return i < n ? static_cast<int>(sm[i]) : -1;
+  }
+};
+
 __device__ __forceinline__ JStaged staged_line(const unsigned char* b, const unsigned char* sm,
                                                StageWin w, long long s, long long e) {
   const long long rel = s - w.w0;
@@ -197,7 +206,9 @@ ingest_parse_kernel(const unsigned char* __restrict__ b, long long len,
     r.n_img = r.n_aud = 0;
     r.img_at = r.aud_at = -1;
   } else {
-    r = j_parse_record(staged_line(b, sm, w, s, e), static_cast<int>(e - s), cap, &fast);
+    const JStaged at = staged_line(b, sm, w, s, e);
+    r = at.sn == at.n ? j_parse_record(JSmem{at.sm, at.n}, at.n, cap, &fast)
+                      : j_parse_record(at, at.n, cap, &fast);
   }
   L.status[k] = r.status | (r.reason << 8) | (fast ? kFastBit : 0);
   const bool ok = r.status == J_OK;
@@ -231,7 +242,11 @@ ingest_write_kernel(const unsigned char* __restrict__ b, long long len,
   o.text_tokens[t.s] = static_cast<int>(L.text[k]);
   o.image_offsets[t.s] = t.i;
   o.audio_offsets[t.s] = t.a;
-  if (fast) {
+  if (fast && at.sn == at.n) {
+    const JSmem as{at.sm, at.n};
+    if (L.img_at[k] >= 0) j_write_array_fast(as, L.img_at[k], o.image_tokens + t.i);
+    if (L.aud_at[k] >= 0) j_write_array_fast(as, L.aud_at[k], o.audio_tokens + t.a);
+  } else if (fast) {
     if (L.img_at[k] >= 0) j_write_array_fast(at, L.img_at[k], o.image_tokens + t.i);
     if (L.aud_at[k] >= 0) j_write_array_fast(at, L.aud_at[k], o.audio_tokens + t.a);
   } else {
