@@ -182,8 +182,20 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   // warp) instead of l predicated ones
   unsigned char* PL = colPL + static_cast<size_t>(t) * pls;
   for (int q = 0; q < l; ++q) PL[q] = static_cast<unsigned char>(q);
+  // removes list position `pos` four bytes per step (rows are word aligned;
+  // little-endian byte order)
   auto list_remove = [&](int pos) {
-    for (int q = pos; q + 1 < npend; ++q) PL[q] = PL[q + 1];
+    unsigned* W = reinterpret_cast<unsigned*>(PL);
+    const int k0 = pos >> 2, nw = (npend + 3) >> 2;
+    const unsigned keep = (1u << (8 * (pos & 3))) - 1u;
+    unsigned w = W[k0];
+    for (int k = k0; k < nw; ++k) {
+      const unsigned nx = k + 1 < nw ? W[k + 1] : 0u;
+      unsigned v = __funnelshift_r(w, nx, 8);
+      if (k == k0) v = (w & keep) | (v & ~keep);
+      W[k] = v;
+      w = nx;
+    }
   };
   auto list_find = [&](int idx) -> int {  // position of idx (ascending list)
     int lo = 0, hi = npend - 1;

@@ -978,6 +978,12 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
                               : tiled_for<false>(a.plan.unit[0].pp, a.plan.unit[1].pp,
                                                  a.plan.unit[2].pp);
     if (fn != nullptr) {
+#ifndef DTB_SIM_CARVEOUT
+#define DTB_SIM_CARVEOUT 0
+#endif
+      // no shared memory: all of the unified L1 caches cost-table rows (the
+      // rows a stream touches, token sums <= seq_len, are ~260 KB)
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, DTB_SIM_CARVEOUT);
       const unsigned g = static_cast<unsigned>((total + kSimT - 1) / kSimT);
       fn<<<g, kSimT, 0, stream>>>(a);
       return cudaGetLastError();
