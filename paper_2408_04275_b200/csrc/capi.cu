@@ -1065,8 +1065,15 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   if (mode->inter) {
     CU(inter.alloc(4ull * n_mb, s));
     ia.orders = inter.as<int>();
-    if (inter_tok) CU(launch_inter_tok(ia, s));
-    else CU(launch_inter(ia, scr.p, inter_bytes, s));
+    DBuf redo;
+    if (inter_tok) {
+      CU(redo.alloc(static_cast<size_t>(ia.batch), s));
+      CU(cudaMemsetAsync(redo.p, 0, static_cast<size_t>(ia.batch), s));
+      ia.redo = redo.as<unsigned char>();
+      CU(launch_inter_tok(ia, s));
+    } else {
+      CU(launch_inter(ia, scr.p, inter_bytes, s));
+    }
   }
   if (compose_needed)
     CU(launch_compose(n_batches, n, dp_lm, dp_me, intra_out, mode->inter ? inter.as<int>() : nullptr,

@@ -69,11 +69,17 @@ __host__ __device__ inline int inter_pl_stride(int l) {
   return 4 * w;
 }
 
-__host__ __device__ inline size_t inter_tok_bytes_per_thread(int l) {
-  return static_cast<size_t>(l) * (3 * 8 + 2 + 1) + 2 * 8 * kBRing + inter_pl_stride(l);
+__host__ __device__ inline size_t inter_tok_bytes_per_thread(int l, bool gather) {
+  return static_cast<size_t>(l) * ((gather ? 0 : 3 * 8) + 2 + 1) + 2 * 8 * kBRing +
+         inter_pl_stride(l);
 }
 
-template <int PE, int PB, int PG>
+// GATHER: forward values and keys are read from the (L1-resident) cost table
+// through the token sums instead of being kept in shared memory — 0.77 KB of
+// on-chip state per problem instead of 3.8 KB, so ~4x the problems per SM.
+// Problems whose sums fall outside the table (or beyond u16) are flagged in
+// a.redo and solved by the shared-memory variant (a.redo_only).
+template <int PE, int PB, int PG, bool GATHER>
 __global__ void __launch_bounds__(128)
 inter_tok_kernel(const __grid_constant__ InterArgs a) {
   constexpr int P = PE + PB + PG;
@@ -83,9 +89,9 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   // shared tables: sequential sums of k copies of the backbone forward value
   double* sb_sum = reinterpret_cast<double*>(smem);  // [l + 1]
   double* colF = sb_sum + (l + 1);                   // [l][T] encoder F
-  double* colG = colF + static_cast<size_t>(l) * T;  // [l][T] generator F
-  double* colK = colG + static_cast<size_t>(l) * T;  // [l][T] forward keys
-  auto* colT = reinterpret_cast<unsigned short*>(colK + static_cast<size_t>(l) * T);  // tokens
+  double* colG = colF + (GATHER ? 0 : static_cast<size_t>(l) * T);  // [l][T] generator F
+  double* colK = colG + (GATHER ? 0 : static_cast<size_t>(l) * T);  // [l][T] forward keys
+  auto* colT = reinterpret_cast<unsigned short*>(colK + (GATHER ? 0 : static_cast<size_t>(l) * T));
   // backward ring [kBRing][T] (encoder, generator), 8-byte aligned after the u16 tokens
   double* colBE = reinterpret_cast<double*>(
       (reinterpret_cast<size_t>(colT + static_cast<size_t>(l) * T) + 7) & ~size_t(7));
@@ -111,6 +117,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   __syncthreads();
   const long long prob = blockIdx.x * static_cast<long long>(T) + t;
   if (prob >= a.batch) return;
+  if (!GATHER && a.redo_only && a.redo[prob] == 0) return;
   int* out = a.orders + prob * l;
   auto F = [&](int i) -> double& { return colF[static_cast<size_t>(i) * T + t]; };
   auto G = [&](int i) -> double& { return colG[static_cast<size_t>(i) * T + t]; };
@@ -119,16 +126,39 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   auto RET = [&](int i) -> unsigned char& { return colR[static_cast<size_t>(i) * T + t]; };
   auto BE = [&](int pos) -> double& { return colBE[static_cast<size_t>(pos % kBRing) * T + t]; };
   auto BG = [&](int pos) -> double& { return colBG[static_cast<size_t>(pos % kBRing) * T + t]; };
+  auto Fv = [&](int i) -> double {
+    if constexpr (GATHER) return ld_row(a.table.eg + TK(i)).x;
+    else return F(i);
+  };
+  auto Gv = [&](int i) -> double {
+    if constexpr (GATHER) return ld_row(a.table.eg + TK(i)).z;
+    else return G(i);
+  };
+  auto Kv = [&](int i) -> double {
+    if constexpr (GATHER) return __ldg(a.table.key + TK(i));
+    else return K(i);
+  };
 
   // ---- fill: rows of the problem's microbatches (staged order)
   const long long bb = prob / a.groups;
   const int grp = static_cast<int>(prob - bb * a.groups);
   int err = 0;
   bool direct_rows = false;
-  for (int i = 0; i < l; ++i) {
+  if constexpr (GATHER) {
+    for (int i = 0; i < l; ++i) {
+      const long long v = a.span == 1 ? a.tok.get(bb, grp * l + i, true)
+                                      : a.mbsum[prob * static_cast<long long>(l) + i];
+      if (v < 0 || v >= a.table.size || v > 0xffff) {
+        a.redo[prob] = 1;
+        return;
+      }
+      TK(i) = static_cast<unsigned short>(v);
+    }
+  } else for (int i = 0; i < l; ++i) {
     const long long v = a.span == 1 ? a.tok.get(bb, grp * l + i, true)
                                     : a.mbsum[prob * static_cast<long long>(l) + i];
-    if (v >= 0 && v < a.table.size) {
+    // TK is u16: larger sums (span >= 3) take the direct rows
+    if (v >= 0 && v < a.table.size && v <= 0xffff) {
       const double4 r = ld_row(a.table.eg + v);
       F(i) = r.x;
       G(i) = r.z;
@@ -228,7 +258,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
       while (m) {
         const int idx = w * 32 + __ffs(m) - 1;
         m &= m - 1;
-        const double k = K(idx);
+        const double k = Kv(idx);
         if (best < 0 || k < kb) {
           best = idx;
           kb = k;
@@ -247,7 +277,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
 #pragma unroll 4
     for (int q = 0; q < npend; ++q) {
       const int idx = PL[q];
-      const double k = K(idx);
+      const double k = Kv(idx);
       const double da = fabs(residual - k);
       const bool over = !(k <= residual);
       const bool take = best < 0 || da < db || (da == db && !over && bover);
@@ -315,11 +345,11 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     const bool enc = s < PE;
     if (r < np) {
       const int row = RET(r);
-      return enc ? F(row) : G(row);
+      return enc ? Fv(row) : Gv(row);
     }
     if (r < np + npend) return enc ? meanE : meanG;
     const int row = rear_row(r - np - npend);
-    return enc ? F(row) : G(row);
+    return enc ? Fv(row) : Gv(row);
   };
   auto candB = [&](int r, int s) -> double {
     if (r >= np && r < np + npend) {
@@ -401,8 +431,14 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
 #pragma unroll 4
       for (int q = 0; q < npend; ++q) {
         const int idx = PL[q];
-        sE += F(idx);
-        sG += G(idx);
+        if constexpr (GATHER) {
+          const double4 r = ld_row(a.table.eg + TK(idx));
+          sE += r.x;
+          sG += r.z;
+        } else {
+          sE += F(idx);
+          sG += G(idx);
+        }
       }
       const double c = static_cast<double>(npend);
       meanE = sE / c;
@@ -434,7 +470,7 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
     for (int q = 0; q < take; ++q) {
       int ppos;
       const int pick = pick_closest(residual, &ppos);
-      residual -= K(pick);
+      residual -= Kv(pick);
       place(pick);
       clear(pick);
       list_remove(ppos);
@@ -460,9 +496,10 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
 }
 
 using InterTokFn = void (*)(InterArgs);
+template <bool GATHER>
 static InterTokFn inter_tok_for(int pe, int pb, int pg) {
 #define DTB_ITOK(E, B, G) \
-  if (pe == E && pb == B && pg == G) return inter_tok_kernel<E, B, G>;
+  if (pe == E && pb == B && pg == G) return inter_tok_kernel<E, B, G, GATHER>;
   DTB_ITOK(1, 1, 1)
   DTB_ITOK(1, 2, 1)
   DTB_ITOK(2, 1, 1)
@@ -482,17 +519,16 @@ static InterTokFn inter_tok_for(int pe, int pb, int pg) {
 bool inter_tok_applies(const InterArgs& a) {
   return a.stream && a.fwd == nullptr && a.vpp == 1 && a.l >= 1 && a.l <= 255 &&
          a.table.size > 0 &&
-         inter_tok_for(a.plan.unit[0].pp, a.plan.unit[1].pp, a.plan.unit[2].pp) != nullptr;
+         inter_tok_for<false>(a.plan.unit[0].pp, a.plan.unit[1].pp, a.plan.unit[2].pp) != nullptr;
 }
 
-cudaError_t launch_inter_tok(const InterArgs& a, cudaStream_t stream) {
-  if (!inter_tok_applies(a)) return cudaErrorNotSupported;
-  const InterTokFn fn = inter_tok_for(a.plan.unit[0].pp, a.plan.unit[1].pp, a.plan.unit[2].pp);
+static cudaError_t launch_inter_tok_one(InterTokFn fn, const InterArgs& a, bool gather,
+                                        cudaStream_t stream) {
   int dev = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t fixed = 8 * static_cast<size_t>(a.l + 1) + 64 + 8;
-  const size_t per = inter_tok_bytes_per_thread(a.l);
+  const size_t per = inter_tok_bytes_per_thread(a.l, gather);
   int T = 128;
   while (T > 1 && fixed + per * T + 64 > static_cast<size_t>(max_smem)) --T;
   const size_t bytes = fixed + per * T + 64;  // + alignment slack of the ring
@@ -503,6 +539,21 @@ cudaError_t launch_inter_tok(const InterArgs& a, cudaStream_t stream) {
   if (a.batch == 0) return cudaSuccess;
   fn<<<static_cast<unsigned>((a.batch + T - 1) / T), T, bytes, stream>>>(a);
   return cudaGetLastError();
+}
+
+// With a.redo (a zeroed byte per problem): the gather variant for every
+// problem, then the shared-memory variant for the flagged ones only.
+cudaError_t launch_inter_tok(const InterArgs& a, cudaStream_t stream) {
+  if (!inter_tok_applies(a)) return cudaErrorNotSupported;
+  const int pe = a.plan.unit[0].pp, pb = a.plan.unit[1].pp, pg = a.plan.unit[2].pp;
+  if (a.redo == nullptr) return launch_inter_tok_one(inter_tok_for<false>(pe, pb, pg), a, false, stream);
+  InterArgs g = a;
+  g.redo_only = false;
+  cudaError_t e = launch_inter_tok_one(inter_tok_for<true>(pe, pb, pg), g, true, stream);
+  if (e != cudaSuccess) return e;
+  InterArgs r = a;
+  r.redo_only = true;
+  return launch_inter_tok_one(inter_tok_for<false>(pe, pb, pg), r, false, stream);
 }
 
 }  // namespace dtb

@@ -217,6 +217,8 @@ struct InterArgs {
   CostTable table;       // optional (size 0 = evaluate directly)
   int* orders;           // [batch * l]
   DevErr* err;
+  unsigned char* redo;   // inter_tok: zeroed flag per problem (gather pass), or null
+  bool redo_only;        // inter_tok shared-memory pass over flagged problems only
 };
 cudaError_t launch_inter(const InterArgs& a, void* scratch, size_t bytes,
                          cudaStream_t stream);

@@ -19,3 +19,25 @@ def test_gpu_matches_oracle(name, gpu, oracle_best):
 @pytest.mark.parametrize("case", G.ALL, ids=lambda f: f.__name__)
 def test_gpu_golden(case, gpu):
     case(gpu)
+
+
+@pytest.mark.gpu
+def test_gpu_stream_large_assembled_sums(gpu, oracle_best):
+    """span 4 with samples of 16K-32K tokens: assembled microbatch sums above
+    65535 (cost-table rows past the u16 token range) in intra+inter mode."""
+    import numpy as np
+    from parity_cases import H, assert_same
+    from paper_2408_04275_b200.api import SampleBatch
+    rng = np.random.default_rng(11)
+    model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
+    ci, co = gpu.cost_model(model, cluster, book), oracle_best.cost_model(model, cluster, book)
+    n_batches, bs, dp, dp_me = 2, 1024, 16, 4
+    pl = H.plan((1, dp_me, 1), (1, dp, 2), (1, dp_me, 1), bs)
+    big = rng.random(n_batches * bs) < 0.5
+    toks = np.where(big, rng.integers(16000, 32000, n_batches * bs),
+                    rng.integers(1, 3000, n_batches * bs))
+    s = SampleBatch.from_lists([(10, [int(t)]) for t in toks])
+    ra = gpu.reorder_stream(ci, pl, s, n_batches, inter=True)
+    rb = oracle_best.reorder_stream(co, pl, s, n_batches, inter=True)
+    for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
+        assert_same(ra[k], rb[k], k)
