@@ -70,7 +70,7 @@ __host__ __device__ inline int inter_pl_stride(int l) {
 }
 
 __host__ __device__ inline size_t inter_tok_bytes_per_thread(int l, bool gather) {
-  return static_cast<size_t>(l) * ((gather ? 0 : 3 * 8) + 2 + 1) + 2 * 8 * kBRing +
+  return static_cast<size_t>(l) * ((gather ? 0 : 3 * 8) + 2 + 1) + (gather ? 0 : 2 * 8 * kBRing) +
          inter_pl_stride(l);
 }
 
@@ -95,8 +95,9 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   // backward ring [kBRing][T] (encoder, generator), 8-byte aligned after the u16 tokens
   double* colBE = reinterpret_cast<double*>(
       (reinterpret_cast<size_t>(colT + static_cast<size_t>(l) * T) + 7) & ~size_t(7));
-  double* colBG = colBE + static_cast<size_t>(kBRing) * T;
-  unsigned char* colR = reinterpret_cast<unsigned char*>(colBG + static_cast<size_t>(kBRing) * T);
+  constexpr int RING = GATHER ? 0 : kBRing;  // the gather variant reads the table instead
+  double* colBG = colBE + static_cast<size_t>(RING) * T;
+  unsigned char* colR = reinterpret_cast<unsigned char*>(colBG + static_cast<size_t>(RING) * T);
   // per-thread pending list (ascending indices), row-contiguous: [T][stride]
   const int pls = inter_pl_stride(l);
   unsigned char* colPL = reinterpret_cast<unsigned char*>(
@@ -292,10 +293,12 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
 
   int nret = 0;
   auto place = [&](int idx) {
-    double eb, gb;
-    bwd_row(idx, &eb, &gb);
-    BE(nret) = eb;
-    BG(nret) = gb;
+    if constexpr (!GATHER) {
+      double eb, gb;
+      bwd_row(idx, &eb, &gb);
+      BE(nret) = eb;
+      BG(nret) = gb;
+    }
     RET(nret++) = static_cast<unsigned char>(idx);
   };
   const int first = pick_min();
@@ -377,7 +380,8 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
       return s < PE ? bmeanE : s < PE + PB ? bmeanB : bmeanG;
     }
     if (s >= PE && s < PE + PB) return bB;
-    if (r < np && r + kBRing >= nret) return s < PE ? BE(r) : BG(r);
+    if constexpr (!GATHER)
+      if (r < np && r + kBRing >= nret) return s < PE ? BE(r) : BG(r);
     const int row = r < np ? static_cast<int>(RET(r)) : rear_row(r - np - npend);
     double eb, gb;
     bwd_row(row, &eb, &gb);
