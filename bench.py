@@ -60,7 +60,10 @@ def dist_init():
     # stdout carries exactly one JSON line: NCCL's INFO/VERSION banner
     # ("NCCL version ...") would precede it on rank 0
     if not os.environ.get("DTB_KEEP_NCCL_DEBUG"):
+        # NCCL logs (incl. its "NCCL version" banner, printed at WARN too) go
+        # to stderr: stdout carries exactly one JSON line
         os.environ["NCCL_DEBUG"] = "WARN"
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
