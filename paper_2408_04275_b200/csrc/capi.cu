@@ -1065,11 +1065,14 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   if (mode->inter) {
     CU(inter.alloc(4ull * n_mb, s));
     ia.orders = inter.as<int>();
-    DBuf redo;
+    DBuf redo, tab_fz;
     if (inter_tok) {
       CU(redo.alloc(static_cast<size_t>(ia.batch), s));
       CU(cudaMemsetAsync(redo.p, 0, static_cast<size_t>(ia.batch), s));
       ia.redo = redo.as<unsigned char>();
+      CU(tab_fz.alloc(sizeof(double2) * tsize, s));
+      CU(launch_table_fz(tab_eg.as<double4>(), tab_fz.as<double2>(), tsize, s));
+      ia.table.fz = tab_fz.as<double2>();
       CU(launch_inter_tok(ia, s));
     } else {
       CU(launch_inter(ia, scr.p, inter_bytes, s));

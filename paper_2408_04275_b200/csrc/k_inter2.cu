@@ -128,11 +128,11 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   auto BE = [&](int pos) -> double& { return colBE[static_cast<size_t>(pos % kBRing) * T + t]; };
   auto BG = [&](int pos) -> double& { return colBG[static_cast<size_t>(pos % kBRing) * T + t]; };
   auto Fv = [&](int i) -> double {
-    if constexpr (GATHER) return ld_row(a.table.eg + TK(i)).x;
+    if constexpr (GATHER) return __ldg(a.table.fz + TK(i)).x;
     else return F(i);
   };
   auto Gv = [&](int i) -> double {
-    if constexpr (GATHER) return ld_row(a.table.eg + TK(i)).z;
+    if constexpr (GATHER) return __ldg(a.table.fz + TK(i)).y;
     else return G(i);
   };
   auto Kv = [&](int i) -> double {
@@ -436,9 +436,9 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
       for (int q = 0; q < npend; ++q) {
         const int idx = PL[q];
         if constexpr (GATHER) {
-          const double4 r = ld_row(a.table.eg + TK(idx));
+          const double2 r = __ldg(a.table.fz + TK(idx));
           sE += r.x;
-          sG += r.z;
+          sG += r.y;
         } else {
           sE += F(idx);
           sG += G(idx);
@@ -552,12 +552,26 @@ static cudaError_t launch_inter_tok_one(InterTokFn fn, const InterArgs& a, bool 
   return cudaGetLastError();
 }
 
-// With a.redo (a zeroed byte per problem): the gather variant for every
+__global__ void table_fz_kernel(const double4* __restrict__ eg, double2* __restrict__ fz, int n) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i < n) {
+    const double4 r = eg[i];
+    fz[i] = make_double2(r.x, r.z);
+  }
+}
+
+cudaError_t launch_table_fz(const double4* eg, double2* fz, int size, cudaStream_t stream) {
+  if (size > 0) table_fz_kernel<<<(size + 255) / 256, 256, 0, stream>>>(eg, fz, size);
+  return cudaGetLastError();
+}
+
+// With a.redo (a zeroed byte per problem) and a.table.fz: the gather variant for every
 // problem, then the shared-memory variant for the flagged ones only.
 cudaError_t launch_inter_tok(const InterArgs& a, cudaStream_t stream) {
   if (!inter_tok_applies(a)) return cudaErrorNotSupported;
   const int pe = a.plan.unit[0].pp, pb = a.plan.unit[1].pp, pg = a.plan.unit[2].pp;
-  if (a.redo == nullptr) return launch_inter_tok_one(inter_tok_for<false>(pe, pb, pg), a, false, stream);
+  if (a.redo == nullptr || a.table.fz == nullptr)
+    return launch_inter_tok_one(inter_tok_for<false>(pe, pb, pg), a, false, stream);
   InterArgs g = a;
   g.redo_only = false;
   cudaError_t e = launch_inter_tok_one(inter_tok_for<true>(pe, pb, pg), g, true, stream);

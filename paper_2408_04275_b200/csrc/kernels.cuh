@@ -153,8 +153,11 @@ struct CostTable {
   const double* key;   // forward key
   int size;            // sums >= size are evaluated directly
   int span;
+  const double2* fz = nullptr;  // optional compact (encoder f, generator f) rows
 };
 constexpr int kCostTableMax = 1 << 20;
+// compact forward rows of a cost table (the inter gather variant's reads)
+cudaError_t launch_table_fz(const double4* eg, double2* fz, int size, cudaStream_t stream);
 cudaError_t launch_cost_table(const DevCM& cm, const dtb_plan& plan, int span, int size,
                               double4* eg, double* key, DevErr* err, cudaStream_t stream);
 
