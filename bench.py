@@ -545,6 +545,36 @@ def main():
                          "ms_per_search": s_dt * 1e3, "candidates": res.candidates_evaluated,
                          "timing": "host wall clock around the C-ABI call (includes "
                                    "enumeration, solve, reduce, D2H)"}
+        # BASELINE config 5: search at BS 16,384, then reorder the resident
+        # 16M stream with the CHOSEN plan (ReorderMode{intra})
+        from paper_2408_04275_b200.api import PlanSpec
+        c5 = A.OrchestrationResult()
+        c5_search = []
+        for it in range(3):
+            t0 = time.perf_counter()
+            pl._check(lib.model_orchestration(pl.ctx, scm.h, C.byref(sstats), BS, 1,
+                                              C.byref(c5), None, 0))
+            c5_search.append(time.perf_counter() - t0)
+        c5_plan = PlanSpec.from_c(c5.best)
+        c5_pc = c5.best
+        c5_dp = c5_pc.unit[1].dp
+        c5_o = [torch.empty(my_batches * c5_dp, dtype=torch.float64, device="cuda")
+                for _ in range(2)] + [torch.empty(my_batches, dtype=torch.float64,
+                                                  device="cuda") for _ in range(2)]
+
+        def c5_step():
+            pl._check(lib.reorder_stream_dev(pl.ctx, scm.h, C.byref(c5_pc), C.byref(mode_intra),
+                                             C.byref(ds), my_batches, ptr(out_order),
+                                             *[ptr(x) for x in c5_o], ptr(kept), sh))
+        c5_ms = timed(c5_step, max(2, args.steps // 3), 1)
+        c5_s = float(np.median(c5_search))
+        out["config5"] = {
+            "metric": "search + reorder of the 16M stream with the chosen plan (model_orchestration "
+                      "72B MLLM, 1172 GPUs, BS 16384; disaggregated_reorder ReorderMode{intra})",
+            "plan": repr(c5_plan), "search_ms": c5_s * 1e3, "reorder_ms": c5_ms,
+            "value": my_batches * BS / (c5_s + c5_ms / 1e3), "unit": "samples/s",
+            "candidates": c5.candidates_evaluated,
+            "timing": "search: host wall clock around the C-ABI call; reorder: CUDA events"}
         # CPU baseline: the compiled reference on this host's cores
         threads = os.cpu_count() or 1
         sample_batches = max(1, min(my_batches, 2 * threads))

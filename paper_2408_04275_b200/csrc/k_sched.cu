@@ -897,6 +897,12 @@ static TiledFn tiled_for(int pe, int pb, int pg) {
 
 // General path (any stage count, interleaved schedules): rows of
 // build_stage_times materialised per group in scratch.
+// Doubles of scratch per group: end-time matrices (interleaved) or three
+// p-vectors (1F1B tick program), the l x 6 rows, avail/busy/next.
+__host__ __device__ inline long long sim_scratch_per(int l, int p, int vpp) {
+  const int devices = p / vpp;
+  return (vpp == 1 ? 3LL * p : 2LL * l * p) + 6LL * l + 3 * devices;
+}
 __global__ void group_sims_kernel(GroupSimArgs a, double* scratch) {
   const long long gid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long total = a.n_batches * a.groups;
@@ -906,10 +912,12 @@ __global__ void group_sims_kernel(GroupSimArgs a, double* scratch) {
   const int p = plan_stages(a.plan);
   const int vpp = a.plan.vpp;
   const int devices = p / vpp;
-  double* s = scratch + gid * (2LL * l * p + 6LL * l + 3 * devices);
+  // vpp == 1 (tick program) keeps only three p-vectors of end times
+  const bool tick = vpp == 1;
+  double* s = scratch + gid * sim_scratch_per(l, p, vpp);
   double* f_end = s;
   double* b_end = s + static_cast<size_t>(l) * p;
-  double* rows = b_end + static_cast<size_t>(l) * p;  // [l][6]
+  double* rows = tick ? s + 3LL * p : b_end + static_cast<size_t>(l) * p;  // [l][6]
   double* avail = rows + 6 * static_cast<size_t>(l);
   double* busy = avail + devices;
   int* next = reinterpret_cast<int*>(busy + devices);
@@ -936,7 +944,7 @@ __global__ void group_sims_kernel(GroupSimArgs a, double* scratch) {
     busy[d] += dur(op.mb, op.stage, op.phase);
     iter = smax(iter, end);
   };
-  if (vpp == 1) {
+  if (tick) {
     tick_1f1b(l, p, dur, f_end, f_end + p, f_end + 2 * p, visit);
   } else {
     const int e = dataflow_schedule(l, p, vpp, dur, f_end, b_end, next, avail, visit);
@@ -953,6 +961,111 @@ __global__ void group_sims_kernel(GroupSimArgs a, double* scratch) {
   a.t_group[gid] = iter;
 }
 
+// General 1F1B path for many stages (p > 8, vpp 1): one warp per group.
+// Every op of tick t depends only on ops of tick t-1 (tick_1f1b), so the
+// stages of a tick are independent: lanes own stages s = lane + 32k and the
+// tick state (prev, cur, avail, busy) lives in shared memory, exchanged with
+// __syncwarp between ticks.  Per-stage op order and every FP operation are
+// tick_1f1b's; the bubble sum runs over devices in order on lane 0.  Rows
+// of build_stage_times are materialised per group in scratch by all lanes.
+constexpr int kWarpSimWarps = 4;
+__global__ void __launch_bounds__(32 * kWarpSimWarps)
+group_sims_warp(GroupSimArgs a, double* scratch) {
+  extern __shared__ double wsh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long gid = blockIdx.x * static_cast<long long>(kWarpSimWarps) + warp;
+  if (gid >= a.n_batches * a.groups) return;  // uniform per warp
+  const GroupTok tok{&a, gid};
+  const int l = a.l;
+  const int p = plan_stages(a.plan);
+  double* rows = scratch + gid * sim_scratch_per(l, p, 1);
+  double* prev = wsh + static_cast<size_t>(warp) * 4 * p;
+  double* cur = prev + p;
+  double* avail = cur + p;
+  double* busy = avail + p;
+  int fault = 0, fault_i = -1;
+  for (int i = lane; i < l; i += 32) {
+    long long e, g;
+    int c;
+    tok(i, &e, &g, &c);
+    StageRow r;
+    const int code = dev_stage_row(a.cm, a.plan, mb_mean(e, c), mb_mean(g, c), &r);
+    if (code) {
+      fault = code;
+      fault_i = i;
+    }
+    for (int u = 0; u < 3; ++u) {
+      rows[i * 6 + u] = r.f[u];
+      rows[i * 6 + 3 + u] = r.b[u];
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {  // last failing row wins, as in i order
+    const int oi = __shfl_down_sync(0xffffffffu, fault_i, off);
+    const int oc = __shfl_down_sync(0xffffffffu, fault, off);
+    if (oi > fault_i) {
+      fault_i = oi;
+      fault = oc;
+    }
+  }
+  for (int s = lane; s < p; s += 32) {
+    prev[s] = 0.0;
+    cur[s] = 0.0;
+    avail[s] = 0.0;
+    busy[s] = 0.0;
+  }
+  __syncwarp();
+  auto dur = [&](int mb, int st, int ph) {
+    return rows[mb * 6 + (ph == DTB_FORWARD ? 0 : 3) + stage_unit(a.plan, st)];
+  };
+  double iter = 0.0;
+  const int last_tick = 2 * l + 2 * p - 3;
+  for (int t = 0; t <= last_tick; ++t) {
+    for (int s = lane; s < p; s += 32) {
+      const int q0 = t - s;
+      if (q0 < 0) continue;
+      if ((q0 & 1) == 0) {
+        const int i = q0 >> 1;
+        if (i >= l) continue;
+        const double dep = s > 0 ? prev[s - 1] : 0.0;
+        const double start = smax(avail[s], dep);
+        const double d = dur(i, s, DTB_FORWARD);
+        const double end = start + d;
+        avail[s] = end;
+        cur[s] = end;
+        busy[s] += d;
+        iter = smax(iter, end);
+      } else {
+        const int q = t - 2 * p + 1 + s;
+        if (q < 0 || (q & 1)) continue;
+        const int j = q >> 1;
+        if (j >= l) continue;
+        const double dep = s + 1 < p ? prev[s + 1] : prev[s];
+        const double start = smax(avail[s], dep);
+        const double d = dur(j, s, DTB_BACKWARD);
+        const double end = start + d;
+        avail[s] = end;
+        cur[s] = end;
+        busy[s] += d;
+        iter = smax(iter, end);
+      }
+    }
+    __syncwarp();
+    for (int s = lane; s < p; s += 32) prev[s] = cur[s];
+    __syncwarp();
+  }
+  for (int off = 16; off > 0; off >>= 1) iter = smax(iter, __shfl_xor_sync(0xffffffffu, iter, off));
+  if (lane != 0) return;
+  double bub = 0.0;
+  if (iter > 0.0 && p > 0) {
+    double idle = 0.0;
+    for (int d = 0; d < p; ++d) idle += iter - busy[d];
+    bub = idle / (p * iter);
+  }
+  if (a.busy) a.busy[gid] = bub;
+  if (fault) dev_fail(a.err, fault);
+  a.t_group[gid] = iter;
+}
+
 static bool fast_sims(const GroupSimArgs& a) {
   const int p = plan_stages(a.plan);
   return a.plan.vpp == 1 && p >= 2 && p <= 8;
@@ -960,9 +1073,7 @@ static bool fast_sims(const GroupSimArgs& a) {
 
 size_t group_sims_scratch(const GroupSimArgs& a) {
   if (fast_sims(a)) return 256;
-  const int p = plan_stages(a.plan);
-  const int devices = p / a.plan.vpp;
-  const long long per = 2LL * a.l * p + 6LL * a.l + 3 * devices;
+  const long long per = sim_scratch_per(a.l, plan_stages(a.plan), a.plan.vpp);
   return static_cast<size_t>(a.n_batches * a.groups * per) * sizeof(double) + 256;
 }
 
@@ -999,6 +1110,14 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
       case 7: a.stream ? group_sims_fast<7, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<7, false><<<grid, T, 0, stream>>>(a); break;
       default: a.stream ? group_sims_fast<8, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<8, false><<<grid, T, 0, stream>>>(a); break;
     }
+  } else if (a.plan.vpp == 1 && plan_stages(a.plan) > 8 &&
+             kWarpSimWarps * 4 * sizeof(double) * plan_stages(a.plan) <= 200 * 1024) {
+    const size_t smem = kWarpSimWarps * 4 * sizeof(double) * plan_stages(a.plan);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(group_sims_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+    const unsigned g = static_cast<unsigned>((total + kWarpSimWarps - 1) / kWarpSimWarps);
+    group_sims_warp<<<g, 32 * kWarpSimWarps, smem, stream>>>(a, static_cast<double*>(scratch));
   } else {
     group_sims_kernel<<<grid, T, 0, stream>>>(a, static_cast<double*>(scratch));
   }

@@ -41,3 +41,40 @@ def test_gpu_stream_large_assembled_sums(gpu, oracle_best):
     rb = oracle_best.reorder_stream(co, pl, s, n_batches, inter=True)
     for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
         assert_same(ra[k], rb[k], k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("inter", [False, True])
+def test_gpu_stream_many_stages(gpu, oracle_best, inter):
+    """General group-simulation path (p = 15 > 8 stages, vpp 1, span 2), the
+    shape of the plan model_orchestration picks for BASELINE config 5."""
+    from parity_cases import H, assert_same
+    from paper_2408_04275_b200.workload import synth_stream
+    model, cluster, book = H.desk_model(), H.desk_cluster(1172), H.desk_book()
+    ci, co = gpu.cost_model(model, cluster, book), oracle_best.cost_model(model, cluster, book)
+    n_batches, bs = 3, 1024
+    pl = H.plan((1, 8, 1), (1, 16, 11), (1, 4, 3), bs)
+    s = synth_stream(n_batches * bs, seed=5, family="mixed")
+    ra = gpu.reorder_stream(ci, pl, s, n_batches, inter=inter)
+    rb = oracle_best.reorder_stream(co, pl, s, n_batches, inter=inter)
+    for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
+        assert_same(ra[k], rb[k], k)
+
+
+@pytest.mark.gpu
+def test_gpu_config5_chosen_plan(gpu, oracle_best):
+    """BASELINE config 5: search the 72B MLLM on 1,172 GPUs at BS 16,384, then
+    reorder (intra) a 16K-sample global batch with the chosen plan."""
+    from parity_cases import H, assert_same
+    from paper_2408_04275_b200.api import stats_to_c
+    from paper_2408_04275_b200.workload import synth_stream
+    m, cl, bk = H.mllm72b_model(), H.a800_cluster(1172), H.mllm72b_book()
+    st = stats_to_c(m.seq_len, 2048.0, 2048.0)
+    ci, co = gpu.cost_model(m, cl, bk), oracle_best.cost_model(m, cl, bk)
+    g, r = gpu.model_orchestration(ci, st, 16384), oracle_best.model_orchestration(co, st, 16384)
+    assert g["best"] == r["best"] and g["times"] == r["times"]
+    s = synth_stream(16384, seed=1000, family="mixed")
+    ra = gpu.reorder_stream(ci, g["best"], s, 1, inter=False)
+    rb = oracle_best.reorder_stream(co, r["best"], s, 1, inter=False)
+    for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
+        assert_same(ra[k], rb[k], k)
