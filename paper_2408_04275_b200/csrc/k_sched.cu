@@ -1066,6 +1066,133 @@ group_sims_warp(GroupSimArgs a, double* scratch) {
   a.t_group[gid] = iter;
 }
 
+// Register form of group_sims_warp for p <= 32K stages: lane-owned stage
+// state (avail, busy) in registers; since a stage's "cur" end time always
+// equals its avail, the neighbours' previous-tick values are exchanged through
+// a double-buffered shared row (one __syncwarp per tick), and the next tick's
+// durations are loaded before this tick's dependency chain.
+template <int K>
+__global__ void __launch_bounds__(32 * kWarpSimWarps)
+group_sims_warp_reg(GroupSimArgs a, double* scratch) {
+  extern __shared__ double wsh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long gid = blockIdx.x * static_cast<long long>(kWarpSimWarps) + warp;
+  if (gid >= a.n_batches * a.groups) return;  // uniform per warp
+  const GroupTok tok{&a, gid};
+  const int l = a.l;
+  const int p = plan_stages(a.plan);
+  double* rows = scratch + gid * sim_scratch_per(l, p, 1);
+  double* buf = wsh + static_cast<size_t>(warp) * 2 * p;
+  int fault = 0, fault_i = -1;
+  for (int i = lane; i < l; i += 32) {
+    long long e, g;
+    int c;
+    tok(i, &e, &g, &c);
+    StageRow r;
+    const int code = dev_stage_row(a.cm, a.plan, mb_mean(e, c), mb_mean(g, c), &r);
+    if (code) {
+      fault = code;
+      fault_i = i;
+    }
+    for (int u = 0; u < 3; ++u) {
+      rows[i * 6 + u] = r.f[u];
+      rows[i * 6 + 3 + u] = r.b[u];
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {  // last failing row wins, as in i order
+    const int oi = __shfl_down_sync(0xffffffffu, fault_i, off);
+    const int oc = __shfl_down_sync(0xffffffffu, fault, off);
+    if (oi > fault_i) {
+      fault_i = oi;
+      fault = oc;
+    }
+  }
+  for (int s = lane; s < 2 * p; s += 32) buf[s] = 0.0;
+  double avail[K], busy[K], nd[K];
+  int unit[K], nk[K];  // nk: op kind at the next tick (0 none, 1 F, 2 B)
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int st = lane + 32 * k;
+    avail[k] = 0.0;
+    busy[k] = 0.0;
+    unit[k] = st < p ? stage_unit(a.plan, st) : 0;
+  }
+  __syncwarp();  // rows and buf visible to the warp
+  auto fetch = [&](int t) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int st = lane + 32 * k;
+      nk[k] = 0;
+      nd[k] = 0.0;
+      if (st >= p) continue;
+      const int q0 = t - st;
+      if (q0 < 0) continue;
+      if ((q0 & 1) == 0) {
+        const int i = q0 >> 1;
+        if (i >= l) continue;
+        nk[k] = 1;
+        nd[k] = rows[i * 6 + unit[k]];
+      } else {
+        const int q = t - 2 * p + 1 + st;
+        if (q < 0 || (q & 1)) continue;
+        const int j = q >> 1;
+        if (j >= l) continue;
+        nk[k] = 2;
+        nd[k] = rows[j * 6 + 3 + unit[k]];
+      }
+    }
+  };
+  double iter = 0.0;
+  const int last_tick = 2 * l + 2 * p - 3;
+  fetch(0);
+  for (int t = 0; t <= last_tick; ++t) {
+    double d[K];
+    int kind[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      d[k] = nd[k];
+      kind[k] = nk[k];
+    }
+    if (t < last_tick) fetch(t + 1);
+    const double* prev = buf + (t & 1) * p;
+    double* cur = buf + ((t + 1) & 1) * p;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int st = lane + 32 * k;
+      if (st >= p) continue;
+      if (kind[k] != 0) {
+        const double dep = kind[k] == 1 ? (st > 0 ? prev[st - 1] : 0.0)
+                                        : (st + 1 < p ? prev[st + 1] : prev[st]);
+        const double start = smax(avail[k], dep);
+        const double end = start + d[k];
+        avail[k] = end;
+        busy[k] += d[k];
+        iter = smax(iter, end);
+      }
+      cur[st] = avail[k];
+    }
+    __syncwarp();
+  }
+  for (int off = 16; off > 0; off >>= 1) iter = smax(iter, __shfl_xor_sync(0xffffffffu, iter, off));
+  // busy per stage to shared (buf is free now) for the in-order bubble sum
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int st = lane + 32 * k;
+    if (st < p) buf[st] = busy[k];
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  double bub = 0.0;
+  if (iter > 0.0 && p > 0) {
+    double idle = 0.0;
+    for (int dd = 0; dd < p; ++dd) idle += iter - buf[dd];
+    bub = idle / (p * iter);
+  }
+  if (a.busy) a.busy[gid] = bub;
+  if (fault) dev_fail(a.err, fault);
+  a.t_group[gid] = iter;
+}
+
 static bool fast_sims(const GroupSimArgs& a) {
   const int p = plan_stages(a.plan);
   return a.plan.vpp == 1 && p >= 2 && p <= 8;
@@ -1110,6 +1237,17 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
       case 7: a.stream ? group_sims_fast<7, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<7, false><<<grid, T, 0, stream>>>(a); break;
       default: a.stream ? group_sims_fast<8, true><<<grid, T, 0, stream>>>(a) : group_sims_fast<8, false><<<grid, T, 0, stream>>>(a); break;
     }
+  } else if (a.plan.vpp == 1 && plan_stages(a.plan) > 8 && plan_stages(a.plan) <= 128) {
+    const int p = plan_stages(a.plan);
+    const size_t smem = kWarpSimWarps * 2 * sizeof(double) * p;
+    const unsigned g = static_cast<unsigned>((total + kWarpSimWarps - 1) / kWarpSimWarps);
+    double* sc = static_cast<double*>(scratch);
+    if (p <= 64)
+      group_sims_warp_reg<2><<<g, 32 * kWarpSimWarps, smem, stream>>>(a, sc);
+    else if (p <= 96)
+      group_sims_warp_reg<3><<<g, 32 * kWarpSimWarps, smem, stream>>>(a, sc);
+    else
+      group_sims_warp_reg<4><<<g, 32 * kWarpSimWarps, smem, stream>>>(a, sc);
   } else if (a.plan.vpp == 1 && plan_stages(a.plan) > 8 &&
              kWarpSimWarps * 4 * sizeof(double) * plan_stages(a.plan) <= 200 * 1024) {
     const size_t smem = kWarpSimWarps * 4 * sizeof(double) * plan_stages(a.plan);

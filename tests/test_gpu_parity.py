@@ -45,15 +45,17 @@ def test_gpu_stream_large_assembled_sums(gpu, oracle_best):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("inter", [False, True])
-def test_gpu_stream_many_stages(gpu, oracle_best, inter):
-    """General group-simulation path (p = 15 > 8 stages, vpp 1, span 2), the
-    shape of the plan model_orchestration picks for BASELINE config 5."""
+@pytest.mark.parametrize("pp", [(11, 3), (71, 7), (140, 3)])
+def test_gpu_stream_many_stages(gpu, oracle_best, inter, pp):
+    """Many-stage group simulations (p = 15 / 79 / 144 > 8 stages, vpp 1,
+    span 2: register and shared-memory warp kernels), the shape of the plan
+    model_orchestration picks for BASELINE config 5."""
     from parity_cases import H, assert_same
     from paper_2408_04275_b200.workload import synth_stream
     model, cluster, book = H.desk_model(), H.desk_cluster(1172), H.desk_book()
     ci, co = gpu.cost_model(model, cluster, book), oracle_best.cost_model(model, cluster, book)
     n_batches, bs = 3, 1024
-    pl = H.plan((1, 8, 1), (1, 16, 11), (1, 4, 3), bs)
+    pl = H.plan((1, 8, 1), (1, 16, pp[0]), (1, 4, pp[1]), bs)
     s = synth_stream(n_batches * bs, seed=5, family="mixed")
     ra = gpu.reorder_stream(ci, pl, s, n_batches, inter=inter)
     rb = oracle_best.reorder_stream(co, pl, s, n_batches, inter=inter)
