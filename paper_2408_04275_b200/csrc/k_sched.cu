@@ -1108,8 +1108,8 @@ group_sims_warp_reg(GroupSimArgs a, double* scratch) {
     }
   }
   for (int s = lane; s < 2 * p; s += 32) buf[s] = 0.0;
-  double avail[K], busy[K], nd[K];
-  int unit[K], nk[K];  // nk: op kind at the next tick (0 none, 1 F, 2 B)
+  double avail[K], busy[K], nd[K], nd2[K];
+  int unit[K], nk[K], nk2[K];  // op kind at ticks t+1 / t+2 (0 none, 1 F, 2 B)
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int st = lane + 32 * k;
@@ -1118,7 +1118,7 @@ group_sims_warp_reg(GroupSimArgs a, double* scratch) {
     unit[k] = st < p ? stage_unit(a.plan, st) : 0;
   }
   __syncwarp();  // rows and buf visible to the warp
-  auto fetch = [&](int t) {
+  auto fetch = [&](int t, double (&nd)[K], int (&nk)[K]) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int st = lane + 32 * k;
@@ -1144,7 +1144,8 @@ group_sims_warp_reg(GroupSimArgs a, double* scratch) {
   };
   double iter = 0.0;
   const int last_tick = 2 * l + 2 * p - 3;
-  fetch(0);
+  fetch(0, nd, nk);
+  fetch(1, nd2, nk2);
   for (int t = 0; t <= last_tick; ++t) {
     double d[K];
     int kind[K];
@@ -1152,8 +1153,10 @@ group_sims_warp_reg(GroupSimArgs a, double* scratch) {
     for (int k = 0; k < K; ++k) {
       d[k] = nd[k];
       kind[k] = nk[k];
+      nd[k] = nd2[k];
+      nk[k] = nk2[k];
     }
-    if (t < last_tick) fetch(t + 1);
+    fetch(t + 2, nd2, nk2);  // two ticks ahead (beyond last_tick: no ops)
     const double* prev = buf + (t & 1) * p;
     double* cur = buf + ((t + 1) & 1) * p;
 #pragma unroll
