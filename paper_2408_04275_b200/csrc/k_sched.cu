@@ -1072,7 +1072,7 @@ group_sims_warp(GroupSimArgs a, double* scratch) {
 // a double-buffered shared row (one __syncwarp per tick), and the next tick's
 // durations are loaded before this tick's dependency chain.
 template <int K>
-__global__ void __launch_bounds__(32 * kWarpSimWarps)
+__global__ void __launch_bounds__(32 * kWarpSimWarps, 8)
 group_sims_warp_reg(GroupSimArgs a, double* scratch) {
   extern __shared__ double wsh[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
