@@ -38,17 +38,17 @@ extern "C" {
 
 /* ---------------------------------------------------------------- status */
 
-/* 1:1 with include/errors.hpp:22-84 (plus two ABI-level codes). */
+/* 1:1 with include/errors.hpp:23-86 (plus two ABI-level codes). */
 typedef enum dtb_status {
   DTB_OK = 0,
-  DTB_ERR_INTERNAL = 1,            /* InternalError        errors.hpp:52   */
-  DTB_ERR_K_TOO_LARGE = 2,         /* KTooLargeError       errors.hpp:58   */
-  DTB_ERR_INDIVISIBLE_VPP = 3,     /* IndivisibleVppError  errors.hpp:72   */
-  DTB_ERR_BATCH_SIZE_MISMATCH = 4, /* BatchSizeMismatchError errors.hpp:78 */
-  DTB_ERR_CONFIG = 5,              /* ConfigError          errors.hpp:22   */
-  DTB_ERR_EMPTY_PROFILE = 6,       /* EmptyProfileError    errors.hpp:28   */
-  DTB_ERR_INFEASIBLE = 7,          /* InfeasibleError      errors.hpp:46   */
-  DTB_ERR_CAP_EXCEEDED = 8,        /* CapExceededError     errors.hpp:64   */
+  DTB_ERR_INTERNAL = 1,            /* InternalError        errors.hpp:56   */
+  DTB_ERR_K_TOO_LARGE = 2,         /* KTooLargeError       errors.hpp:62   */
+  DTB_ERR_INDIVISIBLE_VPP = 3,     /* IndivisibleVppError  errors.hpp:75   */
+  DTB_ERR_BATCH_SIZE_MISMATCH = 4, /* BatchSizeMismatchError errors.hpp:81 */
+  DTB_ERR_CONFIG = 5,              /* ConfigError          errors.hpp:23   */
+  DTB_ERR_EMPTY_PROFILE = 6,       /* EmptyProfileError    errors.hpp:29   */
+  DTB_ERR_INFEASIBLE = 7,          /* InfeasibleError      errors.hpp:50   */
+  DTB_ERR_CAP_EXCEEDED = 8,        /* CapExceededError     errors.hpp:68   */
   DTB_ERR_TRACE = 9,               /* TraceError           errors.hpp:35   */
   DTB_ERR_INVALID_ARGUMENT = 100,  /* null pointer / ABI limit exceeded    */
   DTB_ERR_CUDA = 101               /* device failure (no reference analogue) */

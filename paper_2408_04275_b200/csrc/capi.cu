@@ -942,6 +942,46 @@ static dtb_status stream_checks(const dtb_cost_model* cm, const dtb_plan* plan,
   return DTB_OK;
 }
 
+// Sort/partition path of a stream of global batches: the streaming cost pass
+// (k_cost.cu: tokens, identity order and loads, batches the averaging bound
+// decides), then the partition kernel on the rest (k_intra.cu).  `fa` holds
+// everything but the cost-pass outputs; `cscr` receives its scratch.
+static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBuf& cscr,
+                                         cudaStream_t s) {
+  cudaError_t e = cscr.alloc(cost_scratch_bytes(n_batches, fa.m), s);
+  if (e != cudaSuccess) return e;
+  CostArgs ca{};
+  ca.n = fa.n;
+  ca.m = fa.m;
+  ca.order = fa.order;
+  ca.intra = fa.intra;
+  ca.n_batches = n_batches;
+  ca.img_off = fa.img_off;
+  ca.img_tok = fa.img_tok;
+  ca.aud_off = fa.aud_off;
+  ca.aud_tok = fa.aud_tok;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  ca.staged = al(fa.img_off) && al(fa.img_tok) &&
+              (fa.aud_off == nullptr || (al(fa.aud_off) && al(fa.aud_tok))) && fa.n % 4 == 0;
+  ca.tok16 = const_cast<unsigned short*>(fa.tok16);
+  ca.order_out = fa.order_out;
+  ca.blk_ident = cscr.as<unsigned>();
+  ca.bstat = ca.blk_ident + n_batches * fa.m;
+  ca.list = ca.bstat + 4 * n_batches;
+  ca.state = ca.list + 1 + n_batches;
+  ca.wide_flag = fa.wide_flag;
+  ca.load_before = fa.load_before;
+  ca.load_after = fa.load_after;
+  ca.kept = fa.kept;
+  ca.div_pg = fa.div_pg;
+  e = launch_cost_stream(ca, s);
+  if (e != cudaSuccess) return e;
+  fa.state = ca.state;
+  fa.blk_ident = ca.blk_ident;
+  fa.list = ca.list;
+  return launch_intra_fused(fa, n_batches, s);
+}
+
 // Device pipeline for n_batches global batches (all pointers device):
 //   token_keys (cost pass) -> intra_fused (sort/greedy/decision, per batch)
 //   -> cost table -> group sims on the input order (t_iter_before)
@@ -979,12 +1019,6 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   CU(tok32s.alloc(4ull * total, s));
   CU(wflag.alloc(4ull * n_batches, s));
   CU(wide.alloc(fused_wide_scratch_bytes(n_batches), s));
-  // Separate streaming cost pass.  (FusedArgs::fuse_cost runs it inside the
-  // fused kernel instead; measured slower on B200 — 409 vs 304 us for the
-  // 16M stream: with two 112 KB CTAs per SM too few CSR loads are in flight,
-  // profiles/r01_summary.md.)
-  CU(launch_token_keys(io, it, ao, at, total, n, tok16.as<unsigned short>(),
-                       wflag.as<unsigned int>(), s));
   FusedArgs fa{};
   fa.n = n;
   fa.m = dp_lm;
@@ -1008,7 +1042,8 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   fa.wide_flag = wflag.as<unsigned int>();
   fa.div_pg = FastDiv::make(static_cast<unsigned>(per_group));
   fa.err = ctx->err;
-  CU(launch_intra_fused(fa, n_batches, s));
+  DBuf cscr;
+  CU(launch_sort_partition(fa, n_batches, cscr, s));
   const TokSrc tok{tok16.as<unsigned short>(), tok16s.as<unsigned short>(), tok32.as<int>(),
                    tok32s.as<int>(), kept_dev, wflag.as<unsigned int>(), n};
   if (span > 1) {  // assembled microbatch sums [b][e][i]
@@ -1084,8 +1119,14 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ga.staged = true;
   ga.mbsum = span > 1 ? mb1.as<int>() : nullptr;
   ga.order = mode->inter ? inter.as<int>() : nullptr;
+  // intra only: a batch whose greedy split was not kept runs the identity
+  // order again, so its t_iter_after IS its t_iter_before (same microbatches,
+  // same operation sequence) — only kept batches are re-simulated
+  const unsigned char* only_kept = mode->inter ? nullptr : kept_dev;
+  ga.only_kept = only_kept;
   CU(launch_group_sims(ga, scr.p, s));
-  CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, ta, s));
+  CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, ta, s,
+                          only_kept, tb));
   return DTB_OK;
 }
 
@@ -1253,10 +1294,6 @@ static dtb_status intra_stream(dtb_context* ctx, int64_t bs, int32_t dp_lm, int3
   const long long total = n_batches * bs;
   CU(tok16.alloc(2ull * total + 16, static_cast<cudaStream_t>(stream)));
   CU(wflag.alloc(4ull * n_batches, static_cast<cudaStream_t>(stream)));
-  CU(launch_token_keys(samples->image_offsets, samples->image_tokens, samples->audio_offsets,
-                       samples->audio_tokens, total, static_cast<int>(bs),
-                       tok16.as<unsigned short>(), wflag.as<unsigned int>(),
-                       static_cast<cudaStream_t>(stream)));
   fa.tok16 = tok16.as<unsigned short>();
   fa.wide_flag = wflag.as<unsigned int>();
   fa.div_pg = FastDiv::make(static_cast<unsigned>(bs / dp_lm));
@@ -1264,7 +1301,8 @@ static dtb_status intra_stream(dtb_context* ctx, int64_t bs, int32_t dp_lm, int3
   fa.dp_me = dp_lm;
   fa.prof = prof;
   fa.err = ctx->err;
-  CU(launch_intra_fused(fa, n_batches, static_cast<cudaStream_t>(stream)));
+  DBuf cscr;
+  CU(launch_sort_partition(fa, n_batches, cscr, static_cast<cudaStream_t>(stream)));
   return DTB_OK;
 }
 
@@ -1277,7 +1315,7 @@ dtb_status dtb_intra_stream_dev(dtb_context* ctx, int64_t bs, int32_t dp_lm, int
 }
 
 // Debug variant (not in the public header): per-batch phase timestamps
-// (globaltimer ns) of the fused kernel, prof_dev[n_batches][8].
+// (globaltimer ns) of the fused kernel, prof_dev[n_batches][64].
 dtb_status dtb_debug_intra_stream_prof_dev(dtb_context* ctx, int64_t bs, int32_t dp_lm,
                                            int32_t sort_order, const dtb_samples* samples,
                                            int64_t n_batches, int32_t* order_out,

@@ -178,6 +178,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
           unsigned part = 0u;
           if (j < r) {
             const int g = G.AG[j], c = G.AC[j];
+#pragma unroll 4
             for (int t = tid / kFG; t < tstar; t += kRows) {
               const int item = k + t * r + j;
               part += sizes(item);

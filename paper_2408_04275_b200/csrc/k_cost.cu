@@ -1,0 +1,382 @@
+// Streaming cost pass of the disaggregated reorder (K0).
+//
+// Per sample: Sample::cost_size (include/core.hpp:160-167, src/core.cpp:90-95)
+// = 2 x (image + audio subsequence tokens), kept as u16 tokens for the
+// simulations and the partition kernel.  Per global batch: the identity
+// order's block_group_loads (src/reorder.cpp:111-119), and — when the last
+// chunk of a batch is done — the keep decision of disaggregated_reorder
+// (src/reorder.cpp:340-354) whenever an averaging bound already settles it.
+//
+// One CTA of 128 threads per chunk of 1024 consecutive samples; ~25 KB of
+// shared memory, so eight CTAs share an SM and the pass streams at HBM rate.
+// A chunk's CSR offsets and the CONTIGUOUS token spans its samples own
+// ([io[c0], io[c0 + 1024]) — a batch's tokens are one span of the CSR) are
+// brought in by bulk asynchronous copies (TMA, cp.async.bulk, completed on an
+// mbarrier); an in-place exclusive prefix sum over the staged tokens turns
+// every sample's sum into two shared-memory reads (no per-sample loops, no
+// divergence, no dependent global loads).
+//
+// The bound: with ascending sizes and equal counts (cap = n / m), the z
+// zero-cost items fill groups 0, 1, ... to cap first (every load is 0 and ties
+// go to the lowest group, src/reorder.cpp:80-88), so floor(z / cap) groups
+// hold no positive item and the positive total T is spread over at most
+// m - floor(z / cap) groups: the greedy's max block load (blocks == groups
+// when n % m == 0) is >= T / (m - floor(z / cap)).  If that exceeds the
+// identity's max block load, the reference keeps the identity order
+// (`<=` keeps the greedy) — exactly, in integers.  Every other batch goes to
+// the partition kernel.
+#include <algorithm>
+
+#include "block_ops.cuh"
+#include "kernels.cuh"
+#include "tma.cuh"
+
+namespace dtb {
+
+constexpr int kCostT = 128;                 // threads per chunk CTA
+constexpr int kCostQ = 1024;                // samples per chunk
+constexpr int kCostOff = kCostQ + 4;        // offsets + the next boundary, padded
+constexpr int kCostTok = 4096;              // token slots (image + audio + spares)
+constexpr int kCostPer = kCostQ / kCostT;   // samples per thread
+
+struct CostSmem {
+  alignas(16) int io[kCostOff];
+  alignas(16) int ao[kCostOff];
+  alignas(16) int tk[kCostTok];
+  alignas(8) unsigned long long bar[2];  // offsets, tokens
+  int bnd[6];  // lo, hi, alo, ahi, image / audio token counts of the stream
+  int tmp[2 * (kCostT / 32)];
+};
+
+// Token slots: image tokens [fl, ceil4(hi)) at [0, ilen), a zero spare slot,
+// audio tokens [afl, ceil4(ahi)) at [abase, abase + alen), a zero spare slot.
+// After the exclusive prefix sum E, a sample's image sum is E[hi - fl] -
+// E[lo - fl].  Copies end at ceil4(hi) unless that passes the stream's last
+// token (tend): then the last < 4 tokens are read by thread 0.
+struct ChunkLayout {
+  int fl, ilen, ilen_tma;
+  int afl, alen, alen_tma, abase;
+  int len;    // slots in the prefix sum
+  bool fits;  // else: per-sample sums from global memory
+};
+__device__ __forceinline__ ChunkLayout chunk_layout(int lo, int hi, int alo, int ahi, int tend,
+                                                    int aend, bool audio) {
+  ChunkLayout L;
+  L.fl = lo & ~3;
+  const int c4 = (hi + 3) & ~3;
+  L.ilen = c4 - L.fl;
+  L.ilen_tma = (c4 <= tend ? c4 : (hi & ~3)) - L.fl;
+  L.abase = (L.ilen + 4) & ~3;
+  if (audio) {
+    L.afl = alo & ~3;
+    const int ac4 = (ahi + 3) & ~3;
+    L.alen = ac4 - L.afl;
+    L.alen_tma = (ac4 <= aend ? ac4 : (ahi & ~3)) - L.afl;
+  } else {
+    L.afl = L.alen = L.alen_tma = 0;
+  }
+  L.len = L.abase + L.alen + 1;
+  L.fits = L.len <= kCostTok;
+  return L;
+}
+
+// In-place exclusive prefix sum of tk[0, len).  Returns true when a slot lies
+// outside [0, 0x7fff] (the int32 sums could overflow, or a sample's sum be
+// negative): the chunk then uses the int64 per-sample path.  Warp w scans a
+// contiguous quarter of the slots, lanes on consecutive 16-byte words
+// (conflict-free): a first pass sums the quarter, one barrier exchanges the
+// four sums, a second pass scans with the carry-in.
+__device__ __forceinline__ bool chunk_prefix(int* tk, int len, int* tmp) {
+  constexpr int W = kCostT / 32;
+  constexpr int L = 8;  // consecutive slots per lane and step (two 16-byte words)
+  const int lane = lane_id(), w = warp_id();
+  const int R = (len + W * 32 * L - 1) / (W * 32 * L) * (32 * L);  // slots per warp
+  const int beg = w * R, end = min(beg + R, len);
+  auto load = [&](int p, int* v) {
+    if (p + L <= end) {
+      const int4 x0 = *reinterpret_cast<const int4*>(tk + p);
+      const int4 x1 = *reinterpret_cast<const int4*>(tk + p + 4);
+      v[0] = x0.x, v[1] = x0.y, v[2] = x0.z, v[3] = x0.w;
+      v[4] = x1.x, v[5] = x1.y, v[6] = x1.z, v[7] = x1.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < L; ++k) v[k] = p + k < end ? tk[p + k] : 0;
+    }
+  };
+  int sum = 0;
+  unsigned orv = 0u;
+  for (int p = beg + L * lane; p < end; p += 32 * L) {
+    int v[L];
+    load(p, v);
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      sum += v[k];
+      orv |= static_cast<unsigned>(v[k]);
+    }
+  }
+  sum = static_cast<int>(__reduce_add_sync(kFull, static_cast<unsigned>(sum)));
+  orv = __reduce_or_sync(kFull, orv);
+  if (lane == 0) {
+    tmp[w] = sum;
+    tmp[W + w] = static_cast<int>(orv);
+  }
+  __syncthreads();
+  int carry = 0;
+  unsigned all_or = 0u;
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    if (k < w) carry += tmp[k];
+    all_or |= static_cast<unsigned>(tmp[W + k]);
+  }
+  const bool bad = all_or > 0x7fffu;
+  if (!bad) {
+    for (int base = beg; base < end; base += 32 * L) {
+      const int p = base + L * lane;
+      int v[L];
+      load(p, v);
+#pragma unroll
+      for (int k = 1; k < L; ++k) v[k] += v[k - 1];  // inclusive within the lane
+      int incl = v[L - 1];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int e = carry + incl - v[L - 1];  // exclusive carry-in of the lane
+      if (p + L <= end) {
+        *reinterpret_cast<int4*>(tk + p) = make_int4(e, e + v[0], e + v[1], e + v[2]);
+        *reinterpret_cast<int4*>(tk + p + 4) = make_int4(e + v[3], e + v[4], e + v[5], e + v[6]);
+      } else {
+        for (int k = 0; k < L && p + k < end; ++k) tk[p + k] = k ? e + v[k - 1] : e;
+      }
+      carry += __shfl_sync(kFull, incl, 31);
+    }
+  }
+  __syncthreads();
+  return bad;
+}
+
+// Per batch, after the cost pass: identity loads, averaging bound, batch
+// state; batches the partition kernel must process are appended to `list`.
+__global__ void __launch_bounds__(kCostT) cost_finalize_kernel(const __grid_constant__ CostArgs a) {
+  __shared__ long long red[kCostT / 32 + 1];
+  const int m = a.m, tid = threadIdx.x;
+  const long long b = blockIdx.x;
+  const unsigned* st = a.bstat + 4 * b;
+  const unsigned z = st[0], total = st[1], flags = st[2];
+  unsigned mi = 0u;
+  for (int g = tid; g < m; g += kCostT) mi = max(mi, a.blk_ident[b * m + g]);
+  mi = static_cast<unsigned>(block_max_ll<kCostT>(mi, red));
+  const bool wide = flags & 1u, big = flags & 2u;
+  bool decided = false;
+  if (!wide) {
+    if (!a.intra) {
+      decided = true;
+    } else if (a.order == DTB_ASCENDING && a.n % m == 0) {
+      const int cap = a.n / m;
+      const long long m_pos = m - static_cast<long long>(z) / cap;
+      decided = static_cast<long long>(total) > static_cast<long long>(mi) * m_pos;
+    }
+  }
+  if (decided) {
+    for (int g = tid; g < m; g += kCostT) {
+      const double l = static_cast<double>(a.blk_ident[b * m + g]);
+      if (a.load_before) a.load_before[b * m + g] = l;
+      if (a.load_after) a.load_after[b * m + g] = l;
+    }
+  }
+  if (tid == 0) {
+    if (decided && a.kept) a.kept[b] = 0;
+    a.wide_flag[b] = wide ? 1u : 0u;
+    a.state[b] = decided ? kBatchDecided : wide ? kBatchWide : big ? kBatchSort : kBatchFast;
+    if (!decided) a.list[1 + atomicAdd(a.list, 1u)] = static_cast<unsigned>(b);
+  }
+}
+
+template <bool STAGED>
+__device__ __forceinline__ void cost_chunk(const CostArgs& a, CostSmem& S) {
+  const int n = a.n, m = a.m, tid = threadIdx.x, lane = lane_id();
+  const int cpb = (n + kCostQ - 1) / kCostQ;
+  const long long b = blockIdx.x / cpb;
+  const int q0 = static_cast<int>(blockIdx.x - b * cpb) * kCostQ;
+  const int qs = min(kCostQ, n - q0);
+  const long long s0 = b * n + q0;
+  const bool audio = a.aud_off != nullptr;
+  if (tid == 0) {
+    const long long last = a.n_batches * n;
+    const unsigned ob = 4u * static_cast<unsigned>(qs);
+    if (STAGED) {  // the offsets need no bounds: their copy overlaps the bounds loads
+      mbar_init(&S.bar[0], 1);
+      mbar_init(&S.bar[1], 1);
+      mbar_init_fence();
+      mbar_arrive_expect_tx(&S.bar[0], ob * (audio ? 2u : 1u));
+      bulk_g2s(S.io, a.img_off + s0, ob, &S.bar[0]);
+      if (audio) bulk_g2s(S.ao, a.aud_off + s0, ob, &S.bar[0]);
+    }
+    const int lo = __ldg(a.img_off + s0), hi = __ldg(a.img_off + s0 + qs);
+    const int alo = audio ? __ldg(a.aud_off + s0) : 0, ahi = audio ? __ldg(a.aud_off + s0 + qs) : 0;
+    const int tend = STAGED ? __ldg(a.img_off + last) : 0;
+    const int aend = STAGED && audio ? __ldg(a.aud_off + last) : 0;
+    S.bnd[0] = lo, S.bnd[1] = hi, S.bnd[2] = alo, S.bnd[3] = ahi, S.bnd[4] = tend, S.bnd[5] = aend;
+    if (STAGED) {
+      const ChunkLayout L = chunk_layout(lo, hi, alo, ahi, tend, aend, audio);
+      S.io[qs] = hi;  // the next boundary (outside the copied range)
+      if (audio) S.ao[qs] = ahi;
+      const unsigned ib = L.fits ? 4u * static_cast<unsigned>(L.ilen_tma) : 0u;
+      const unsigned ab = L.fits ? 4u * static_cast<unsigned>(L.alen_tma) : 0u;
+      if (L.fits) {  // slots the prefix sum reads but no copy writes
+        for (int k = L.ilen; k < L.abase; ++k) S.tk[k] = 0;
+        S.tk[L.abase + L.alen] = 0;
+      }
+      mbar_arrive_expect_tx(&S.bar[1], ib + ab);
+      if (ib) bulk_g2s(S.tk, a.img_tok + L.fl, ib, &S.bar[1]);
+      if (ab) bulk_g2s(S.tk + L.abase, a.aud_tok + L.afl, ab, &S.bar[1]);
+    }
+  }
+  __syncthreads();
+  const int* io_s = STAGED ? S.io : a.img_off + s0;
+  const int* ao_s = STAGED ? S.ao : (audio ? a.aud_off + s0 : nullptr);
+  ChunkLayout L{};
+  bool pre = false;
+  if (STAGED) {
+    L = chunk_layout(S.bnd[0], S.bnd[1], S.bnd[2], S.bnd[3], S.bnd[4], S.bnd[5], audio);
+    mbar_wait(&S.bar[1], 0u);
+    if (L.fits) {
+      if (L.ilen_tma < L.ilen || L.alen_tma < L.alen) {  // the stream's last tokens
+        if (tid == 0) {
+          for (int k = L.ilen_tma; k < L.ilen; ++k)
+            S.tk[k] = L.fl + k < S.bnd[1] ? __ldg(a.img_tok + L.fl + k) : 0;
+          for (int k = L.alen_tma; k < L.alen; ++k)
+            S.tk[L.abase + k] = L.afl + k < S.bnd[3] ? __ldg(a.aud_tok + L.afl + k) : 0;
+        }
+        __syncthreads();
+      }
+      pre = !chunk_prefix(S.tk, L.len, S.tmp);
+    }
+    mbar_wait(&S.bar[0], 0u);
+  }
+  // ---- per sample: thread t takes 4 consecutive samples per round (5
+  // boundaries, one 8-byte token store)
+  unsigned zeros = 0u, total = 0u;
+  bool wide = false, big = false;
+  unsigned short* tok_out = a.tok16 + s0;
+  unsigned* blk = a.blk_ident + b * m;
+  for (int j0 = 4 * tid; j0 < qs; j0 += 4 * kCostT) {  // qs % 4 == 0 when STAGED
+    unsigned t4[4];
+    if (STAGED && pre) {
+      const int4 o = *reinterpret_cast<const int4*>(io_s + j0);
+      const int o4 = io_s[j0 + 4];
+      const int e0 = S.tk[o.x - L.fl], e1 = S.tk[o.y - L.fl], e2 = S.tk[o.z - L.fl],
+                e3 = S.tk[o.w - L.fl], e4 = S.tk[o4 - L.fl];
+      int v[4] = {e1 - e0, e2 - e1, e3 - e2, e4 - e3};
+      if (audio) {
+        const int4 p = *reinterpret_cast<const int4*>(ao_s + j0);
+        const int p4 = ao_s[j0 + 4];
+        const int* E = S.tk + L.abase - L.afl;
+        const int f0 = E[p.x], f1 = E[p.y], f2 = E[p.z], f3 = E[p.w], f4 = E[p4];
+        v[0] += f1 - f0, v[1] += f2 - f1, v[2] += f3 - f2, v[3] += f4 - f3;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) t4[k] = static_cast<unsigned>(v[k]);  // in [0, 0x7fff * len]
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = j0 + k;
+        long long t = 0;
+        if (j < qs) {
+          for (int x = io_s[j]; x < io_s[j + 1]; ++x) t += __ldg(a.img_tok + x);
+          if (audio)
+            for (int y = ao_s[j]; y < ao_s[j + 1]; ++y) t += __ldg(a.aud_tok + y);
+        }
+        t4[k] = t < 0 ? 0xffffffffu : t > 0xfffffffell ? 0xfffffffeu : static_cast<unsigned>(t);
+      }
+    }
+    unsigned s2 = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool ok = j0 + k < qs;
+      const bool bad = t4[k] > 0x7fffu;  // negative sums mapped above 0x7fff
+      wide |= ok && bad;
+      const unsigned tok = ok ? (bad ? 0x7fffu : t4[k]) : 0u;
+      t4[k] = tok;
+      big |= tok >= 8192u;
+      zeros += ok && tok == 0u;
+      s2 += 2u * tok;
+    }
+    total += s2;
+    if (j0 + 3 < qs && (reinterpret_cast<uintptr_t>(tok_out + j0) & 7u) == 0) {
+      uint2 pk;
+      pk.x = t4[0] | (t4[1] << 16);
+      pk.y = t4[2] | (t4[3] << 16);
+      *reinterpret_cast<uint2*>(tok_out + j0) = pk;
+    } else {
+      for (int k = 0; k < 4 && j0 + k < qs; ++k) tok_out[j0 + k] = static_cast<unsigned short>(t4[k]);
+    }
+    // identity block loads: one atomic per warp when its 128 samples share a
+    // block, else per sample
+    const unsigned bl0 = min(a.div_pg.div(static_cast<unsigned>(q0 + j0)), static_cast<unsigned>(m - 1));
+    const unsigned bl3 =
+        min(a.div_pg.div(static_cast<unsigned>(q0 + min(j0 + 3, qs - 1))), static_cast<unsigned>(m - 1));
+    const unsigned am = __activemask();
+    const unsigned w0 = __shfl_sync(am, bl0, __ffs(am) - 1);
+    if (__all_sync(am, bl0 == w0 && bl3 == w0)) {
+      const unsigned sum = __reduce_add_sync(am, s2);
+      if (lane == __ffs(am) - 1) atomicAdd(blk + w0, sum);
+    } else if (bl0 == bl3) {
+      atomicAdd(blk + bl0, s2);
+    } else {
+      for (int k = 0; k < 4 && j0 + k < qs; ++k)
+        atomicAdd(blk + min(a.div_pg.div(static_cast<unsigned>(q0 + j0 + k)),
+                            static_cast<unsigned>(m - 1)),
+                  2u * t4[k]);
+    }
+  }
+  // ---- identity order for the chunk (kept batches are overwritten later)
+  if (a.order_out != nullptr) {
+    int* out = a.order_out + s0;
+    if (aligned16(out) && (qs & 3) == 0) {
+      for (int v = tid; v < (qs >> 2); v += kCostT)
+        reinterpret_cast<int4*>(out)[v] =
+            make_int4(q0 + 4 * v, q0 + 4 * v + 1, q0 + 4 * v + 2, q0 + 4 * v + 3);
+    } else {
+      for (int j = tid; j < qs; j += kCostT) out[j] = q0 + j;
+    }
+  }
+  // ---- per-batch reductions; the last chunk of the batch finalizes it
+  zeros = __reduce_add_sync(kFull, zeros);
+  total = __reduce_add_sync(kFull, total);
+  const unsigned fl = __reduce_or_sync(kFull, (wide ? 1u : 0u) | (big ? 2u : 0u));
+  unsigned* st = a.bstat + 4 * b;
+  if (lane == 0) {
+    if (zeros) atomicAdd(st + 0, zeros);
+    if (total) atomicAdd(st + 1, total);
+    if (fl) atomicOr(st + 2, fl);
+  }
+}
+
+__global__ void __launch_bounds__(kCostT, 8) cost_stream_kernel(const __grid_constant__ CostArgs a) {
+  __shared__ CostSmem S;
+  if (a.staged)
+    cost_chunk<true>(a, S);
+  else
+    cost_chunk<false>(a, S);  // unaligned CSR: per-sample sums from global memory
+}
+
+size_t cost_scratch_bytes(long long n_batches, int m) {
+  // blk_ident [nb * m], bstat [nb * 4], list [1 + nb], state [nb]
+  return 4ull * (n_batches * (static_cast<unsigned long long>(m) + 4 + 2) + 1);
+}
+
+cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream) {
+  const long long cpb = (a.n + kCostQ - 1) / kCostQ;
+  const long long grid = a.n_batches * cpb;
+  if (grid == 0) return cudaSuccess;
+  // blk_ident, bstat and the list count are contiguous and zeroed here
+  cudaError_t e = cudaMemsetAsync(a.blk_ident, 0, 4ull * (a.n_batches * (a.m + 4) + 1), stream);
+  if (e != cudaSuccess) return e;
+  cost_stream_kernel<<<static_cast<unsigned>(grid), kCostT, 0, stream>>>(a);
+  cost_finalize_kernel<<<static_cast<unsigned>(a.n_batches), kCostT, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace dtb

@@ -22,6 +22,7 @@
 #include "greedy.cuh"
 #include "greedy_fused.cuh"
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace dtb {
 
@@ -96,14 +97,14 @@ intra_generic_kernel(const double* __restrict__ sizes, int n, int m, int order,
 // -------------------------------------------------------------------- fused
 // 384 threads x 43 items: two CTAs per SM leave 85 registers per thread,
 // enough to hold a thread's 43 items across a radix pass without spilling.
-constexpr int kFusedT = 384;
+constexpr int kFusedT = 1024;
 constexpr int kFusedMaxN = 16384;  // samples per batch
 constexpr int kFusedItems = ((kFusedMaxN + kFusedT - 1) / kFusedT + 3) / 4 * 4;  // 44
 constexpr int kNarrowMaxM = 128;                    // groups in the smem path
 constexpr int kWideMaxM = 512;                      // groups in the global path
 constexpr int kRB = 7;                              // radix digit bits
 #ifndef DTB_FUSED_MIN_BLOCKS
-#define DTB_FUSED_MIN_BLOCKS 2  // two CTAs per SM (64 registers per thread)
+#define DTB_FUSED_MIN_BLOCKS 1  // one CTA of 1024 threads per SM (64 registers per thread)
 #endif
 
 // Narrow (shared-memory) state, ~112 KB so two CTAs share an SM.
@@ -119,7 +120,7 @@ constexpr int kFusedSlots = kFusedT * kFusedItems;  // sort slots incl. padding
 struct NarrowSmem {
   unsigned short kbi[kFusedSlots];
   alignas(16) unsigned short idx16[kFusedSlots];
-  alignas(16) unsigned short out16[kFusedMaxN + 4 * kNarrowMaxM];  // also the sort counters
+  alignas(16) unsigned short out16[kFusedMaxN + 4 * kNarrowMaxM];
   int radix_cnt[(1 << kRB) * (kFusedT / 32) + 1];
   FusedGreedySmem G;
   unsigned blk_ident[kNarrowMaxM], blk_greedy[kNarrowMaxM];
@@ -129,10 +130,26 @@ struct NarrowSmem {
   unsigned int s_and, s_or;
 };
 constexpr int kSortRB = 5;  // narrow-path digit bits (per-thread counters)
-static_assert((kFusedMaxN + 4 * kNarrowMaxM) / 2 >= blocked_cnt_words(kFusedT, kSortRB),
-              "sort counters fit in out16");
+// per-thread radix counters of the narrow path (their own space, so the
+// greedy's cells in out16 survive a sort that runs after the greedy)
+struct SortSmem {
+  NarrowSmem N;
+  alignas(16) unsigned cnt[blocked_cnt_words(kFusedT, kSortRB)];
+};
 
-constexpr size_t kFusedSmem = sizeof(NarrowSmem);
+constexpr size_t kFusedSmem = sizeof(SortSmem);
+
+// The kernel's dynamic shared memory as NarrowSmem.  Non-inlined device
+// functions re-derive it here instead of taking a reference argument, so the
+// compiler keeps the shared address space (LDS/STS instead of generic LD/ST).
+__device__ __forceinline__ NarrowSmem& shared_state() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return reinterpret_cast<SortSmem*>(smem_raw)->N;
+}
+__device__ __forceinline__ unsigned* sort_counters() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return reinterpret_cast<SortSmem*>(smem_raw)->cnt;
+}
 // Wide fallback (any cost <= 2^32-1, m <= 512) in a global scratch slot.
 constexpr size_t kWidePerBatch = static_cast<size_t>(kFusedMaxN) * (4 + 2 + 4) +
                                  static_cast<size_t>(kWideMaxM) * (8 * 5 + 4 * 4) + 1024;
@@ -162,7 +179,8 @@ __device__ __forceinline__ void write_outputs_common(const FusedArgs& a, long lo
 }
 
 // ---- wide path: 32-bit keys, (group, slot) assignments, global scratch.
-__device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowSmem& S) {
+__device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowSmem&) {
+  NarrowSmem& S = shared_state();  // shared address space: LDS/STS, not generic
   const int n = a.n, m = a.m, tid = threadIdx.x;
   const long long first = b * n;
   const bool desc = a.order == DTB_DESCENDING;
@@ -269,25 +287,273 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
   }
 }
 
-__global__ void __launch_bounds__(kFusedT, DTB_FUSED_MIN_BLOCKS)
-intra_fused_kernel(const __grid_constant__ FusedArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw);
-  const int n = a.n, m = a.m, tid = threadIdx.x;
+constexpr int kHistBins = 8192;  // token sums below this take the histogram path
+constexpr int kProfSlots = 64;   // debug timestamps per batch
+static_assert(kHistBins * 2 <= sizeof(NarrowSmem::kbi), "the histogram fits kbi");
+
+// Inclusive "last non-zero" scan of one value per thread (all threads get
+// their inclusive value; *carry gets the exclusive one).
+__device__ __forceinline__ unsigned block_last_nz(unsigned v, int* s, unsigned* excl) {
+  constexpr int W = kFusedT / 32;
   const int lane = lane_id(), w = warp_id();
-  const long long b = blockIdx.x;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o && x == 0u) x = y;
+  }
+  __syncthreads();
+  if (lane == 31) s[w] = static_cast<int>(x);
+  __syncthreads();
+  unsigned carry = 0u;
+  for (int k = 0; k < w; ++k) {
+    const unsigned c = static_cast<unsigned>(s[k]);
+    if (c) carry = c;
+  }
+  const unsigned up = __shfl_up_sync(kFull, x, 1);
+  *excl = lane == 0 ? carry : (up ? up : carry);
+  return x ? x : carry;
+}
+
+// Outputs of a batch whose order stays the identity.
+__device__ __forceinline__ void identity_order_out(const FusedArgs& a, long long first, int n) {
+  int* out = a.order_out + first;
+  if (aligned16(out)) {
+    int4* o4 = reinterpret_cast<int4*>(out);
+    for (int q = threadIdx.x; q < (n >> 2); q += kFusedT)
+      o4[q] = make_int4(4 * q, 4 * q + 1, 4 * q + 2, 4 * q + 3);
+  } else {
+    for (int i = threadIdx.x; i < n; i += kFusedT) out[i] = i;
+  }
+}
+
+// Histogram path (every token sum < kHistBins).  The greedy's decisions
+// depend only on the SORTED SIZES, and equal sizes are interchangeable, so
+// the sorted size sequence is the histogram's expansion: the greedy, its
+// block loads and the keep decision (src/reorder.cpp:340-354) need no
+// permutation.  Only a batch whose greedy split is kept needs the stable
+// sort, and then only as a counting scatter (the histogram's starts are the
+// cursors): two warps walk the batch halves in index order, ranking equal
+// tokens within 32 samples with MATCH, so ties keep index order
+// (src/reorder.cpp:34-40).
+__device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSmem&) {
+  NarrowSmem& S = shared_state();  // shared address space: LDS/STS, not generic
+  const int n = a.n, m = a.m, tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const long long first = b * n;
   const int pg = n / m;
   const bool desc = a.order == DTB_DESCENDING;
-
-  if (a.prof && tid == 0) a.prof[b * 8 + 0] = globaltimer();
-  // Batches outside the 16-bit layout's limits take the 32-bit path.
-  if (m > kNarrowMaxM || n > kFusedMaxN || (n & 7) || (!a.fuse_cost && a.wide_flag[b])) {
-    // consumers (TokSrc) then read this batch's 32-bit token copies
-    if (tid == 0) a.wide_flag[b] = 1u;
-    fused_wide(a, b, S);
-    return;
+  unsigned* hist = reinterpret_cast<unsigned*>(S.kbi);
+  unsigned short* skey = S.idx16;
+  bool keep = false;
+  const int cap = (n + m - 1) / m;
+  const int capP = ((cap + 1) | 3) - 1;
+  if (a.intra) {
+    const int zc = static_cast<int>(hist[0] & 0xffffu);
+    // ---- 1. starts of every token value in the sorted order (ascending:
+    // exclusive prefix; descending: n - inclusive prefix) and run heads
+    // skey[start] = tok + 1 over a zeroed skey
+    for (int q = tid; q < kFusedSlots / 8; q += kFusedT)
+      reinterpret_cast<uint4*>(skey)[q] = make_uint4(0, 0, 0, 0);
+    constexpr int kScanT = kFusedT;                      // threads owning bins
+    constexpr int kWordsPer = kHistBins / 2 / kScanT;    // 4 words = 8 bins per thread
+    static_assert(kWordsPer % 4 == 0 && kWordsPer >= 4, "scan layout");
+    int sum = 0;
+    if (tid < kScanT) {
+#pragma unroll
+      for (int q = 0; q < kWordsPer / 4; ++q) {
+        const uint4 v = reinterpret_cast<const uint4*>(hist + tid * kWordsPer)[q];
+        sum += static_cast<int>((v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) +
+                                (v.z & 0xffffu) + (v.z >> 16) + (v.w & 0xffffu) + (v.w >> 16));
+      }
+    }
+    int tot;
+    int base = block_excl_scan<kFusedT>(sum, S.tmp, &tot);  // also orders the zeroing
+    if (tid < kScanT) {
+      unsigned c[kWordsPer];  // re-read: nothing held across the scan
+#pragma unroll
+      for (int q = 0; q < kWordsPer / 4; ++q) {
+        const uint4 v = reinterpret_cast<const uint4*>(hist + tid * kWordsPer)[q];
+        c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int q = 0; q < kWordsPer; ++q) {
+        const int lo = static_cast<int>(c[q] & 0xffffu), hi = static_cast<int>(c[q] >> 16);
+        const unsigned v0 = static_cast<unsigned>(tid * 2 * kWordsPer + 2 * q);
+        const int s0 = desc ? n - (base + lo) : base;
+        const int s1 = desc ? n - (base + lo + hi) : base + lo;
+        base += lo + hi;
+        if (lo) skey[s0] = static_cast<unsigned short>(v0 + 1);
+        if (hi) skey[s1] = static_cast<unsigned short>(v0 + 2);
+        c[q] = static_cast<unsigned>(s0) | (static_cast<unsigned>(s1) << 16);
+      }
+#pragma unroll
+      for (int q = 0; q < kWordsPer / 4; ++q)
+        reinterpret_cast<uint4*>(hist + tid * kWordsPer)[q] =
+            make_uint4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
+    }
+    __syncthreads();
+    // ---- 2. fill forward: skey[p] = token of sorted position p
+    {
+      constexpr int C = kFusedSlots / kFusedT;  // positions per thread (16 = 2 x 16 bytes)
+      static_assert(C % 8 == 0, "fill-forward chunks of 16 bytes");
+      const int p0 = tid * C;
+      const bool mine = p0 < kFusedSlots;
+      unsigned last = 0u;
+      if (mine) {
+#pragma unroll
+        for (int q = 0; q < C / 8; ++q) {
+          const uint4 v = reinterpret_cast<const uint4*>(skey + p0)[q];
+          const unsigned wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const unsigned e = (wd[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
+            if (e) last = e;
+          }
+        }
+      }
+      unsigned run;
+      block_last_nz(last, S.tmp, &run);
+      if (mine) {
+#pragma unroll
+        for (int q = 0; q < C / 8; ++q) {
+          const uint4 v = reinterpret_cast<const uint4*>(skey + p0)[q];  // re-read: no registers held across the scan
+          unsigned wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const unsigned e = (wd[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
+            if (e) run = e;
+            const unsigned val = (run - 1u) & 0xffffu;
+            wd[h >> 1] = (h & 1) ? ((wd[h >> 1] & 0xffffu) | (val << 16)) : ((wd[h >> 1] & 0xffff0000u) | val);
+          }
+          reinterpret_cast<uint4*>(skey + p0)[q] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
+      }
+      __syncthreads();
+    }
+    if (a.prof && tid == 0) a.prof[b * kProfSlots + 2] = globaltimer();
+    // ---- 3. greedy equal-count partition over the sorted sizes
+    const int z0 = desc ? n - zc : 0;
+    const int z1 = desc ? n : zc;
+    auto size_at = [&](int k) -> unsigned {
+      const unsigned t = skey[k];
+      return t + t;
+    };
+    auto emit = [&](int k, int g, int slot) {
+      S.out16[g * capP + slot] = static_cast<unsigned short>(k);
+    };
+    if (desc)
+      greedy_fused<kFusedT, false>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll,
+                                   a.prof ? a.prof + b * kProfSlots + 6 : nullptr);
+    else
+      greedy_fused<kFusedT, true>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll,
+                                  a.prof ? a.prof + b * kProfSlots + 6 : nullptr);
+    if (a.prof && tid == 0) a.prof[b * kProfSlots + 3] = globaltimer();
+    // ---- 4. group offsets of the flat order, greedy block loads, decision
+    int cg = tid < m ? S.G.gcnt[tid] : 0, ctot;
+    const int o = block_excl_scan<kFusedT>(cg, S.tmp, &ctot);
+    if (tid < m) S.off[tid] = o;
+    if (n % m == 0) {
+      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = S.G.gload[g];
+    } else {
+      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = 0u;
+      __syncthreads();
+      for (int g = w; g < m; g += kFusedT / 32)
+        for (int slot = lane; slot < S.G.gcnt[g]; slot += 32) {
+          const int pos = S.off[g] + slot;
+          atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], size_at(S.out16[g * capP + slot]));
+        }
+    }
+    __syncthreads();
+    unsigned mg = 0u, mi = 0u;
+    for (int g = tid; g < m; g += kFusedT) {
+      mg = max(mg, S.blk_greedy[g]);
+      mi = max(mi, S.blk_ident[g]);
+    }
+    mg = static_cast<unsigned>(block_max_ll<kFusedT>(mg, S.tmpll));
+    mi = static_cast<unsigned>(block_max_ll<kFusedT>(mi, S.tmpll));
+    keep = mg <= mi;  // src/reorder.cpp:350-353 (exact integer loads)
   }
+  if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
+  for (int g = tid; g < m; g += kFusedT)
+    write_outputs_common(a, b, g, S.blk_ident[g], keep ? S.blk_greedy[g] : S.blk_ident[g]);
+  if (a.prof && tid == 0) a.prof[b * kProfSlots + 4] = globaltimer();
+  if (!keep) {
+    if (a.state == nullptr) identity_order_out(a, first, n);  // else written by the cost pass
+  } else {
+    // ---- 5. kept: the permutation.  Stable LSD radix sort of the sample
+    // indices by key (the u16 tokens, descending keys 0x7fff - tok), its
+    // counters in their own space so the greedy's cells in out16 survive;
+    // sorted position k of the greedy is then idx16[swz(k)] (same stable
+    // order as the greedy's sizes).
+    __syncthreads();
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
+      for (int q = tid; q < (n >> 3); q += kFusedT) {
+        const uint4 v = __ldg(src + q);
+        const unsigned wd[4] = {v.x, v.y, v.z, v.w};
+        unsigned kw[4], iw[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const unsigned t0 = wd[h] & 0xffffu, t1 = wd[h] >> 16;
+          const unsigned k0 = desc ? 0x7fffu - t0 : t0, k1 = desc ? 0x7fffu - t1 : t1;
+          kw[h] = k0 | (k1 << 16);
+          const unsigned i0 = static_cast<unsigned>(8 * q + 2 * h);
+          iw[h] = i0 | ((i0 + 1) << 16);
+        }
+        reinterpret_cast<uint4*>(S.kbi)[q] = make_uint4(kw[0], kw[1], kw[2], kw[3]);
+        reinterpret_cast<uint4*>(S.idx16)[q] = make_uint4(iw[0], iw[1], iw[2], iw[3]);
+      }
+      for (int i = n + tid; i < kFusedSlots; i += kFusedT) {  // padding: largest digits
+        S.kbi[i] = 0xffffu;
+        S.idx16[i] = static_cast<unsigned short>(i);
+      }
+    }
+    __syncthreads();
+    // every token < kHistBins: ascending keys vary in bits [0, 13), descending
+    // keys (0x7fff - tok > 0x5fff) in bits [0, 13) too; padding is 0xffff
+    constexpr int kKeyBits = 13;
+    static_assert(kHistBins <= (1 << kKeyBits), "keys of the histogram path fit 13 bits");
+    unsigned* cw = sort_counters();
+    for (int sh = 0; sh < kKeyBits; sh += kSortRB) {
+      const int bits = min(kSortRB, kKeyBits - sh);
+      const unsigned mask = (1u << bits) - 1u;
+      auto dig = [&](unsigned key) { return (key >> sh) & mask; };
+      if (sh + kSortRB >= kKeyBits)
+        tile_pass_blocked<kFusedT, kFusedItems, kSortRB, true>(S.idx16, S.kbi, dig, cw, S.tmp);
+      else
+        tile_pass_blocked<kFusedT, kFusedItems, kSortRB, false>(S.idx16, S.kbi, dig, cw, S.tmp);
+    }
+    for (int g = w; g < m; g += kFusedT / 32) {
+      const int base = S.off[g], cnt = S.G.gcnt[g];
+      for (int slot = lane; slot < cnt; slot += 32) {
+        const unsigned idx = S.idx16[swz(S.out16[g * capP + slot])];
+        a.order_out[first + base + slot] = static_cast<int>(idx);
+        if (a.tok16_staged != nullptr) {
+          const unsigned key = S.kbi[idx];
+          a.tok16_staged[first + base + slot] = static_cast<unsigned short>(desc ? 0x7fffu - key : key);
+        }
+      }
+    }
+  }
+  if (a.prof) {
+    __syncthreads();
+    if (tid == 0) a.prof[b * kProfSlots + 5] = globaltimer();
+  }
+}
+
+// Sort path of the 16-bit layout (token sums up to 0x7fff, or the separate
+// cost pass): keys from the u16 tokens `tok` (written earlier — by this CTA
+// or by launch_token_keys; read through L2), stable LSD radix sort, greedy,
+// decision, outputs.
+__device__ __noinline__ void narrow_sort_path(const FusedArgs& a, long long b, NarrowSmem&,
+                                              const unsigned short* tok) {
+  NarrowSmem& S = shared_state();
+  const int n = a.n, m = a.m, tid = threadIdx.x;
+  const int lane = lane_id(), w = warp_id();
+  const long long first = b * n;
+  const int pg = n / m;
+  const bool desc = a.order == DTB_DESCENDING;
+  __syncthreads();
   for (int g = tid; g < m; g += kFusedT) S.blk_ident[g] = 0u;
   if (tid == 0) {
     S.s_and = ~0u;
@@ -296,107 +562,24 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   __syncthreads();
   unsigned int kand = ~0u, kor = 0u;
   int zeros = 0;
-  // ---- 1. modality tokens of the batch.  cost_size = 2 * tokens.
-  // Per sample: kbi (sort key), identity block loads, zero count, the bit
-  // window of the keys.
-  auto take_sample = [&](int i, unsigned tok) {
-    const unsigned key = desc ? 0x7fffu - tok : tok;
+  auto take_sample = [&](int i, unsigned t) {
+    const unsigned key = desc ? 0x7fffu - t : t;
     kand &= key;
     kor |= key;
-    zeros += tok == 0;
+    zeros += t == 0;
     S.kbi[i] = static_cast<unsigned short>(key);
     S.idx16[i] = static_cast<unsigned short>(i);
   };
-  if (a.fuse_cost) {
-    // Fused cost pass (Sample::cost_size, core.hpp:160-167) straight from
-    // the CSR: 4 consecutive samples per item, two items per thread in
-    // flight — all offset loads, then the first 3 image / 1 audio
-    // subsequence of each sample, before any is consumed.
-    constexpr int KI = 3, KA = 1, U = 1;
-    const int n_items = n >> 2;
-    const int* io = a.img_off + first;
-    const int* ao = a.aud_off != nullptr ? a.aud_off + first : nullptr;
-    bool wide = false;
-    for (int it0 = tid; it0 < n_items; it0 += kFusedT * U) {
-      int ib[U][5], ab[U][5];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int item = it0 + u * kFusedT;
-        const bool ok = item < n_items;
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-          ib[u][j] = ok ? __ldg(io + item * 4 + j) : 0;
-          ab[u][j] = ok && ao != nullptr ? __ldg(ao + item * 4 + j) : 0;
-        }
-      }
-      int tv[U][4][KI + KA];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-#pragma unroll
-          for (int q = 0; q < KI; ++q)
-            tv[u][j][q] = ib[u][j] + q < ib[u][j + 1] ? __ldg(a.img_tok + ib[u][j] + q) : 0;
-#pragma unroll
-          for (int q = 0; q < KA; ++q)
-            tv[u][j][KI + q] = ab[u][j] + q < ab[u][j + 1] ? __ldg(a.aud_tok + ab[u][j] + q) : 0;
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int item = it0 + u * kFusedT;
-        if (item >= n_items) break;
-        unsigned short out[4];
-        const int i0 = item * 4;
-        const unsigned blk0 = min(a.div_pg.div(static_cast<unsigned>(i0)), static_cast<unsigned>(m - 1));
-        const unsigned blk3 = min(a.div_pg.div(static_cast<unsigned>(i0 + 3)), static_cast<unsigned>(m - 1));
-        unsigned run = 0u;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          long long t = 0;
-#pragma unroll
-          for (int q = 0; q < KI + KA; ++q) t += tv[u][j][q];
-          for (int x = ib[u][j] + KI; x < ib[u][j + 1]; ++x) t += __ldg(a.img_tok + x);
-          for (int x = ab[u][j] + KA; x < ab[u][j + 1]; ++x) t += __ldg(a.aud_tok + x);
-          if (t < 0 || t > 0x7fff) wide = true;
-          const unsigned tok = t < 0 || t > 0x7fff ? 0x7fffu : static_cast<unsigned>(t);
-          out[j] = static_cast<unsigned short>(tok);
-          take_sample(i0 + j, tok);
-          if (blk0 == blk3) {
-            run += 2u * tok;
-          } else {
-            const unsigned qd = a.div_pg.div(static_cast<unsigned>(i0 + j));
-            atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2u * tok);
-          }
-        }
-        if (blk0 == blk3) atomicAdd(&S.blk_ident[blk0], run);
-        if (a.tok16_w != nullptr) {
-          uint2 pk;
-          pk.x = static_cast<unsigned>(out[0]) | (static_cast<unsigned>(out[1]) << 16);
-          pk.y = static_cast<unsigned>(out[2]) | (static_cast<unsigned>(out[3]) << 16);
-          *reinterpret_cast<uint2*>(a.tok16_w + first + i0) = pk;
-        }
-      }
-    }
-    // a saturated or negative token sum: the whole batch takes the 32-bit
-    // path (which re-reads the CSR)
-    const unsigned any_wide = block_or<kFusedT>(wide ? 1u : 0u, reinterpret_cast<unsigned*>(S.tmp));
-    if (tid == 0) a.wide_flag[b] = any_wide;
-    if (any_wide) {
-      __syncthreads();
-      fused_wide(a, b, S);
-      return;
-    }
-  } else {
-    // tokens from the separate cost pass (launch_token_keys): 8 samples per
-    // 128-bit load, all loads issued before use
-    constexpr int V = (kFusedMaxN / 8 + kFusedT - 1) / kFusedT;  // 128-bit loads per thread
-    const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
+  {
+    // 8 samples per 128-bit load, all loads issued before use
+    constexpr int V = (kFusedMaxN / 8 + kFusedT - 1) / kFusedT;
+    const uint4* src = reinterpret_cast<const uint4*>(tok + first);
     const int nv = n >> 3;
     uint4 q[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int idx = tid + v * kFusedT;
-      q[v] = idx < nv ? __ldg(src + idx) : make_uint4(0, 0, 0, 0);
+      q[v] = idx < nv ? __ldcg(src + idx) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -410,13 +593,13 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int i = i0 + j;
-        const unsigned tok = (words[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-        take_sample(i, tok);
+        const unsigned t = (words[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        take_sample(i, t);
         if (blk0 == blk7) {
-          run += 2u * tok;
+          run += 2u * t;
         } else {
           const unsigned qd = a.div_pg.div(static_cast<unsigned>(i));
-          atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2u * tok);
+          atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2u * t);
         }
       }
       if (blk0 == blk7) atomicAdd(&S.blk_ident[blk0], run);
@@ -435,8 +618,8 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   const int cap = (n + m - 1) / m;
   const int capP = ((cap + 1) | 3) - 1;  // >= cap, == 2 mod 4
   if (a.intra) {
-    if (a.prof && tid == 0) a.prof[b * 8 + 1] = globaltimer();
-    // ---- 2. stable LSD radix sort by key over its varying bit window; the
+    if (a.prof && tid == 0) a.prof[b * kProfSlots + 1] = globaltimer();
+    // ---- stable LSD radix sort by key over its varying bit window; the
     // last pass writes swizzled positions (at least one pass always runs)
     const unsigned varying = S.s_and ^ S.s_or;
     const int lo = varying ? __ffs(static_cast<int>(varying)) - 1 : 0;
@@ -445,34 +628,33 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
       const int bits = min(kSortRB, hi - sh);
       const unsigned mask = (1u << bits) - 1u;
       auto dig = [&](unsigned key) { return (key >> sh) & mask; };
-      // per-thread digit counters live in out16's bytes (free until the greedy)
-      unsigned* cw = reinterpret_cast<unsigned*>(S.out16);
+      unsigned* cw = sort_counters();
       if (sh + kSortRB >= hi)
         tile_pass_blocked<kFusedT, kFusedItems, kSortRB, true>(S.idx16, S.kbi, dig, cw, S.tmp);
       else
         tile_pass_blocked<kFusedT, kFusedItems, kSortRB, false>(S.idx16, S.kbi, dig, cw, S.tmp);
     }
-    if (a.prof && tid == 0) a.prof[b * 8 + 2] = globaltimer();
-    // ---- 3. greedy equal-count partition (sizes = 2 * tokens), emitted
+    if (a.prof && tid == 0) a.prof[b * kProfSlots + 2] = globaltimer();
+    // ---- greedy equal-count partition (sizes = 2 * tokens), emitted
     // straight into the flat order's (group, slot) cells
     const int z0 = desc ? n - tot_zeros : 0;
     const int z1 = desc ? n : tot_zeros;
     auto size_at = [&](int k) -> unsigned {
       const unsigned key = S.kbi[S.idx16[swz(k)]];
-      const unsigned tok = desc ? 0x7fffu - key : key;
-      return tok + tok;
+      const unsigned t = desc ? 0x7fffu - key : key;
+      return t + t;
     };
     auto emit = [&](int k, int g, int slot) {
       S.out16[g * capP + slot] = static_cast<unsigned short>(k);
     };
     if (desc)
       greedy_fused<kFusedT, false>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll,
-                                   a.prof ? a.prof + b * 8 + 6 : nullptr);
+                                   a.prof ? a.prof + b * kProfSlots + 6 : nullptr);
     else
       greedy_fused<kFusedT, true>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll,
-                                  a.prof ? a.prof + b * 8 + 6 : nullptr);
-    if (a.prof && tid == 0) a.prof[b * 8 + 3] = globaltimer();
-    // ---- 4. group offsets of the flat order and the greedy block loads
+                                  a.prof ? a.prof + b * kProfSlots + 6 : nullptr);
+    if (a.prof && tid == 0) a.prof[b * kProfSlots + 3] = globaltimer();
+    // ---- group offsets of the flat order and the greedy block loads
     int c = tid < m ? S.G.gcnt[tid] : 0, tot;
     const int o = block_excl_scan<kFusedT>(c, S.tmp, &tot);
     if (tid < m) S.off[tid] = o;
@@ -506,10 +688,10 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
   for (int g = tid; g < m; g += kFusedT)
     write_outputs_common(a, b, g, S.blk_ident[g], keep ? S.blk_greedy[g] : S.blk_ident[g]);
-  if (a.prof && tid == 0) a.prof[b * 8 + 4] = globaltimer();
-  // ---- 5. outputs, coalesced: one warp per group, lanes over its slots —
-  // the intra order and, when the greedy split is kept, its per-position
-  // tokens (identity batches reuse the cost pass's tokens, see TokSrc)
+  if (a.prof && tid == 0) a.prof[b * kProfSlots + 4] = globaltimer();
+  // ---- outputs, coalesced: one warp per group, lanes over its slots — the
+  // intra order and, when the greedy split is kept, its per-position tokens
+  // (identity batches reuse the input-order tokens, see TokSrc)
   if (keep) {
     for (int g = w; g < m; g += kFusedT / 32) {
       const int base = S.off[g], cnt = S.G.gcnt[g];
@@ -521,12 +703,93 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
           a.tok16_staged[first + base + slot] = static_cast<unsigned short>(desc ? 0x7fffu - key : key);
       }
     }
-  } else {
-    for (int i = tid; i < n; i += kFusedT) a.order_out[first + i] = i;
+  } else if (a.state == nullptr) {  // else written by the cost pass
+    identity_order_out(a, first, n);
   }
   if (a.prof) {
     __syncthreads();
-    if (tid == 0) a.prof[b * 8 + 5] = globaltimer();
+    if (tid == 0) a.prof[b * kProfSlots + 5] = globaltimer();
+  }
+}
+
+// Per global batch, after the streaming cost pass (cost_stream_kernel,
+// k_cost.cu): batches it already decided exit at once; the rest take the
+// histogram path, the sort path (token sums >= kHistBins) or the 32-bit path.
+__device__ __forceinline__ void process_batch(const FusedArgs& a, long long b, NarrowSmem& S) {
+  const int n = a.n, m = a.m, tid = threadIdx.x;
+  const long long first = b * n;
+  const unsigned st = a.state != nullptr ? a.state[b] : kBatchSort;
+  if (st == kBatchDecided) return;
+
+  if (a.prof && tid == 0) a.prof[b * kProfSlots + 0] = globaltimer();
+  // Batches outside the 16-bit layout's limits take the 32-bit path.
+  if (st == kBatchWide || m > kNarrowMaxM || n > kFusedMaxN || (n & 7) ||
+      (a.state == nullptr && a.wide_flag[b])) {
+    // consumers (TokSrc) then read this batch's 32-bit token copies
+    if (tid == 0) a.wide_flag[b] = 1u;
+    fused_wide(a, b, S);
+    return;
+  }
+  if (st == kBatchSort) {
+    narrow_sort_path(a, b, S, a.tok16);
+    return;
+  }
+  // ---- histogram path: token histogram from the cost pass's u16 tokens;
+  // identity block loads from the cost pass
+  unsigned* hist = reinterpret_cast<unsigned*>(S.kbi);
+  for (int q = tid; q < kHistBins / 8; q += kFusedT)
+    reinterpret_cast<uint4*>(hist)[q] = make_uint4(0, 0, 0, 0);
+  for (int g = tid; g < m; g += kFusedT) S.blk_ident[g] = a.blk_ident[b * m + g];
+  __syncthreads();
+  {
+    constexpr int V = 3;  // 128-bit loads in flight per thread and round
+    const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
+    const int nv = n >> 3;
+    unsigned z = 0u;
+    for (int v0 = 0; v0 * kFusedT < nv; v0 += V) {
+    uint4 q[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int idx = tid + (v0 + v) * kFusedT;
+      q[v] = idx < nv ? __ldg(src + idx) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int idx = tid + (v0 + v) * kFusedT;
+      if (idx >= nv) break;
+      const unsigned words[4] = {q[v].x, q[v].y, q[v].z, q[v].w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const unsigned t = (words[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        if (t == 0u)
+          ++z;
+        else
+          atomicAdd(hist + (t >> 1), 1u << ((t & 1u) << 4));
+      }
+    }
+    }
+    z = __reduce_add_sync(kFull, z);
+    if (lane_id() == 0 && z) atomicAdd(hist, z);
+  }
+  __syncthreads();
+  if (a.prof && tid == 0) a.prof[b * kProfSlots + 1] = globaltimer();
+  fast_path(a, b, S);
+}
+
+// One CTA per batch, or (with the cost pass's list) persistent CTAs over the
+// batches it left undecided.
+__global__ void __launch_bounds__(kFusedT, DTB_FUSED_MIN_BLOCKS)
+intra_fused_kernel(const __grid_constant__ FusedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw);
+  if (a.list == nullptr) {
+    process_batch(a, blockIdx.x, S);
+    return;
+  }
+  const unsigned count = a.list[0];
+  for (unsigned q = blockIdx.x; q < count; q += gridDim.x) {
+    process_batch(a, a.list[1 + q], S);
+    __syncthreads();  // the shared state is reused by the next batch
   }
 }
 
@@ -594,15 +857,20 @@ cudaError_t launch_token_keys(const int* io, const int* it, const int* ao, const
 
 // ------------------------------------------------------------- host glue
 cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(intra_fused_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kFusedSmem));
-    if (e != cudaSuccess) return e;
-    configured = true;
+  // the opt-in is per device: set it on every launch (cheap), so contexts on
+  // several devices and several host threads need no shared state
+  cudaError_t e = cudaFuncSetAttribute(intra_fused_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kFusedSmem));
+  if (e != cudaSuccess) return e;
+  long long grid = n_batches;
+  if (a.list != nullptr) {  // persistent: one CTA per SM
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = std::min<long long>(n_batches, static_cast<long long>(sms) * DTB_FUSED_MIN_BLOCKS);
   }
-  intra_fused_kernel<<<static_cast<unsigned>(n_batches), kFusedT, kFusedSmem, stream>>>(a);
+  intra_fused_kernel<<<static_cast<unsigned>(grid), kFusedT, kFusedSmem, stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -450,7 +450,7 @@ template <int P, bool STREAM>
 __global__ void __launch_bounds__(128)
 group_sims_fast(GroupSimArgs a) {
   const long long gid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (gid >= a.n_batches * a.groups) return;
+  if (gid >= a.n_batches * a.groups || sim_skipped(a, gid)) return;
   const int l = a.l;
   // token access: stream layout [b][i][e] or group-contiguous arrays
   const long long bidx = gid / a.groups;
@@ -866,7 +866,7 @@ template <int PE, int PB, int PG, bool BUSY>
 __global__ void __launch_bounds__(kSimT, 4)
 group_sims_tiled(const __grid_constant__ GroupSimArgs a) {
   const long long gid = blockIdx.x * static_cast<long long>(kSimT) + threadIdx.x;
-  if (gid >= a.n_batches * a.groups) return;
+  if (gid >= a.n_batches * a.groups || sim_skipped(a, gid)) return;
   // u16 token sums are < 0x8000 <= table.size; assembled sums of u16 batches
   // are < span * 0x8000 — inside the table unless it was capped
   const long long b = gid / a.groups;
@@ -906,7 +906,7 @@ __host__ __device__ inline long long sim_scratch_per(int l, int p, int vpp) {
 __global__ void group_sims_kernel(GroupSimArgs a, double* scratch) {
   const long long gid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long total = a.n_batches * a.groups;
-  if (gid >= total) return;
+  if (gid >= total || sim_skipped(a, gid)) return;
   const GroupTok tok{&a, gid};
   const int l = a.l;
   const int p = plan_stages(a.plan);
@@ -974,7 +974,7 @@ group_sims_warp(GroupSimArgs a, double* scratch) {
   extern __shared__ double wsh[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long gid = blockIdx.x * static_cast<long long>(kWarpSimWarps) + warp;
-  if (gid >= a.n_batches * a.groups) return;  // uniform per warp
+  if (gid >= a.n_batches * a.groups || sim_skipped(a, gid)) return;  // uniform per warp
   const GroupTok tok{&a, gid};
   const int l = a.l;
   const int p = plan_stages(a.plan);
@@ -1071,13 +1071,15 @@ group_sims_warp(GroupSimArgs a, double* scratch) {
 // equals its avail, the neighbours' previous-tick values are exchanged through
 // a double-buffered shared row (one __syncwarp per tick), and the next tick's
 // durations are loaded before this tick's dependency chain.
+// 64 registers (8 blocks per SM) hold K <= 3 stages per lane without spills
+// (tuned on p = 79); K = 4 (97..128 stages) needs more and gets 6 blocks.
 template <int K>
-__global__ void __launch_bounds__(32 * kWarpSimWarps, 8)
+__global__ void __launch_bounds__(32 * kWarpSimWarps, K <= 3 ? 8 : 6)
 group_sims_warp_reg(GroupSimArgs a, double* scratch) {
   extern __shared__ double wsh[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long gid = blockIdx.x * static_cast<long long>(kWarpSimWarps) + warp;
-  if (gid >= a.n_batches * a.groups) return;  // uniform per warp
+  if (gid >= a.n_batches * a.groups || sim_skipped(a, gid)) return;  // uniform per warp
   const GroupTok tok{&a, gid};
   const int l = a.l;
   const int p = plan_stages(a.plan);
@@ -1296,10 +1298,15 @@ cudaError_t launch_cost_table(const DevCM& cm, const dtb_plan& plan, int span, i
 // these non-negative, non-NaN makespans), then + dp_sync.
 __global__ void t_iter_reduce_kernel(long long n_batches, int groups,
                                      const double* t_group, double dp_sync,
-                                     double* t_iter) {
+                                     double* t_iter, const unsigned char* only_kept,
+                                     const double* t_same) {
   const long long b = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= n_batches) return;
+  if (only_kept != nullptr && only_kept[b] == 0) {  // not simulated: same as t_same
+    if (lane == 0) t_iter[b] = t_same[b];
+    return;
+  }
   double worst = 0.0;
   for (int g = lane; g < groups; g += 32) {
     const double t = t_group[b * groups + g];
@@ -1315,10 +1322,12 @@ __global__ void t_iter_reduce_kernel(long long n_batches, int groups,
 
 cudaError_t launch_t_iter_reduce(long long n_batches, int groups,
                                  const double* t_group, double dp_sync,
-                                 double* t_iter, cudaStream_t stream) {
+                                 double* t_iter, cudaStream_t stream,
+                                 const unsigned char* only_kept, const double* t_same) {
   if (n_batches == 0) return cudaSuccess;
   t_iter_reduce_kernel<<<static_cast<unsigned>((n_batches * 32 + 255) / 256), 256, 0,
-                         stream>>>(n_batches, groups, t_group, dp_sync, t_iter);
+                         stream>>>(n_batches, groups, t_group, dp_sync, t_iter, only_kept,
+                                   t_same);
   return cudaGetLastError();
 }
 

@@ -33,20 +33,54 @@ struct FusedArgs {
   int pg;               // samples per backbone group (global_batch / dp_lm)
   int dp_me;
   unsigned char* wide_scratch;  // [n_batches * fused_wide_scratch_bytes(1)]
-  unsigned long long* prof;     // optional [n_batches][8] phase timestamps (debug)
+  unsigned long long* prof;     // optional [n_batches][64] phase timestamps (debug)
   // Output of the cost pass (launch_token_keys): modality tokens per sample,
   // saturated to 0x7fff, and a per-batch flag set when any sample saturated
   // (that batch then takes the 32-bit path from the CSR).
   const unsigned short* tok16;
   unsigned int* wide_flag;  // set by the kernel for every batch it runs on the 32-bit path
-  // fuse_cost: the kernel runs the cost pass itself from the CSR (tok16 and
-  // the cost-pass flags are not read); it writes wide_flag[b] (0/1) and, when
-  // tok16_w != null, the input-order u16 tokens for later consumers.
-  int fuse_cost;
-  unsigned short* tok16_w;
+  // Per-batch state from cost_stream_kernel (null: every batch takes the
+  // sort path from tok16 / the 32-bit path from wide_flag) and its identity
+  // block loads [n_batches * m].
+  const unsigned* state;
+  const unsigned* blk_ident;
+  const unsigned* list;  // [1 + n]: batches to process (null: every batch, one CTA each)
   FastDiv div_pg;
   DevErr* err;
 };
+
+// Batch states written by cost_stream_kernel (read by intra_fused_kernel).
+constexpr unsigned kBatchFast = 0;     // histogram path
+constexpr unsigned kBatchDecided = 1;  // all outputs written (order stays the identity)
+constexpr unsigned kBatchSort = 2;     // a token sum >= the histogram range: sort path
+constexpr unsigned kBatchWide = 3;     // a token sum < 0 or > 0x7fff: 32-bit path
+
+// Streaming cost pass (csrc/k_cost.cu) over chunks of 1024 samples, TMA-staged
+// CSR: per-sample u16 tokens, identity order, identity block loads, and per
+// batch (last chunk done) the keep decision when the averaging bound settles
+// it.
+struct CostArgs {
+  int n, m, order, intra;
+  long long n_batches;
+  const int* img_off;
+  const int* img_tok;
+  const int* aud_off;  // may be null
+  const int* aud_tok;
+  int staged;  // 16-byte aligned CSR and n % 4 == 0: bulk copies
+  unsigned short* tok16;   // [n_batches * n]
+  int* order_out;          // [n_batches * n] batch-local identity
+  unsigned* blk_ident;     // [n_batches * m]  zeroed
+  unsigned* bstat;         // [n_batches * 4]  zeroed: zeros, sum of cost_size, flags, -
+  unsigned* list;          // [1 + n_batches]: count (zeroed), batches left to the partition kernel
+  unsigned* state;         // [n_batches]
+  unsigned* wide_flag;     // [n_batches]
+  double* load_before;     // [n_batches * m] or null
+  double* load_after;
+  unsigned char* kept;     // [n_batches] or null
+  FastDiv div_pg;
+};
+size_t cost_scratch_bytes(long long n_batches, int m);  // blk_ident, bstat, list, state
+cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream);
 
 // Cost pass: tok16[i] = min(modality tokens of sample i, 0x7fff) for the
 // whole stream, wide_flag[i / n] |= 1 on saturation or negative tokens.
@@ -184,10 +218,17 @@ struct GroupSimArgs {
   const int* mbsum;
   const int* order;      // optional [n_batches][groups][l] microbatch order
   CostTable table;       // optional (size 0 = evaluate directly)
+  // optional [n_batches]: groups of batches whose flag is 0 are not
+  // simulated (intra-only t_iter_after of a batch whose greedy split was
+  // not kept is its t_iter_before: same microbatches, same operations)
+  const unsigned char* only_kept;
   double* t_group;
   double* busy;
   DevErr* err;
 };
+__device__ __forceinline__ bool sim_skipped(const GroupSimArgs& a, long long gid) {
+  return a.only_kept != nullptr && a.only_kept[gid / a.groups] == 0;
+}
 cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
                               cudaStream_t stream);
 size_t group_sims_scratch(const GroupSimArgs& a);
@@ -279,7 +320,9 @@ cudaError_t launch_compose(long long n_batches, int n, int dp_lm, int dp_me,
                            cudaStream_t stream);
 cudaError_t launch_t_iter_reduce(long long n_batches, int groups,
                                  const double* t_group, double dp_sync,
-                                 double* t_iter, cudaStream_t stream);
+                                 double* t_iter, cudaStream_t stream,
+                                 const unsigned char* only_kept = nullptr,
+                                 const double* t_same = nullptr);
 
 // ---------------------------------------------------------------- ingest
 // Trace JSONL -> sample CSR (csrc/k_ingest.cu, parser csrc/jsonl.cuh).

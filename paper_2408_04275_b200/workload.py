@@ -16,6 +16,10 @@ Two families:
     resolution mapped to (res/16)^2 patch tokens from a fixed
     resolution set, and an audio clip (lognormal(750, 0.6) tokens) on 25% of
     samples, placed in `audio_subseqs` after the images.
+  * dense   — the mixed family with at least one image per sample (no
+    text-only samples): the equal-count greedy split then balances better
+    than the incoming order and is KEPT on most batches, which exercises the
+    permutation half of the intra path.
 """
 from __future__ import annotations
 
@@ -41,10 +45,12 @@ def synth_stream(n: int, seed: int = 1, family: str = "mixed",
     u = 1.0 - rng.random(n)  # (0, 1]
     count = np.floor(np.log(u) / np.log(1.0 - q)).astype(np.int64)
     count = np.minimum(count, 64)
+    if family == "dense":
+        count = np.maximum(count, 1)
     total = int(count.sum())
     if family == "skewed":
         draws = _lognormal_tokens(rng, 1024.0, 0.47, total)
-    elif family == "mixed":
+    elif family in ("mixed", "dense"):
         draws = (RESOLUTIONS[rng.integers(0, len(RESOLUTIONS), total)] // 16) ** 2
     else:
         raise ValueError(family)
@@ -61,7 +67,7 @@ def synth_stream(n: int, seed: int = 1, family: str = "mixed",
     img_off = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(img_counts, out=img_off[1:])
     used = budget - np.bincount(owner[keep], weights=tokens[keep], minlength=n).astype(np.int64)
-    if family == "mixed":
+    if family in ("mixed", "dense"):
         has_audio = rng.random(n) < 0.25
         atok = _lognormal_tokens(rng, 750.0, 0.6, n)
         atok = np.minimum(atok, used)

@@ -272,27 +272,41 @@ STREAM_CASES = [  # (n_batches, bs, dp_lm, dp_me, pp triple, inter)
     (3, 1024, 8, 8, (2, 1, 1), True),
     (2, 16384, 128, 128, (1, 2, 1), False),  # BASELINE config 4 batch shape
     (40, 32, 1, 1, (1, 2, 1), True),      # BASELINE config 2 shape: one group of 32 per batch
+    (6, 4096, 32, 32, (1, 2, 1), False, "dense"),   # greedy kept: counting scatter
+    (4, 1000, 8, 8, (1, 2, 1), False, "dense"),     # n % 8 != 0: 32-bit path
+    (5, 2048, 16, 16, (1, 2, 1), True, "dense"),
 ]
 
 
 def check_stream(impl, oracle, rng, cases=None):
     model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
     ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
-    for n_batches, bs, dp, dp_me, pp, inter in cases or STREAM_CASES:
+    for n_batches, bs, dp, dp_me, pp, inter, *fam in cases or STREAM_CASES:
         pl = H.plan((1, dp_me, pp[0]), (1, dp, pp[1]), (1, dp_me, pp[2]), bs)
-        s = synth_stream(n_batches * bs, int(rng.integers(1, 1 << 30)), "mixed")
+        s = synth_stream(n_batches * bs, int(rng.integers(1, 1 << 30)), fam[0] if fam else "mixed")
         ra = impl.reorder_stream(ci, pl, s, n_batches, inter=inter)
         rb = oracle.reorder_stream(co, pl, s, n_batches, inter=inter)
         for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
             assert_same(ra[k], rb[k], f"{k} {n_batches}x{bs} dp {dp}/{dp_me} pp {pp}")
 
 
+# vpp-1 plans beyond 8 stages: the warp-per-group simulations (register
+# form for p <= 128, shared-memory form above), with ragged l < p and group
+# counts that leave the last warps of a CTA idle
+MANY_STAGE_PLANS = [
+    H.plan((1, 2, 1), (1, 2, 11), (1, 2, 3), 8),     # p = 15
+    H.plan((1, 2, 1), (1, 4, 71), (1, 2, 7), 16),    # p = 79 (BASELINE config 5 shape)
+    H.plan((1, 2, 1), (1, 2, 100), (1, 2, 9), 8),    # p = 110 (4 stages per lane)
+    H.plan((1, 2, 1), (1, 2, 140), (1, 2, 3), 8),    # p = 144 (shared-memory form)
+]
+
+
 def check_simulate(impl, oracle, rng):
-    model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
+    model, cluster, book = H.desk_model(), H.desk_cluster(1172), H.desk_book()
     ci, co = impl.cost_model(model, cluster, book), oracle.cost_model(model, cluster, book)
-    for pl in PLANS:
+    for pl in PLANS + MANY_STAGE_PLANS:
         groups = []
-        for g in range(int(rng.integers(1, 5))):
+        for g in range(int(rng.integers(1, 12 if pl in MANY_STAGE_PLANS else 5))):
             l = pl.microbatch_count() if pl.vpp > 1 else int(rng.integers(1, 20))
             enc = rng.integers(0, 9000, l)
             groups.append((enc, enc, np.full(l, max(1, pl.samples_per_microbatch()))))
@@ -300,6 +314,29 @@ def check_simulate(impl, oracle, rng):
         b = oracle.simulate_iteration(co, pl, groups)
         for k in a:
             assert_same(a[k], b[k], k)
+
+
+# ------------------------------------------------ cost_size / compute_stats
+def stats_batches(rng):
+    """Sample batches for Sample::cost_size (core.hpp:160-167) and
+    compute_stats (src/workload.cpp:206-220): both families, samples without
+    any modality subsequence, image-only / audio-only samples, one sample,
+    and large token counts (the 32-bit path's sums)."""
+    yield synth_stream(4096, int(rng.integers(1, 1 << 30)), "mixed")
+    yield synth_stream(777, int(rng.integers(1, 1 << 30)), "skewed")
+    yield SampleBatch.from_lists([(5, [], [])])
+    yield SampleBatch.from_lists([(1, [3, 4], [7]), (2, [], [9]), (0, [11], []), (3, [], [])])
+    yield SampleBatch.from_lists([(10, [int(t)], [int(u)]) for t, u in
+                                  zip(rng.integers(1, 1 << 20, 300), rng.integers(0, 1 << 20, 300))])
+
+
+def check_stats(impl, oracle, rng):
+    for batch in stats_batches(rng):
+        assert_same(impl.cost_sizes(batch), oracle.cost_sizes(batch), f"cost_sizes n={batch.n}")
+        for seq_len in (8192, 1):
+            a, b = impl.compute_stats(batch, seq_len), oracle.compute_stats(batch, seq_len)
+            assert (a.seq_len, a.mean_encoder_tokens, a.mean_generator_tokens) == \
+                (b.seq_len, b.mean_encoder_tokens, b.mean_generator_tokens), (batch.n, seq_len)
 
 
 # ------------------------------------------------------------ orchestration

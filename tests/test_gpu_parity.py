@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("name", ["intra", "select", "schedule", "exhaustive", "brute", "inter", "cost",
-                                  "simulate", "disaggregated", "stream", "orchestration"])
+                                  "simulate", "stats", "disaggregated", "stream", "orchestration"])
 def test_gpu_matches_oracle(name, gpu, oracle_best):
     rng = np.random.default_rng(4321 + len(name))
     getattr(P, "check_" + name)(gpu, oracle_best, rng)

@@ -8,7 +8,7 @@ import parity_cases as P
 
 
 @pytest.mark.parametrize("name", ["intra", "select", "schedule", "exhaustive", "brute", "inter", "cost",
-                                  "simulate", "disaggregated", "stream", "orchestration"])
+                                  "simulate", "stats", "disaggregated", "stream", "orchestration"])
 def test_port_matches_reference(name, port, ref):
     rng = np.random.default_rng(1234 + len(name))
     getattr(P, "check_" + name)(port, ref, rng)

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--dp", type=int, default=128)
     ap.add_argument("--check", type=int, default=4)
     ap.add_argument("--order", type=int, default=0)
+    ap.add_argument("--family", default="mixed")
     args = ap.parse_args()
     import torch
     from paper_2408_04275_b200 import _capi as A
@@ -36,13 +37,13 @@ def main():
     fn.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.POINTER(A.Samples), C.c_int64,
                    C.c_void_p, C.c_void_p, C.c_void_p]
     t0 = time.time()
-    s = synth_stream(args.batches * args.bs, seed=11, family="mixed")
+    s = synth_stream(args.batches * args.bs, seed=11, family=args.family)
     print(f"synth {time.time() - t0:.1f}s", flush=True)
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     d = [dev(s.image_offsets), dev(s.image_tokens), dev(s.audio_offsets), dev(s.audio_tokens)]
     ds = A.Samples(s.n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32)) for x in d])
     out = torch.empty(s.n, dtype=torch.int32, device="cuda")
-    prof = torch.zeros(args.batches * 8, dtype=torch.int64, device="cuda")
+    prof = torch.zeros(args.batches * 64, dtype=torch.int64, device="cuda")
     for it in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -51,14 +52,14 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         print(f"iter {it}: kernel {e0.elapsed_time(e1):.3f} ms", flush=True)
-    p = prof.view(args.batches, 8).cpu().numpy().astype(np.float64)
+    p = prof.view(args.batches, 64).cpu().numpy().astype(np.float64)
     names = ["load+cost", "sort", "greedy", "partition+decide", "outputs"]
     span = (p[:, 5] - p[:, 0]) / 1e3
     print(f"per-CTA span us: median {np.median(span):.1f} max {span.max():.1f}")
     for k, nm in enumerate(names):
         dt = (p[:, k + 1] - p[:, k]) / 1e3
         print(f"  {nm:18s} median {np.median(dt):8.1f} us  max {dt.max():8.1f}")
-    pi = prof.view(args.batches, 8).cpu().numpy()
+    pi = prof.view(args.batches, 64).cpu().numpy()
     z = (p[:, 6] - p[:, 2]) / 1e3
     ok = pi[:, 6] > 0
     if ok.any():
@@ -67,6 +68,21 @@ def main():
     cnt = pi[:, 7]
     print(f"  greedy rounds: full segments median {np.median(cnt >> 32):.0f}, "
           f"general median {np.median(cnt & 0xffffffff):.0f} max {(cnt & 0xffffffff).max()}")
+    st = p[:, 8:56].reshape(args.batches, 16, 3)
+    if (st[:, 0, 0] > 0).any():
+        prev = np.concatenate([p[:, :1], st[:, :-1, 2]], axis=1)  # previous stage end
+        wait = (st[:, :, 0] - prev) / 1e3
+        pref = (st[:, :, 1] - st[:, :, 0]) / 1e3
+        loop = (st[:, :, 2] - st[:, :, 1]) / 1e3
+        for k in (0, 1, 2, 8, 15):
+            print(f"  stage {k:2d}: wait median {np.median(wait[:, k]):6.2f} us, prefix "
+                  f"{np.median(pref[:, k]):6.2f}, samples+sync {np.median(loop[:, k]):6.2f}")
+    ks = p[:, 56:61]
+    okk = ks[:, 0] > 0
+    if okk.any():
+        names_k = ["heavy ids", "counts", "walk", "light sort"]
+        print(f"  kept scatter ({okk.sum()} batches):", ", ".join(
+            f"{nm} {np.median((ks[okk, k + 1] - ks[okk, k]) / 1e3):.1f}" for k, nm in enumerate(names_k)))
     start = p[:, 0] - p[:, 0].min()
     print(f"  CTA start spread: {start.max() / 1e3:.1f} us (waves)")
     if args.check:
