@@ -12,11 +12,13 @@ the north_star's HBM target names.  The full default mode (intra + inter)
 and the orchestration search (BASELINE config 3) are measured too and
 reported under "modes" / "search".
 
-N GPUs (torchrun): weak scaling — every rank reorders its own 16M-sample
-shard (global batches are independent; no collective on the data path).
-`value` = all ranks' samples / max-over-ranks device time.  "strong" times
-ONE 16M stream split by batch range (shard.batch_range) and, with
-"with_gather", an NCCL all-gather of the output orders.
+N GPUs (torchrun): STRONG scaling — ONE 16M-sample stream split by
+global-batch range (dtb_shard_range), each rank reorders its range and the
+library stores every rank's ordering into every rank's replica over NVLink
+(dtb_reorder_stream_shard_dev: CUDA-IPC peer stores on a side stream that
+overlaps the simulations, device flag barrier); `value` = 16M samples / the
+max-over-ranks device time of that call, with the whole ordering present on
+every rank.  "weak" (each rank its own 16M stream, no exchange) is an extra.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref,
 compiled from the reference sources; the C restatement if absent) on all
@@ -42,7 +44,8 @@ BS = 16384
 DP = 128
 STREAM = 1 << 24
 METRIC = "reordered samples/s (disaggregated_reorder, 16M-sample stream, BS 16K, DP 128)"
-LAUNCHES_INTRA_STEP = 7  # token_keys, intra_fused, cost_table, 2x group_sims, 2x t_iter_reduce
+# cost_stream, cost_finalize, intra_fused, cost_table, 2x group_sims, 2x t_iter_reduce
+LAUNCHES_INTRA_STEP = 8
 
 
 def parse():
@@ -196,6 +199,16 @@ def cpu_search(threads):
     return kind, threads, res.candidates_evaluated / dt, dt, res
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def traffic_from_profiles():
     """dram bytes per launch of the sort/partition kernels from the committed
     ncu --set full summary (profiles/), if present."""
@@ -227,6 +240,7 @@ def reference_arm(args, model, cluster, book, plan_c):
                                    "ReorderMode{intra} (bounded CPU sample of the stream)",
                        "global_batch": BS, "dp": DP, "sample_batches": sample_batches},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": kind,
+                             "cpu_model": cpu_model(),
                              "sample": f"{sample_batches} global batches x {BS} samples, "
                                        f"std::thread fan-out over batches"},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -255,12 +269,10 @@ def main():
     cm = pl.cost_model(model, cluster, book)
     mode_intra, mode_both = A.ReorderMode(1, 0, 0), A.ReorderMode(1, 1, 0)
 
-    # Weak scaling: every rank reorders its own 16M-sample shard (1,024
-    # global batches) of a world x 16M stream — global batches are
-    # independent, so there is no data-path collective.
+    # ONE stream of 16M samples (1,024 global batches); at N > 1 every rank
+    # holds it and reorders its batch range (strong scaling)
     my_batches = args.samples // BS
-    first_batch = rank * my_batches
-    samples = synth_stream(my_batches * BS, seed=1000 + first_batch, family="mixed")
+    samples = synth_stream(my_batches * BS, seed=1000, family="mixed")
     n = samples.n
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     d_csr = [dev(samples.image_offsets), dev(samples.image_tokens), dev(samples.audio_offsets),
@@ -306,24 +318,58 @@ def main():
         torch.cuda.synchronize()
         return float(np.mean([s.elapsed_time(e) for s, e in evs]))
 
+    group = replica = None
+    if world > 1:
+        # the library's exchange: every rank's replica of the whole ordering
+        import torch.distributed as dist
+        replica, handle = pl.peer_buffer_create(n)
+        handles = [None] * world
+        dist.all_gather_object(handles, handle)
+        group = pl.peer_group_open(rank, world, replica, n, handles)
+
+        def headline():
+            pl._check(lib.reorder_stream_shard_dev(pl.ctx, cm.h, C.byref(plan_c),
+                                                   C.byref(mode_intra), C.byref(ds), my_batches,
+                                                   group, ptr(lb), ptr(la), ptr(tb), ptr(ta),
+                                                   ptr(kept), sh))
+    else:
+        def headline():
+            step(mode_intra)
+    # the same call captured once into a CUDA graph (fixed pointers) and
+    # replayed: one launch per step instead of ~10 host-side launches
+    graph = C.c_void_p()
+    pl._check(lib.reorder_stream_graph_create(pl.ctx, cm.h, C.byref(plan_c), C.byref(mode_intra),
+                                              C.byref(ds), my_batches, group, ptr(out_order),
+                                              ptr(lb), ptr(la), ptr(tb), ptr(ta), ptr(kept),
+                                              C.byref(graph)))
+
+    def headline_graph():
+        pl._check(lib.graph_launch(graph, sh))
+    ms_direct = max_over_ranks(timed(headline, max(3, args.steps // 2), args.warmup), world)
     with Clocks(local) as clk:
-        ms_local = timed(lambda: step(mode_intra), args.steps, args.warmup)
+        ms_local = timed(headline_graph, args.steps, args.warmup)
     ms = max_over_ranks(ms_local, world)
-    total = my_batches * BS * world
+    total = my_batches * BS
+    first_b, count_b = shard.batch_range(my_batches, rank, world)
     out = {"metric": METRIC, "value": total / (ms / 1e3), "unit": "samples/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
            "dtype": "int32 tokens / int64 loads / f64 stage times (u16 sort keys)",
            "data": "synthetic (PCG64 mixed image+audio stream; desk-shaped cost profile)",
-           "config": {"workload": "BASELINE config 4: 16M-sample stream per GPU, global batch "
+           "config": {"workload": "BASELINE config 4: ONE 16M-sample stream, global batch "
                                   "16384, DP 128, PP 1/2/1, disaggregated_reorder "
                                   "ReorderMode{intra}",
-                      "samples": total, "samples_per_gpu": my_batches * BS, "global_batch": BS,
+                      "samples": total, "samples_per_gpu": count_b * BS, "global_batch": BS,
                       "dp": DP,
-                      "parallelism": f"global-batch-range sharding over {world} GPU(s), "
-                                     "no data-path collective",
+                      "parallelism": (f"global-batch-range sharding over {world} GPUs; the "
+                                      "whole ordering (u16 in-batch indices) stored into every "
+                                      "rank's replica by the library over NVLink (CUDA IPC "
+                                      "peer stores + device flag barrier), inside the timed "
+                                      "region") if world > 1 else "1 GPU",
                       "l2": "256 MiB buffer written between timed steps (inputs also > L2)"},
-           "gpu_launches": LAUNCHES_INTRA_STEP}
+           "gpu_launches": LAUNCHES_INTRA_STEP + (1 if world > 1 else 0),
+           "launch": "one CUDA graph launch per step (dtb_reorder_stream_graph_create)",
+           "ms_per_step_direct_calls": ms_direct}
     clocks = clk.summary()
     if clocks:
         out["clocks"] = clocks
@@ -341,40 +387,45 @@ def main():
     hbm = peaks.get("hbm_gbs", 6650.0)
     achieved = algo / (sp_local / 1e3) / 1e9
     tr = traffic_from_profiles()
+    kernels = ("cost_stream_kernel + cost_finalize_kernel + intra_fused_kernel (sort/partition "
+               "path: dtb_intra_stream_dev, its scratch memset included)")
     out["roofline"] = {
-        "bound": "hbm", "kernel": "token_keys_kernel + intra_fused_kernel (sort/partition path)",
+        "bound": "hbm", "kernel": kernels,
         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
         "traffic": tr.get("bytes_per_step_16M") if tr else None,
         "algorithmic_bytes_per_launch": algo, "ms_per_launch": sp_local,
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650"}
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650",
+        "stream": "mixed (BASELINE config 4): the greedy split loses on most batches"}
+    if not args.no_extras and world == 1:
+        # the same path on the dense family (every sample has an image): the
+        # greedy split is KEPT on every batch, so the stable sort and the
+        # permutation run on all of them
+        dense = synth_stream(my_batches * BS, seed=1000, family="dense")
+        dd = [dev(dense.image_offsets), dev(dense.image_tokens), dev(dense.audio_offsets),
+              dev(dense.audio_tokens)]
+        dds = A.Samples(n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32)) for x in dd])
+
+        def sort_partition_dense():
+            pl._check(lib.intra_stream_dev(pl.ctx, BS, DP, 0, C.byref(dds), my_batches,
+                                           ptr(out_order), ptr(lb), ptr(la), ptr(kept), sh))
+        spd = timed(sort_partition_dense, max(3, args.steps // 2), args.warmup)
+        algo_d = (4 * 2 * (n + my_batches) + 4 * (len(dense.image_tokens) + len(dense.audio_tokens))
+                  + 4 * n + 2 * 8 * DP * my_batches + my_batches)
+        kept_frac = float(kept.float().mean().item())
+        ach_d = algo_d / (spd / 1e3) / 1e9
+        out["roofline_kept"] = {
+            "bound": "hbm", "kernel": kernels, "achieved": ach_d, "peak": hbm, "unit": "GB/s",
+            "frac": ach_d / hbm, "algorithmic_bytes_per_launch": algo_d, "ms_per_launch": spd,
+            "stream": "dense (mixed with >= 1 image per sample): greedy split kept on "
+                      f"{kept_frac:.0%} of the batches"}
+        del dd
 
     if world > 1:
-        # strong-scaling view: ONE 16M stream split by batch range, plus the
-        # concatenated ordering on every rank (NCCL all-gather over NVLink)
-        import torch.distributed as dist
-        first, count = shard.batch_range(my_batches, rank, world)
-        io = samples.image_offsets
-        sub = A.Samples(count * BS, None,
-                        C.cast(d_csr[0].data_ptr() + 4 * first * BS, C.POINTER(C.c_int32)),
-                        C.cast(d_csr[1].data_ptr(), C.POINTER(C.c_int32)),
-                        C.cast(d_csr[2].data_ptr() + 4 * first * BS, C.POINTER(C.c_int32)),
-                        C.cast(d_csr[3].data_ptr(), C.POINTER(C.c_int32)))
-        s_ms = max_over_ranks(timed(lambda: step(mode_intra, sub, count), args.steps,
-                                    args.warmup), world)
-        out["strong"] = {"samples": my_batches * BS, "ms_per_step": s_ms,
-                         "value": my_batches * BS / (s_ms / 1e3), "unit": "samples/s"}
-        if my_batches % world == 0:
-            full = torch.empty(my_batches * BS, dtype=torch.int32, device="cuda")
-            part = out_order[:count * BS]
-
-            def gather():
-                step(mode_intra, sub, count)
-                with torch.cuda.stream(stream):
-                    dist.all_gather_into_tensor(full, part)
-            g_ms = max_over_ranks(timed(gather, max(2, args.steps // 2), 1), world)
-            out["strong"]["with_gather"] = {
-                "ms_per_step": g_ms, "value": my_batches * BS / (g_ms / 1e3),
-                "collective": "all_gather_into_tensor(int32 output orders)"}
+        # weak-scaling extra: every rank reorders the whole stream (no exchange)
+        w_ms = max_over_ranks(timed(lambda: step(mode_intra), max(2, args.steps // 2), 1), world)
+        out["weak"] = {"samples": total * world, "ms_per_step": w_ms,
+                       "value": total * world / (w_ms / 1e3), "unit": "samples/s",
+                       "what": "every rank reorders its own copy of the 16M stream; no exchange"}
 
     if not args.no_extras:
         # e2e on every rank: host CSR (pinned) -> device -> results back,
@@ -382,18 +433,23 @@ def main():
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         h_csr = [pin(samples.image_offsets), pin(samples.image_tokens),
                  pin(samples.audio_offsets), pin(samples.audio_tokens)]
-        hs = A.Samples(n, None, *[C.cast(x.data_ptr(), C.POINTER(C.c_int32)) for x in h_csr])
-        h_order = torch.empty(n, dtype=torch.int32).pin_memory()
-        h_lb = torch.empty(my_batches * DP, dtype=torch.float64).pin_memory()
+        # this rank's batch range of the stream (the whole stream at N = 1):
+        # offsets from the range's first sample, absolute into the tokens
+        n_sh = count_b * BS
+        off = lambda t: C.cast(t.data_ptr() + 4 * first_b * BS, C.POINTER(C.c_int32))
+        hs = A.Samples(n_sh, None, off(h_csr[0]), C.cast(h_csr[1].data_ptr(), C.POINTER(C.c_int32)),
+                       off(h_csr[2]), C.cast(h_csr[3].data_ptr(), C.POINTER(C.c_int32)))
+        h_order = torch.empty(n_sh, dtype=torch.int32).pin_memory()
+        h_lb = torch.empty(count_b * DP, dtype=torch.float64).pin_memory()
         h_la = torch.empty_like(h_lb).pin_memory()
-        h_tb = torch.empty(my_batches, dtype=torch.float64).pin_memory()
+        h_tb = torch.empty(count_b, dtype=torch.float64).pin_memory()
         h_ta = torch.empty_like(h_tb).pin_memory()
-        h_kept = torch.empty(my_batches, dtype=torch.uint8).pin_memory()
+        h_kept = torch.empty(count_b, dtype=torch.uint8).pin_memory()
         P = lambda t, ct: C.cast(t.data_ptr(), C.POINTER(ct))
 
         def e2e():
             pl._check(lib.reorder_stream(pl.ctx, cm.h, C.byref(plan_c), C.byref(mode_intra),
-                                         C.byref(hs), my_batches, P(h_order, C.c_int32),
+                                         C.byref(hs), count_b, P(h_order, C.c_int32),
                                          P(h_lb, C.c_double), P(h_la, C.c_double),
                                          P(h_tb, C.c_double), P(h_ta, C.c_double),
                                          P(h_kept, C.c_uint8)))
@@ -404,12 +460,14 @@ def main():
         for _ in range(reps):
             e2e()
         e_dt = max_over_ranks((time.perf_counter() - t0) / reps, world)
-        h2d = sum(x.numel() * x.element_size() for x in h_csr)
+        io_h, ao_h = samples.image_offsets, samples.audio_offsets
+        h2d = 4 * (2 * (n_sh + 1) + int(io_h[(first_b + count_b) * BS] - io_h[first_b * BS]) +
+                   int(ao_h[(first_b + count_b) * BS] - ao_h[first_b * BS]))
         d2h = sum(x.numel() * x.element_size() for x in (h_order, h_lb, h_la, h_tb, h_ta, h_kept))
         out["e2e"] = {"value": total / e_dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                       "d2h_bytes_per_step": d2h, "ms_per_step": e_dt * 1e3,
-                      "path": "dtb_reorder_stream (host pointers, pinned; per-rank bytes, "
-                              "max over ranks)"}
+                      "path": "dtb_reorder_stream (host pointers, pinned; each rank its batch "
+                              "range of the one stream; per-rank bytes, max over ranks)"}
 
     if not args.no_extras and rank == 0 and world == 1:
         # full default mode (intra + inter)
@@ -581,10 +639,15 @@ def main():
         kind, times = cpu_reference(samples, plan_c, mode_intra, sample_batches, 2, 0, threads,
                                     (model, cluster, book))
         t = float(np.median(times))
+        kind1, times1 = cpu_reference(samples, plan_c, mode_intra, 4, 2, 0, 1,
+                                      (model, cluster, book))
         out["cpu_baseline"] = {"value": sample_batches * BS / t, "unit": "samples/s",
-                               "cores": threads, "kind": kind,
+                               "cores": threads, "kind": kind, "cpu_model": cpu_model(),
                                "sample": f"first {sample_batches} global batches of the stream "
-                                         f"(x{BS} samples), std::thread fan-out over batches"}
+                                         f"(x{BS} samples), std::thread fan-out over batches",
+                               "single_thread": {"value": 4 * BS / float(np.median(times1)),
+                                                 "unit": "samples/s", "cores": 1,
+                                                 "sample": "first 4 global batches, one thread"}}
         try:
             kind_s, th_s, cps, s_cpu, _ = cpu_search(threads)
             out["search"]["cpu_baseline"] = {"value": cps, "unit": "candidates/s",

@@ -562,6 +562,74 @@ dtb_status dtb_best_reduce_dev(dtb_context* ctx, const dtb_candidate* records,
                                int64_t n, dtb_candidate* best_dev,
                                void* stream);
 
+/* ------------------------------------- multi-GPU reorder stream (§8e) */
+
+/* One process per GPU.  The reorder stream shards by global-batch range
+ * (batches are independent; src/reorder.cpp:319-396 reads
+ * one batch); the concatenated ordering is exchanged INSIDE the library over
+ * NVLink: every rank owns a replica buffer of the whole ordering (u16
+ * in-batch sample indices, global position = batch * global_batch + index),
+ * opened by every peer over CUDA IPC, and the sharded call stores its shard
+ * straight into every replica (peer stores) on a second stream that overlaps
+ * the simulations, ending with a device-side flag barrier over the group.
+ * Host transport of the 64-byte handles is the caller's (e.g.
+ * torch.distributed all_gather_object); no NCCL on the data path. */
+typedef struct dtb_peer_handle {
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} dtb_peer_handle;
+typedef struct dtb_peer_group dtb_peer_group;
+
+/* Replica buffer for n_samples (device memory of ctx's GPU) and its handle. */
+dtb_status dtb_peer_buffer_create(dtb_context* ctx, int64_t n_samples, uint16_t** replica,
+                                  dtb_peer_handle* handle);
+dtb_status dtb_peer_buffer_destroy(dtb_context* ctx, uint16_t* replica);
+/* handles[world] in rank order (this rank's own handle included). */
+dtb_status dtb_peer_group_open(dtb_context* ctx, int32_t rank, int32_t world,
+                               uint16_t* replica, int64_t n_samples,
+                               const dtb_peer_handle* handles, dtb_peer_group** out);
+dtb_status dtb_peer_group_close(dtb_peer_group* group);
+/* (first batch, batch count) of rank `rank` of `world` over n_batches:
+ * contiguous ranges whose sizes differ by at most one (the first
+ * n_batches % world ranks get one more). */
+dtb_status dtb_shard_range(int64_t n_batches, int32_t rank, int32_t world, int64_t* first,
+                           int64_t* count);
+/* disaggregated_reorder over this rank's batch range of the stream
+ * (`samples` = the WHOLE stream, device pointers; n_batches = the whole
+ * stream's batch count).  Per-batch outputs are written at their global
+ * batch positions of the (whole-stream-sized) device arrays
+ * load_before/after[n_batches * dp_lm], t_iter_before/after[n_batches],
+ * greedy_kept[n_batches] (any may be NULL except t_iter_before /
+ * t_iter_after); the ordering goes to every replica of the group.  When the
+ * call's work on `stream` completes, every rank's replica holds the whole
+ * ordering of every rank that made the same call. */
+dtb_status dtb_reorder_stream_shard_dev(dtb_context* ctx, const dtb_cost_model* cm,
+                                        const dtb_plan* plan, const dtb_reorder_mode* mode,
+                                        const dtb_samples* samples, int64_t n_batches,
+                                        dtb_peer_group* group, double* load_before,
+                                        double* load_after, double* t_iter_before,
+                                        double* t_iter_after, uint8_t* greedy_kept,
+                                        void* stream);
+
+/* ------------------------------------------- CUDA graphs of a stream call */
+
+/* The whole device pipeline of one reorder-stream call (cost pass,
+ * partition, simulations, [inter reorder, composition], [peer exchange]) is
+ * captured once into a CUDA graph for FIXED device pointers and replayed with
+ * one launch: dtb_reorder_stream_dev when group == NULL (output_order
+ * required), else dtb_reorder_stream_shard_dev (output_order ignored).  The
+ * peer exchange's barrier counts calls on the device, so replays stay in
+ * step across ranks. */
+typedef struct dtb_graph dtb_graph;
+dtb_status dtb_reorder_stream_graph_create(dtb_context* ctx, const dtb_cost_model* cm,
+                                           const dtb_plan* plan, const dtb_reorder_mode* mode,
+                                           const dtb_samples* samples, int64_t n_batches,
+                                           dtb_peer_group* group, int32_t* output_order,
+                                           double* load_before, double* load_after,
+                                           double* t_iter_before, double* t_iter_after,
+                                           uint8_t* greedy_kept, dtb_graph** out);
+dtb_status dtb_graph_launch(dtb_graph* graph, void* stream);
+dtb_status dtb_graph_destroy(dtb_graph* graph);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -127,6 +127,10 @@ class ReorderReport(C.Structure):
                 ("t_iter_after", c_f64)]
 
 
+class PeerHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
 VP = C.c_void_p
 _SIGS = {
     "last_error": (C.c_char_p, []),
@@ -203,6 +207,17 @@ _SIGS = {
     "orchestration_shard_dev": (c_i32, [VP, VP, P(WorkloadStats), c_i64,
                                         c_i32, c_i64, c_i64, VP, VP, VP]),
     "best_reduce_dev": (c_i32, [VP, VP, c_i64, VP, VP]),
+    "peer_buffer_create": (c_i32, [VP, c_i64, P(VP), P(PeerHandle)]),
+    "peer_buffer_destroy": (c_i32, [VP, VP]),
+    "peer_group_open": (c_i32, [VP, c_i32, c_i32, VP, c_i64, P(PeerHandle), P(VP)]),
+    "peer_group_close": (c_i32, [VP]),
+    "shard_range": (c_i32, [c_i64, c_i32, c_i32, P(c_i64), P(c_i64)]),
+    "reorder_stream_shard_dev": (c_i32, [VP, VP, P(Plan), P(ReorderMode), P(Samples), c_i64, VP,
+                                         VP, VP, VP, VP, VP, VP]),
+    "reorder_stream_graph_create": (c_i32, [VP, VP, P(Plan), P(ReorderMode), P(Samples), c_i64,
+                                            VP, VP, VP, VP, VP, VP, VP, P(VP)]),
+    "graph_launch": (c_i32, [VP, VP]),
+    "graph_destroy": (c_i32, [VP]),
     # oracle-only extras (CPU baselines)
     "set_threads": (None, [C.c_int]),
     "stream_prepare": (c_i32, [P(Samples), c_i64, P(VP)]),

@@ -698,6 +698,34 @@ class Planner:
                     times=(res.times.t_warm, res.times.t_steady, res.times.t_iter),
                     candidates_evaluated=res.candidates_evaluated)
 
+    # ---- multi-GPU reorder stream (one process per GPU) ------------------
+    def peer_buffer_create(self, n_samples: int):
+        """Replica buffer of the whole ordering on this planner's GPU:
+        (device pointer, 64-byte IPC handle)."""
+        p, h = C.c_void_p(), A.PeerHandle()
+        self._check(self.lib.peer_buffer_create(self.ctx, n_samples, C.byref(p), C.byref(h)))
+        return p.value, bytes(h.bytes)
+
+    def peer_buffer_destroy(self, replica: int):
+        self._check(self.lib.peer_buffer_destroy(self.ctx, C.c_void_p(replica)))
+
+    def peer_group_open(self, rank: int, world: int, replica: int, n_samples: int, handles):
+        arr = (A.PeerHandle * world)()
+        for i, h in enumerate(handles):
+            C.memmove(arr[i].bytes, h, 64)
+        g = C.c_void_p()
+        self._check(self.lib.peer_group_open(self.ctx, rank, world, C.c_void_p(replica), n_samples,
+                                             arr, C.byref(g)))
+        return g
+
+    def peer_group_close(self, group):
+        self._check(self.lib.peer_group_close(group))
+
+    def shard_range(self, n_batches: int, rank: int, world: int):
+        f, c = C.c_int64(), C.c_int64()
+        self._check(self.lib.shard_range(n_batches, rank, world, C.byref(f), C.byref(c)))
+        return f.value, c.value
+
     def ingest_trace(self, data: bytes, seq_len_cap: int) -> "SampleBatch":
         """ingest_trace (src/workload.cpp:115-153): JSONL bytes -> SampleBatch.
         Raises TraceError with kind()/line() like the reference."""

@@ -29,7 +29,7 @@ if os.environ.get("DTB_DEFINES"):  # experiment builds stay out of the product p
     OBJ = OBJ + "_" + "_".join(os.environ["DTB_DEFINES"].split()).replace("=", "")
     OUT = os.path.join(OBJ, "libdisttrain_b200.so")
 SOURCES = ["capi.cu", "k_cost.cu", "k_intra.cu", "k_sched.cu", "k_inter.cu", "k_inter2.cu", "k_orch.cu",
-           "k_misc.cu", "k_exhaustive.cu", "k_ingest.cu"]
+           "k_misc.cu", "k_exhaustive.cu", "k_ingest.cu", "k_peer.cu"]
 
 
 def _stale(src_list, target):

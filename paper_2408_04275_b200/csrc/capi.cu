@@ -61,7 +61,17 @@ struct dtb_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-buffer pipelines (lazy)
+  cudaStream_t side = nullptr;                          // peer exchange (lazy)
   DevErr* err = nullptr;  // device
+};
+
+struct dtb_peer_group {
+  int device = 0, rank = 0, world = 1;
+  int64_t n_samples = 0;
+  uint16_t* replica[dtb::kMaxPeers] = {};  // [rank] = local, others IPC-mapped
+  unsigned* flags[dtb::kMaxPeers] = {};
+  bool opened[dtb::kMaxPeers] = {};
+  unsigned* done = nullptr;  // device: [0] CTA counter, [1] call counter (epoch)
 };
 
 struct dtb_cost_model {
@@ -321,6 +331,7 @@ dtb_status dtb_context_destroy(dtb_context* ctx) {
   cudaStreamDestroy(ctx->stream);
   if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
   if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   delete ctx;
   return DTB_OK;
 }
@@ -930,10 +941,9 @@ static dtb_status stream_checks(const dtb_cost_model* cm, const dtb_plan* plan,
   if (dp_lm < 1 || dp_me < 1 || plan->unit[DTB_GENERATOR].dp < 1)
     return fail(DTB_ERR_INTERNAL, "parallel sizes must be >= 1");
   if (bs / dp_lm == 0) return fail(DTB_ERR_INTERNAL, "fewer samples than groups");
-  if (bs > fused_max_n() || dp_lm > fused_max_m())
-    return fail(DTB_ERR_INVALID_ARGUMENT,
-                "global batch %lld / dp %d beyond the fused kernel's limits (%d / %d)", bs, dp_lm,
-                fused_max_n(), fused_max_m());
+  if ((bs > fused_max_n() || dp_lm > fused_max_m()) && dp_lm > intra_generic_max_m())
+    return fail(DTB_ERR_INVALID_ARGUMENT, "more than %d DP groups", intra_generic_max_m());
+  if (bs > 0x7fffffffLL) return fail(DTB_ERR_INVALID_ARGUMENT, "global batch beyond int32");
   // simulate_iteration(identity) is the first cost-model consumer
   TRY(check_stage_queries(cm, *plan));
   const int per_group = static_cast<int>(bs / dp_lm);
@@ -946,8 +956,45 @@ static dtb_status stream_checks(const dtb_cost_model* cm, const dtb_plan* plan,
 // (k_cost.cu: tokens, identity order and loads, batches the averaging bound
 // decides), then the partition kernel on the rest (k_intra.cu).  `fa` holds
 // everything but the cost-pass outputs; `cscr` receives its scratch.
+// Global batches beyond the fused kernels' limits (more than 16,384 samples
+// or 512 groups): per batch, the per-sample costs, a stable device radix
+// sort of (orderable cost, index) and the one-CTA equal-count greedy
+// (launch_intra_generic, any n, m <= 4096), the block loads of both orders
+// and the keep decision; consumers read the 32-bit tokens.
+static cudaError_t launch_sort_partition_generic(FusedArgs& fa, long long n_batches,
+                                                 cudaStream_t s) {
+  const int n = fa.n, m = fa.m;
+  DBuf sizes, flat, offs, li, lg, scr;
+  const size_t sb = intra_generic_scratch(n, m);
+  cudaError_t e = sizes.alloc(8ull * n, s);
+  if (e == cudaSuccess) e = flat.alloc(4ull * n, s);
+  if (e == cudaSuccess) e = offs.alloc(8ull * (m + 1), s);
+  if (e == cudaSuccess) e = li.alloc(8ull * m, s);
+  if (e == cudaSuccess) e = lg.alloc(8ull * m, s);
+  if (e == cudaSuccess) e = scr.alloc(sb, s);
+  for (long long b = 0; b < n_batches && e == cudaSuccess; ++b) {
+    e = launch_batch_tokens(fa.img_off, fa.img_tok, fa.aud_off, fa.aud_tok, b * n, n,
+                            fa.tok32_orig, sizes.as<double>(), fa.err, static_cast<int>(b), s);
+    if (e == cudaSuccess) e = launch_block_loads(sizes.as<double>(), nullptr, n, m, li.as<double>(), s);
+    if (e == cudaSuccess && fa.intra) {
+      e = launch_intra_generic(sizes.as<double>(), n, m, fa.order, 1, scr.p, sb, flat.as<int>(),
+                               offs.as<long long>(), s);
+      if (e == cudaSuccess)
+        e = launch_block_loads(sizes.as<double>(), flat.as<int>(), n, m, lg.as<double>(), s);
+    }
+    if (e == cudaSuccess)
+      e = launch_generic_decide(li.as<double>(), fa.intra ? lg.as<double>() : li.as<double>(), m,
+                                n, b, fa.intra, flat.as<int>(), fa.tok32_orig, fa.order_out,
+                                fa.tok32_staged, fa.load_before, fa.load_after, fa.kept,
+                                fa.wide_flag, s);
+  }
+  return e;
+}
+
 static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBuf& cscr,
                                          cudaStream_t s) {
+  if (fa.n > fused_max_n() || fa.m > fused_max_m())
+    return launch_sort_partition_generic(fa, n_batches, s);
   cudaError_t e = cscr.alloc(cost_scratch_bytes(n_batches, fa.m), s);
   if (e != cudaSuccess) return e;
   CostArgs ca{};
@@ -991,7 +1038,30 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
                              const dtb_reorder_mode* mode, const int* io, const int* it,
                              const int* ao, const int* at, long long n_batches, int* order_out,
                              double* lb, double* la, double* tb, double* ta, unsigned char* kept,
-                             cudaStream_t s) {
+                             cudaStream_t s, const PeerBcast* peer = nullptr) {
+  // Peer exchange of the final order on the side stream, joined at the end:
+  // it overlaps everything after the order is final (the simulations).
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  auto exchange = [&]() -> cudaError_t {
+    if (peer == nullptr) return cudaSuccess;
+    cudaError_t e = cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_ready, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->side, ev_ready, 0);
+    PeerBcast pb = *peer;
+    pb.src = order_out;
+    if (e == cudaSuccess) e = launch_peer_broadcast(pb, ctx->side);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_done, ctx->side);
+    return e;
+  };
+  struct EvGuard {
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    ~EvGuard() {
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+    }
+  } ev_guard{&ev_ready, &ev_done};
   const int n = static_cast<int>(plan->global_batch);
   const int dp_lm = plan->unit[DTB_BACKBONE].dp;
   const int dp_me = plan->unit[DTB_ENCODER].dp;
@@ -1044,6 +1114,7 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   fa.err = ctx->err;
   DBuf cscr;
   CU(launch_sort_partition(fa, n_batches, cscr, s));
+  if (!compose_needed) CU(exchange());  // the intra order is the output order
   const TokSrc tok{tok16.as<unsigned short>(), tok16s.as<unsigned short>(), tok32.as<int>(),
                    tok32s.as<int>(), kept_dev, wflag.as<unsigned int>(), n};
   if (span > 1) {  // assembled microbatch sums [b][e][i]
@@ -1113,9 +1184,11 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
       CU(launch_inter(ia, scr.p, inter_bytes, s));
     }
   }
-  if (compose_needed)
+  if (compose_needed) {
     CU(launch_compose(n_batches, n, dp_lm, dp_me, intra_out, mode->inter ? inter.as<int>() : nullptr,
                       order_out, s));
+    CU(exchange());
+  }
   ga.staged = true;
   ga.mbsum = span > 1 ? mb1.as<int>() : nullptr;
   ga.order = mode->inter ? inter.as<int>() : nullptr;
@@ -1127,7 +1200,153 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   CU(launch_group_sims(ga, scr.p, s));
   CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, ta, s,
                           only_kept, tb));
+  if (ev_done != nullptr) CU(cudaStreamWaitEvent(s, ev_done, 0));  // join the exchange
   return DTB_OK;
+}
+
+// ------------------------------------------------------------ peer groups
+namespace {
+size_t replica_bytes(int64_t n_samples) {
+  return (static_cast<size_t>(n_samples) * 2 + 255) / 256 * 256;
+}
+}  // namespace
+
+dtb_status dtb_peer_buffer_create(dtb_context* ctx, int64_t n_samples, uint16_t** replica,
+                                  dtb_peer_handle* handle) {
+  TRY(set_device(ctx));
+  if (replica == nullptr || handle == nullptr || n_samples < 0)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "peer buffer: bad arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(dtb_peer_handle), "IPC handle size");
+  void* p = nullptr;
+  const size_t bytes = replica_bytes(n_samples) + 4 * dtb::kMaxPeers;
+  CU(cudaMalloc(&p, bytes));
+  CU(cudaMemset(p, 0, bytes));  // flags start at epoch 0
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    CU(e);
+  }
+  std::memcpy(handle->bytes, &h, sizeof(h));
+  *replica = static_cast<uint16_t*>(p);
+  return DTB_OK;
+}
+
+dtb_status dtb_peer_buffer_destroy(dtb_context* ctx, uint16_t* replica) {
+  TRY(set_device(ctx));
+  if (replica) CU(cudaFree(replica));
+  return DTB_OK;
+}
+
+dtb_status dtb_peer_group_open(dtb_context* ctx, int32_t rank, int32_t world, uint16_t* replica,
+                               int64_t n_samples, const dtb_peer_handle* handles,
+                               dtb_peer_group** out) {
+  TRY(set_device(ctx));
+  if (out == nullptr || handles == nullptr || replica == nullptr || world < 1 ||
+      world > dtb::kMaxPeers || rank < 0 || rank >= world)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "peer group: rank %d of %d (at most %d ranks)", rank,
+                world, dtb::kMaxPeers);
+  auto* g = new dtb_peer_group;
+  g->device = ctx->device;
+  g->rank = rank;
+  g->world = world;
+  g->n_samples = n_samples;
+  for (int p = 0; p < world; ++p) {
+    void* ptr = replica;
+    if (p != rank) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles[p].bytes, sizeof(h));
+      const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        dtb_peer_group_close(g);
+        CU(e);
+      }
+      g->opened[p] = true;
+    }
+    g->replica[p] = static_cast<uint16_t*>(ptr);
+    g->flags[p] = reinterpret_cast<unsigned*>(static_cast<char*>(ptr) + replica_bytes(n_samples));
+  }
+  cudaError_t e = cudaMalloc(&g->done, 2 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(g->done, 0, 2 * sizeof(unsigned));
+  if (e != cudaSuccess) {
+    dtb_peer_group_close(g);
+    CU(e);
+  }
+  if (ctx->side == nullptr) CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  *out = g;
+  return DTB_OK;
+}
+
+dtb_status dtb_peer_group_close(dtb_peer_group* g) {
+  if (g == nullptr) return DTB_OK;
+  cudaSetDevice(g->device);
+  for (int p = 0; p < g->world; ++p)
+    if (g->opened[p]) cudaIpcCloseMemHandle(g->replica[p]);
+  if (g->done) cudaFree(g->done);
+  delete g;
+  return DTB_OK;
+}
+
+dtb_status dtb_shard_range(int64_t n_batches, int32_t rank, int32_t world, int64_t* first,
+                           int64_t* count) {
+  if (world < 1 || rank < 0 || rank >= world || n_batches < 0 || !first || !count)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "shard range: rank %d of %d", rank, world);
+  const int64_t base = n_batches / world, extra = n_batches % world;
+  *first = rank * base + std::min<int64_t>(rank, extra);
+  *count = base + (rank < extra ? 1 : 0);
+  return DTB_OK;
+}
+
+dtb_status dtb_reorder_stream_shard_dev(dtb_context* ctx, const dtb_cost_model* cm,
+                                        const dtb_plan* plan, const dtb_reorder_mode* mode,
+                                        const dtb_samples* samples, int64_t n_batches,
+                                        dtb_peer_group* group, double* load_before,
+                                        double* load_after, double* t_iter_before,
+                                        double* t_iter_after, uint8_t* greedy_kept,
+                                        void* stream) {
+  TRY(set_device(ctx));
+  if (group == nullptr || group->device != ctx->device)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "peer group of another device");
+  if (t_iter_before == nullptr || t_iter_after == nullptr)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "t_iter_before / t_iter_after are required");
+  const dtb_reorder_mode def{1, 1, DTB_ASCENDING};
+  const dtb_reorder_mode* md = mode ? mode : &def;
+  TRY(stream_checks(cm, plan, md, samples->n, n_batches));
+  if (samples->n > group->n_samples)
+    return fail(DTB_ERR_INVALID_ARGUMENT, "stream of %lld samples, replicas hold %lld",
+                static_cast<long long>(samples->n), static_cast<long long>(group->n_samples));
+  int64_t first = 0, count = 0;
+  TRY(dtb_shard_range(n_batches, group->rank, group->world, &first, &count));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long n = plan->global_batch;
+  const int dp = plan->unit[DTB_BACKBONE].dp;
+  const long long s0 = first * n, cnt = count * n;
+  DBuf shard_order;
+  CU(shard_order.alloc(4ull * std::max<long long>(cnt, 1), s));
+  dtb::PeerBcast pb{};
+  pb.count = cnt;
+  pb.world = group->world;
+  pb.rank = group->rank;
+  pb.done = group->done;
+  pb.epoch = group->done + 1;
+  pb.flags_local = group->flags[group->rank];
+  bool al = (reinterpret_cast<uintptr_t>(shard_order.p) & 15u) == 0;
+  for (int p = 0; p < group->world; ++p) {
+    pb.dst[p] = group->replica[p] + s0;
+    pb.flags[p] = group->flags[p];
+    al = al && (reinterpret_cast<uintptr_t>(pb.dst[p]) & 15u) == 0;
+  }
+  pb.aligned = al ? 1 : 0;
+  if (count == 0) {  // nothing to reorder; still take part in the barrier
+    CU(launch_peer_broadcast(pb, s));
+    return DTB_OK;
+  }
+  const int* ao = samples->audio_offsets ? samples->audio_offsets + s0 : nullptr;
+  return run_stream(ctx, cm, plan, md, samples->image_offsets + s0, samples->image_tokens, ao,
+                    samples->audio_tokens, count, shard_order.as<int>(),
+                    load_before ? load_before + first * dp : nullptr,
+                    load_after ? load_after + first * dp : nullptr, t_iter_before + first,
+                    t_iter_after + first, greedy_kept ? greedy_kept + first : nullptr, s, &pb);
 }
 
 dtb_status dtb_reorder_stream_dev(dtb_context* ctx, const dtb_cost_model* cm,
@@ -1272,8 +1491,8 @@ static dtb_status intra_stream(dtb_context* ctx, int64_t bs, int32_t dp_lm, int3
     return fail(DTB_ERR_BATCH_SIZE_MISMATCH, "stream has %lld samples, expected %lld",
                 static_cast<long long>(samples->n), static_cast<long long>(n_batches * bs));
   if (bs / dp_lm == 0) return fail(DTB_ERR_INTERNAL, "fewer samples than groups");
-  if (bs > fused_max_n() || dp_lm > fused_max_m())
-    return fail(DTB_ERR_INVALID_ARGUMENT, "global batch / dp beyond the fused kernel's limits");
+  if ((bs > fused_max_n() || dp_lm > fused_max_m()) && dp_lm > intra_generic_max_m())
+    return fail(DTB_ERR_INVALID_ARGUMENT, "more than %d DP groups", intra_generic_max_m());
   FusedArgs fa{};
   fa.n = static_cast<int>(bs);
   fa.m = dp_lm;
@@ -1805,3 +2024,70 @@ dtb_status dtb_ingest_trace(dtb_context* ctx, const char* bytes, int64_t len,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------- CUDA graphs
+struct dtb_graph {
+  int device = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+dtb_status dtb_reorder_stream_graph_create(dtb_context* ctx, const dtb_cost_model* cm,
+                                           const dtb_plan* plan, const dtb_reorder_mode* mode,
+                                           const dtb_samples* samples, int64_t n_batches,
+                                           dtb_peer_group* group, int32_t* output_order,
+                                           double* load_before, double* load_after,
+                                           double* t_iter_before, double* t_iter_after,
+                                           uint8_t* greedy_kept, dtb_graph** out) {
+  TRY(set_device(ctx));
+  if (out == nullptr) return fail(DTB_ERR_INVALID_ARGUMENT, "null graph output");
+  cudaStream_t cs = nullptr;
+  CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  dtb_status st = DTB_OK;
+  cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    st = group ? dtb_reorder_stream_shard_dev(ctx, cm, plan, mode, samples, n_batches, group,
+                                              load_before, load_after, t_iter_before,
+                                              t_iter_after, greedy_kept, cs)
+               : dtb_reorder_stream_dev(ctx, cm, plan, mode, samples, n_batches, output_order,
+                                        load_before, load_after, t_iter_before, t_iter_after,
+                                        greedy_kept, cs);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+    if (st == DTB_OK && e2 == cudaSuccess) {
+      auto* gr = new dtb_graph;
+      gr->device = ctx->device;
+      gr->graph = g;
+      e = cudaGraphInstantiate(&gr->exec, g, 0);
+      if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        delete gr;
+      } else {
+        *out = gr;
+      }
+    } else {
+      if (g) cudaGraphDestroy(g);
+      if (st == DTB_OK) e = e2;
+    }
+  }
+  cudaStreamDestroy(cs);
+  if (st != DTB_OK) return st;
+  CU(e);
+  return DTB_OK;
+}
+
+dtb_status dtb_graph_launch(dtb_graph* g, void* stream) {
+  if (g == nullptr) return fail(DTB_ERR_INVALID_ARGUMENT, "null graph");
+  CU(cudaSetDevice(g->device));
+  CU(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+  return DTB_OK;
+}
+
+dtb_status dtb_graph_destroy(dtb_graph* g) {
+  if (g == nullptr) return DTB_OK;
+  cudaSetDevice(g->device);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return DTB_OK;
+}

@@ -36,7 +36,7 @@ namespace dtb {
 constexpr int kCostT = 128;                 // threads per chunk CTA
 constexpr int kCostQ = 1024;                // samples per chunk
 constexpr int kCostOff = kCostQ + 4;        // offsets + the next boundary, padded
-constexpr int kCostTok = 4096;              // token slots (image + audio + spares)
+constexpr int kCostTok = 3072;              // token slots (image + audio + spares; ~2.1K used)
 constexpr int kCostPer = kCostQ / kCostT;   // samples per thread
 
 struct CostSmem {
@@ -354,7 +354,7 @@ __device__ __forceinline__ void cost_chunk(const CostArgs& a, CostSmem& S) {
   }
 }
 
-__global__ void __launch_bounds__(kCostT, 8) cost_stream_kernel(const __grid_constant__ CostArgs a) {
+__global__ void __launch_bounds__(kCostT, 10) cost_stream_kernel(const __grid_constant__ CostArgs a) {
   __shared__ CostSmem S;
   if (a.staged)
     cost_chunk<true>(a, S);

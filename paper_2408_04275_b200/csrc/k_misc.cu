@@ -1,3 +1,4 @@
+#include <climits>
 // Small kernels of the path: per-sample costs, workload stats,
 // block_group_loads, select_min/select_closest, microbatch assembly and
 // output-order composition.
@@ -74,13 +75,97 @@ __global__ void block_loads_kernel(const double* sizes, const int* order, int n,
   const int lo = g * per;
   const int hi = g == m - 1 ? n : lo + per;
   double acc = 0.0;
-  for (int pos = lo; pos < hi; ++pos) acc += sizes[order[pos]];
+  for (int pos = lo; pos < hi; ++pos) acc += sizes[order ? order[pos] : pos];
   loads[g] = acc;
 }
 
 cudaError_t launch_block_loads(const double* sizes, const int* order, int n, int m,
                                double* loads, cudaStream_t stream) {
   block_loads_kernel<<<(m + 127) / 128, 128, 0, stream>>>(sizes, order, n, m, loads);
+  return cudaGetLastError();
+}
+
+// ---- one global batch beyond the fused kernels' limits (n > 16,384 or
+// more than 512 groups): per-sample cost_size (include/core.hpp:160-167) as
+// int64 -> double sizes and 32-bit tokens for the simulations; a
+// modality-token sum beyond int32 is reported (E_COST_RANGE).
+__global__ void batch_tokens_kernel(const int* io, const int* it, const int* ao, const int* at,
+                                    long long first, int n, int* tok32, double* sizes,
+                                    DevErr* err, int bidx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long s = first + i;
+  long long t = 0;
+  for (int x = io[s]; x < io[s + 1]; ++x) t += it[x];
+  if (ao != nullptr)
+    for (int x = ao[s]; x < ao[s + 1]; ++x) t += at[x];
+  sizes[i] = static_cast<double>(t + t);
+  if (t < INT_MIN || t > INT_MAX) dev_fail(err, E_COST_RANGE, bidx);
+  if (tok32 != nullptr) tok32[s] = static_cast<int>(t);
+}
+
+// The keep decision of disaggregated_reorder (src/reorder.cpp:340-354) for
+// one batch of the generic route and its outputs: loads, kept, the intra
+// order (greedy flat order if kept, else identity) and the staged tokens.
+__global__ void __launch_bounds__(1024)
+generic_decide_kernel(const double* li, const double* lg, int m, int n, long long b, int intra,
+                      const int* flat, const int* tok32, int* order_out, int* tok32_staged,
+                      double* load_before, double* load_after, unsigned char* kept,
+                      unsigned* wide_flag) {
+  __shared__ double red[2][32];
+  double mi = 0.0, mg = 0.0;
+  for (int g = threadIdx.x; g < m; g += blockDim.x) {
+    mi = fmax(mi, li[g]);
+    mg = fmax(mg, lg[g]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mi = fmax(mi, __shfl_xor_sync(0xffffffffu, mi, o));
+    mg = fmax(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = mi;
+    red[1][threadIdx.x >> 5] = mg;
+  }
+  __syncthreads();
+  mi = red[0][0];
+  mg = red[1][0];
+  for (unsigned w = 1; w < blockDim.x / 32; ++w) {
+    mi = fmax(mi, red[0][w]);
+    mg = fmax(mg, red[1][w]);
+  }
+  // sizes are non-negative integers here (loads exact), so max is exact
+  const bool keep = intra && mg <= mi;
+  const long long first = b * n;
+  for (int g = threadIdx.x; g < m; g += blockDim.x) {
+    if (load_before) load_before[b * m + g] = li[g];
+    if (load_after) load_after[b * m + g] = keep ? lg[g] : li[g];
+  }
+  if (threadIdx.x == 0) {
+    if (kept) kept[b] = keep ? 1 : 0;
+    if (wide_flag) wide_flag[b] = 1u;  // consumers read the 32-bit tokens
+  }
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int src = keep ? flat[k] : k;
+    order_out[first + k] = src;
+    if (tok32_staged != nullptr && tok32 != nullptr) tok32_staged[first + k] = tok32[first + src];
+  }
+}
+
+cudaError_t launch_batch_tokens(const int* io, const int* it, const int* ao, const int* at,
+                                long long first, int n, int* tok32, double* sizes, DevErr* err,
+                                int bidx, cudaStream_t stream) {
+  batch_tokens_kernel<<<(n + 255) / 256, 256, 0, stream>>>(io, it, ao, at, first, n, tok32,
+                                                          sizes, err, bidx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generic_decide(const double* li, const double* lg, int m, int n, long long b,
+                                  int intra, const int* flat, const int* tok32, int* order_out,
+                                  int* tok32_staged, double* load_before, double* load_after,
+                                  unsigned char* kept, unsigned* wide_flag, cudaStream_t stream) {
+  generic_decide_kernel<<<1, 1024, 0, stream>>>(li, lg, m, n, b, intra, flat, tok32, order_out,
+                                                tok32_staged, load_before, load_after, kept,
+                                                wide_flag);
   return cudaGetLastError();
 }
 

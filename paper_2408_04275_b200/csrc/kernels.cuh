@@ -82,6 +82,22 @@ struct CostArgs {
 size_t cost_scratch_bytes(long long n_batches, int m);  // blk_ident, bstat, list, state
 cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream);
 
+// Multi-GPU exchange (k_peer.cu): this rank's shard of the ordering (int32
+// batch-local indices) stored as u16 into every rank's replica, then a flag
+// barrier over the group.
+constexpr int kMaxPeers = 8;
+struct PeerBcast {
+  const int* src;                   // [count] this rank's shard, batch-local indices
+  long long count;
+  unsigned short* dst[kMaxPeers];   // replica of rank p + the shard's stream offset
+  unsigned* flags[kMaxPeers];       // flag array [world] of replica p
+  const unsigned* flags_local;      // this rank's flag array
+  unsigned* done;                   // CTA counter (zeroed by the launcher)
+  unsigned* epoch;                  // this rank's call counter (device; graph-replay safe)
+  int world, rank, aligned;         // aligned: src / dst 16-byte aligned
+};
+cudaError_t launch_peer_broadcast(const PeerBcast& a, cudaStream_t stream);
+
 // Cost pass: tok16[i] = min(modality tokens of sample i, 0x7fff) for the
 // whole stream, wide_flag[i / n] |= 1 on saturation or negative tokens.
 cudaError_t launch_token_keys(const int* img_off, const int* img_tok, const int* aud_off,
@@ -122,7 +138,15 @@ cudaError_t launch_intra_generic(const double* sizes, int n, int m, int order,
                                  long long* offsets_out, cudaStream_t stream);
 
 cudaError_t launch_block_loads(const double* sizes, const int* order, int n,
-                               int m, double* loads, cudaStream_t stream);
+                               int m, double* loads, cudaStream_t stream);  // order null: identity
+// Generic route for global batches beyond the fused kernels (k_misc.cu).
+cudaError_t launch_batch_tokens(const int* io, const int* it, const int* ao, const int* at,
+                                long long first, int n, int* tok32, double* sizes, DevErr* err,
+                                int bidx, cudaStream_t stream);
+cudaError_t launch_generic_decide(const double* li, const double* lg, int m, int n, long long b,
+                                  int intra, const int* flat, const int* tok32, int* order_out,
+                                  int* tok32_staged, double* load_before, double* load_after,
+                                  unsigned char* kept, unsigned* wide_flag, cudaStream_t stream);
 cudaError_t launch_select(const double* keys, const int* pending, int np,
                           int k, int closest, double target, int* out,
                           cudaStream_t stream);

@@ -38,6 +38,9 @@ REQUIRED = [
     "inter_reorder_batch", "inter_reorder_batch_dev", "disaggregated_reorder", "reorder_stream",
     "reorder_stream_dev", "intra_stream_dev", "predict_times", "enumerate_parallelism", "solve_subproblem",
     "model_orchestration", "orchestration_shard_dev", "best_reduce_dev",
+    "peer_buffer_create", "peer_buffer_destroy", "peer_group_open", "peer_group_close",
+    "shard_range", "reorder_stream_shard_dev", "reorder_stream_graph_create", "graph_launch",
+    "graph_destroy",
 ]
 
 

@@ -36,7 +36,12 @@ def test_oracles_export_the_same_abi(ref, port):
     names = [s[len("dtb_"):] for s in declared_symbols()]
     device_only = {"schedule_batch_dev", "inter_reorder_batch_dev", "reorder_stream_dev",
                    "orchestration_shard_dev", "best_reduce_dev", "infeasible_reason_text",
-                   "intra_stream_dev", "ingest_trace_dev"}
+                   "intra_stream_dev", "ingest_trace_dev",
+                   # multi-GPU plumbing (CUDA IPC peer groups)
+                   "peer_buffer_create", "peer_buffer_destroy", "peer_group_open",
+                   "peer_group_close", "shard_range", "reorder_stream_shard_dev",
+                   # CUDA graphs of a device call
+                   "reorder_stream_graph_create", "graph_launch", "graph_destroy"}
     # trace ingest is pinned by the compiled reference and nlohmann itself
     # (tests/test_ingest.py); the C port does not restate a JSON library
     ref_only = {"ingest_trace"}

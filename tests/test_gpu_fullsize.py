@@ -158,3 +158,17 @@ def test_stats_full_stream(gpu, ora, c4_stream):
     a, b = gpu.compute_stats(sub, 8192), ora.compute_stats(sub, 8192)
     assert (a.seq_len, a.mean_encoder_tokens, a.mean_generator_tokens) == \
         (b.seq_len, b.mean_encoder_tokens, b.mean_generator_tokens)
+
+
+@pytest.mark.parametrize("bs,dp,inter,fam", [(32768, 128, False, "mixed"), (32768, 128, True, "dense"),
+                                             (32768, 1024, False, "dense"), (20000, 100, False, "mixed")])
+def test_beyond_fused_limits(gpu, ora, bs, dp, inter, fam):
+    """Global batches beyond the fused kernels' 16,384 samples / 512 groups
+    (the reference accepts any batch, src/reorder.cpp:319-396): the generic
+    route (device radix sort + one-CTA greedy per batch)."""
+    ci, co = _desk(gpu, ora)
+    pl = H.plan((1, dp, 1), (1, dp, 2), (1, dp, 1), bs)
+    s = synth_stream(2 * bs, seed=31, family=fam)
+    ra = gpu.reorder_stream(ci, pl, s, 2, inter=inter)
+    rb = ora.reorder_stream(co, pl, s, 2, inter=inter)
+    _compare(ra, rb, f"BS {bs} DP {dp} inter {inter}")
