@@ -25,11 +25,15 @@ REF_SOURCES = "/root/reference/proj/core/src"
 
 
 def build(ref: bool = True) -> None:
-    """Compile the port (always) and the reference (when its sources exist)."""
+    """Compile the port (always) and the reference (when its sources exist),
+    and the reference's own tests linked against the GPU shim
+    (oracle/refcheck, needs the product library built first)."""
     targets = ["port"]
     if ref and os.path.isdir(REF_SOURCES):
         targets.append("ref")
     subprocess.run(["make", "-s", "-j8", "-C", HERE, *targets], check=True)
+    if ref and os.path.isdir(REF_SOURCES):
+        subprocess.run(["make", "-s", "-j8", "-C", os.path.join(HERE, "refcheck")], check=True)
 
 
 def ref_available() -> bool:

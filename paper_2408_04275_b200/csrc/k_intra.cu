@@ -16,6 +16,7 @@
 // and one CTA's loads overlap the other's sort/greedy.  A batch whose costs
 // or (group, slot) ranges do not fit 16 bits is processed by the same code
 // with 32-bit arrays in a global scratch slot (`wide_scratch`).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "block_ops.cuh"
@@ -25,6 +26,8 @@
 #include "tma.cuh"
 
 namespace dtb {
+
+namespace cg = cooperative_groups;
 
 // Orderable bits of a double: -0.0 folds onto +0.0 (the reference
 // comparator treats them as equal, src/reorder.cpp:34-40).
@@ -128,6 +131,7 @@ struct NarrowSmem {
   int tmp[kFusedT / 32 + 3];
   long long tmpll[kFusedT / 32 + 1];
   unsigned int s_and, s_or;
+  unsigned deferred;  // fast path: a kept batch's permutation is left to the cluster peer
 };
 constexpr int kSortRB = 5;  // narrow-path digit bits (per-thread counters)
 // per-thread radix counters of the narrow path (their own space, so the
@@ -327,6 +331,78 @@ __device__ __forceinline__ void identity_order_out(const FusedArgs& a, long long
   }
 }
 
+// The permutation of a kept batch: stable LSD radix sort of the sample
+// indices by key (the u16 tokens; descending keys 0x7fff - tok) in kbi /
+// idx16, counters in their own space so the greedy's cells in out16
+// survive.  Sorted position k (the greedy's k: the same stable order of the
+// sizes) is then idx16[swz(k)].
+__device__ __noinline__ void sort_batch_keys(const FusedArgs& a, long long b, NarrowSmem&) {
+  NarrowSmem& S = shared_state();
+  const int n = a.n, tid = threadIdx.x;
+  const long long first = b * n;
+  const bool desc = a.order == DTB_DESCENDING;
+  const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
+  for (int q = tid; q < (n >> 3); q += kFusedT) {
+    const uint4 v = __ldg(src + q);
+    const unsigned wd[4] = {v.x, v.y, v.z, v.w};
+    unsigned kw[4], iw[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const unsigned t0 = wd[h] & 0xffffu, t1 = wd[h] >> 16;
+      const unsigned k0 = desc ? 0x7fffu - t0 : t0, k1 = desc ? 0x7fffu - t1 : t1;
+      kw[h] = k0 | (k1 << 16);
+      const unsigned i0 = static_cast<unsigned>(8 * q + 2 * h);
+      iw[h] = i0 | ((i0 + 1) << 16);
+    }
+    reinterpret_cast<uint4*>(S.kbi)[q] = make_uint4(kw[0], kw[1], kw[2], kw[3]);
+    reinterpret_cast<uint4*>(S.idx16)[q] = make_uint4(iw[0], iw[1], iw[2], iw[3]);
+  }
+  for (int i = n + tid; i < kFusedSlots; i += kFusedT) {  // padding: largest digits
+    S.kbi[i] = 0xffffu;
+    S.idx16[i] = static_cast<unsigned short>(i);
+  }
+  __syncthreads();
+  // every token < kHistBins: ascending keys vary in bits [0, 13), descending
+  // keys (0x7fff - tok > 0x5fff) in bits [0, 13) too; padding is 0xffff
+  constexpr int kKeyBits = 13;
+  static_assert(kHistBins <= (1 << kKeyBits), "keys of the histogram path fit 13 bits");
+  unsigned* cw = sort_counters();
+  for (int sh = 0; sh < kKeyBits; sh += kSortRB) {
+    const int bits = min(kSortRB, kKeyBits - sh);
+    const unsigned mask = (1u << bits) - 1u;
+    auto dig = [&](unsigned key) { return (key >> sh) & mask; };
+    if (sh + kSortRB >= kKeyBits)
+      tile_pass_blocked<kFusedT, kFusedItems, kSortRB, true>(S.idx16, S.kbi, dig, cw, S.tmp);
+    else
+      tile_pass_blocked<kFusedT, kFusedItems, kSortRB, false>(S.idx16, S.kbi, dig, cw, S.tmp);
+  }
+}
+
+// Outputs of a kept batch from the greedy's cells (this CTA) and the sorted
+// indices / keys (`idx`, `key`: this CTA's or, in a cluster pair, the peer's
+// shared memory through DSMEM): the intra order and its staged tokens,
+// coalesced per group.
+__device__ __noinline__ void kept_output(const FusedArgs& a, long long b, NarrowSmem&,
+                                         const unsigned short* idx, const unsigned short* key) {
+  NarrowSmem& S = shared_state();
+  const int n = a.n, m = a.m, lane = lane_id(), w = warp_id();
+  const long long first = b * n;
+  const bool desc = a.order == DTB_DESCENDING;
+  const int cap = (n + m - 1) / m;
+  const int capP = ((cap + 1) | 3) - 1;
+  for (int g = w; g < m; g += kFusedT / 32) {
+    const int base = S.off[g], cnt = S.G.gcnt[g];
+    for (int slot = lane; slot < cnt; slot += 32) {
+      const unsigned i = idx[swz(S.out16[g * capP + slot])];
+      a.order_out[first + base + slot] = static_cast<int>(i);
+      if (a.tok16_staged != nullptr) {
+        const unsigned k = key[i];
+        a.tok16_staged[first + base + slot] = static_cast<unsigned short>(desc ? 0x7fffu - k : k);
+      }
+    }
+  }
+}
+
 // Histogram path (every token sum < kHistBins).  The greedy's decisions
 // depend only on the SORTED SIZES, and equal sizes are interchangeable, so
 // the sorted size sequence is the histogram's expansion: the greedy, its
@@ -336,7 +412,8 @@ __device__ __forceinline__ void identity_order_out(const FusedArgs& a, long long
 // cursors): two warps walk the batch halves in index order, ranking equal
 // tokens within 32 samples with MATCH, so ties keep index order
 // (src/reorder.cpp:34-40).
-__device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSmem&) {
+__device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSmem&,
+                                      bool defer_kept) {
   NarrowSmem& S = shared_state();  // shared address space: LDS/STS, not generic
   const int n = a.n, m = a.m, tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const long long first = b * n;
@@ -480,59 +557,13 @@ __device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSm
   if (!keep) {
     if (a.state == nullptr) identity_order_out(a, first, n);  // else written by the cost pass
   } else {
-    // ---- 5. kept: the permutation.  Stable LSD radix sort of the sample
-    // indices by key (the u16 tokens, descending keys 0x7fff - tok), its
-    // counters in their own space so the greedy's cells in out16 survive;
-    // sorted position k of the greedy is then idx16[swz(k)] (same stable
-    // order as the greedy's sizes).
-    __syncthreads();
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
-      for (int q = tid; q < (n >> 3); q += kFusedT) {
-        const uint4 v = __ldg(src + q);
-        const unsigned wd[4] = {v.x, v.y, v.z, v.w};
-        unsigned kw[4], iw[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const unsigned t0 = wd[h] & 0xffffu, t1 = wd[h] >> 16;
-          const unsigned k0 = desc ? 0x7fffu - t0 : t0, k1 = desc ? 0x7fffu - t1 : t1;
-          kw[h] = k0 | (k1 << 16);
-          const unsigned i0 = static_cast<unsigned>(8 * q + 2 * h);
-          iw[h] = i0 | ((i0 + 1) << 16);
-        }
-        reinterpret_cast<uint4*>(S.kbi)[q] = make_uint4(kw[0], kw[1], kw[2], kw[3]);
-        reinterpret_cast<uint4*>(S.idx16)[q] = make_uint4(iw[0], iw[1], iw[2], iw[3]);
-      }
-      for (int i = n + tid; i < kFusedSlots; i += kFusedT) {  // padding: largest digits
-        S.kbi[i] = 0xffffu;
-        S.idx16[i] = static_cast<unsigned short>(i);
-      }
-    }
-    __syncthreads();
-    // every token < kHistBins: ascending keys vary in bits [0, 13), descending
-    // keys (0x7fff - tok > 0x5fff) in bits [0, 13) too; padding is 0xffff
-    constexpr int kKeyBits = 13;
-    static_assert(kHistBins <= (1 << kKeyBits), "keys of the histogram path fit 13 bits");
-    unsigned* cw = sort_counters();
-    for (int sh = 0; sh < kKeyBits; sh += kSortRB) {
-      const int bits = min(kSortRB, kKeyBits - sh);
-      const unsigned mask = (1u << bits) - 1u;
-      auto dig = [&](unsigned key) { return (key >> sh) & mask; };
-      if (sh + kSortRB >= kKeyBits)
-        tile_pass_blocked<kFusedT, kFusedItems, kSortRB, true>(S.idx16, S.kbi, dig, cw, S.tmp);
-      else
-        tile_pass_blocked<kFusedT, kFusedItems, kSortRB, false>(S.idx16, S.kbi, dig, cw, S.tmp);
-    }
-    for (int g = w; g < m; g += kFusedT / 32) {
-      const int base = S.off[g], cnt = S.G.gcnt[g];
-      for (int slot = lane; slot < cnt; slot += 32) {
-        const unsigned idx = S.idx16[swz(S.out16[g * capP + slot])];
-        a.order_out[first + base + slot] = static_cast<int>(idx);
-        if (a.tok16_staged != nullptr) {
-          const unsigned key = S.kbi[idx];
-          a.tok16_staged[first + base + slot] = static_cast<unsigned short>(desc ? 0x7fffu - key : key);
-        }
-      }
+    // ---- 5. kept: the permutation (here, or by the cluster peer)
+    if (defer_kept) {
+      if (tid == 0) S.deferred = 1u;
+    } else {
+      __syncthreads();
+      sort_batch_keys(a, b, S);
+      kept_output(a, b, S, S.idx16, S.kbi);
     }
   }
   if (a.prof) {
@@ -715,7 +746,8 @@ __device__ __noinline__ void narrow_sort_path(const FusedArgs& a, long long b, N
 // Per global batch, after the streaming cost pass (cost_stream_kernel,
 // k_cost.cu): batches it already decided exit at once; the rest take the
 // histogram path, the sort path (token sums >= kHistBins) or the 32-bit path.
-__device__ __forceinline__ void process_batch(const FusedArgs& a, long long b, NarrowSmem& S) {
+__device__ __forceinline__ void process_batch(const FusedArgs& a, long long b, NarrowSmem& S,
+                                              bool defer_kept = false) {
   const int n = a.n, m = a.m, tid = threadIdx.x;
   const long long first = b * n;
   const unsigned st = a.state != nullptr ? a.state[b] : kBatchSort;
@@ -773,7 +805,7 @@ __device__ __forceinline__ void process_batch(const FusedArgs& a, long long b, N
   }
   __syncthreads();
   if (a.prof && tid == 0) a.prof[b * kProfSlots + 1] = globaltimer();
-  fast_path(a, b, S);
+  fast_path(a, b, S, defer_kept);
 }
 
 // One CTA per batch, or (with the cost pass's list) persistent CTAs over the
@@ -787,9 +819,37 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
     return;
   }
   const unsigned count = a.list[0];
-  for (unsigned q = blockIdx.x; q < count; q += gridDim.x) {
-    process_batch(a, a.list[1 + q], S);
-    __syncthreads();  // the shared state is reused by the next batch
+  const unsigned pairs = gridDim.x / 2;  // launched as clusters of two CTAs
+  if (count > pairs) {  // many batches: every CTA takes its own
+    for (unsigned q = blockIdx.x; q < count; q += gridDim.x) {
+      process_batch(a, a.list[1 + q], S);
+      __syncthreads();  // the shared state is reused by the next batch
+    }
+    return;
+  }
+  // Few batches (latency-bound): the two CTAs of a cluster share one.  Rank 0
+  // runs the histogram, greedy and keep decision while rank 1 runs the
+  // stable radix sort; a kept batch's order is then written by rank 0 from
+  // its cells and rank 1's sorted indices, read through distributed shared
+  // memory.
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank();
+  for (unsigned q = blockIdx.x / 2; q < count; q += pairs) {
+    const long long b = a.list[1 + q];
+    const bool fast = a.state[b] == kBatchFast && a.m <= kNarrowMaxM && a.n <= kFusedMaxN &&
+                      (a.n & 7) == 0;
+    if (threadIdx.x == 0) S.deferred = 0u;
+    __syncthreads();
+    if (rank == 1) {
+      if (fast) sort_batch_keys(a, b, S);
+    } else {
+      process_batch(a, b, S, fast);
+    }
+    cl.sync();  // the peer's sorted indices and this CTA's cells are ready
+    if (rank == 0 && S.deferred) {
+      kept_output(a, b, S, cl.map_shared_rank(S.idx16, 1), cl.map_shared_rank(S.kbi, 1));
+    }
+    cl.sync();  // the peer's shared memory is free again
   }
 }
 
@@ -868,7 +928,20 @@ cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches, cudaStre
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid = std::min<long long>(n_batches, static_cast<long long>(sms) * DTB_FUSED_MIN_BLOCKS);
+    grid = static_cast<long long>(sms) * DTB_FUSED_MIN_BLOCKS / 2 * 2;  // clusters of two
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kFusedT);
+    cfg.dynamicSmemBytes = kFusedSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, intra_fused_kernel, a);
   }
   intra_fused_kernel<<<static_cast<unsigned>(grid), kFusedT, kFusedSmem, stream>>>(a);
   return cudaGetLastError();
