@@ -17,12 +17,16 @@
 namespace dtb {
 
 // Stage-time access: explicit row-major matrices...
+// col(s): the column class of stage s — stages of one class hold the same
+// value in every row, so the pending-row means of a step are per class.
 struct ExplicitTimes {
   const double* f;
   const double* b;
   int p;
   __device__ double F(int i, int s) const { return f[static_cast<size_t>(i) * p + s]; }
   __device__ double B(int i, int s) const { return b[static_cast<size_t>(i) * p + s]; }
+  __device__ int col(int s) const { return s; }
+  __device__ int ncols() const { return p; }
 };
 // ...or per-microbatch unit rows (build_stage_times: every stage of a unit
 // carries the unit's value).
@@ -31,6 +35,8 @@ struct RowTimes {
   dtb_plan plan;
   __device__ double F(int i, int s) const { return rows[i * 6 + stage_unit(plan, s)]; }
   __device__ double B(int i, int s) const { return rows[i * 6 + 3 + stage_unit(plan, s)]; }
+  __device__ int col(int s) const { return stage_unit(plan, s); }
+  __device__ int ncols() const { return 3; }
 };
 
 // select_closest (reorder.cpp:136-175) over the pending flags, one pick.
@@ -129,38 +135,34 @@ __device__ int inter_one(const Times& tm, const double* keys, int l, int p,
     double* s_avail = cur + p;
     double* s_prev = s_avail + p;
     double* s_cur = s_prev + p;
-    double* mean_f = s_cur + p;  // [p] lazily filled per step
+    // pending-row means of the current step, per column class (NaN = not
+    // yet computed; valid times are never NaN): [0, ncols) forward,
+    // [ncols, 2 ncols) backward — at most 2p doubles
+    double* mean_c = s_cur + p;
+    const int nc = tm.ncols();
     int Tc = 0;
     double f00_end = 0.0, last_b0_end = 0.0;
     for (int s = 0; s < p; ++s) avail[s] = prev[s] = cur[s] = 0.0;
     int np = nret;
     // candidate row accessors for the current step
-    unsigned mean_valid_f = 0;  // bit s: mean_f[s] computed (p <= 32 fast path)
     auto mean_of = [&](int s, bool fwd) -> double {
       // sequential mean over pending rows in ascending index order
-      double acc = 0.0;
-      for (int idx = 0; idx < l; ++idx)
-        if (pend[idx]) acc += fwd ? tm.F(idx, s) : tm.B(idx, s);
-      return acc / static_cast<double>(npend);
+      // (src/reorder.cpp:191-201), once per class and step
+      double* slot = mean_c + (fwd ? 0 : nc) + tm.col(s);
+      if (isnan(*slot)) {
+        double acc = 0.0;
+        for (int idx = 0; idx < l; ++idx)
+          if (pend[idx]) acc += fwd ? tm.F(idx, s) : tm.B(idx, s);
+        *slot = acc / static_cast<double>(npend);
+      }
+      return *slot;
     };
     auto cand = [&](int r, int s, int ph) -> double {
       if (r < np) {
         const int row = sc.ret[r];
         return ph == DTB_FORWARD ? tm.F(row, s) : tm.B(row, s);
       }
-      if (r < np + npend) {
-        if (ph == DTB_FORWARD) {
-          if (s < 32) {
-            if (!(mean_valid_f >> s & 1u)) {
-              mean_f[s] = mean_of(s, true);
-              mean_valid_f |= 1u << s;
-            }
-            return mean_f[s];
-          }
-          return mean_of(s, true);
-        }
-        return mean_of(s, false);
-      }
+      if (r < np + npend) return mean_of(s, ph == DTB_FORWARD);
       const int row = sc.rear[r - np - npend];
       return ph == DTB_FORWARD ? tm.F(row, s) : tm.B(row, s);
     };
@@ -218,7 +220,7 @@ __device__ int inter_one(const Times& tm, const double* keys, int l, int p,
         s_prev[s] = prev[s];
         s_cur[s] = cur[s];
       }
-      mean_valid_f = 0;
+      for (int c = 0; c < 2 * nc; ++c) mean_c[c] = __longlong_as_double(0x7ff8000000000000ll);
       double sf00 = f00_end, sb0 = last_b0_end, b_start = 0.0;
       auto spec_visit = [&](int s, int i, int ph, double start, double end) {
         if (s != 0) return;
