@@ -28,7 +28,7 @@ FLAGS = [
 if os.environ.get("DTB_DEFINES"):  # experiment builds stay out of the product path
     OBJ = OBJ + "_" + "_".join(os.environ["DTB_DEFINES"].split()).replace("=", "")
     OUT = os.path.join(OBJ, "libdisttrain_b200.so")
-SOURCES = ["capi.cu", "k_cost.cu", "k_intra.cu", "k_sched.cu", "k_inter.cu", "k_inter2.cu", "k_orch.cu",
+SOURCES = ["capi.cu", "k_cost.cu", "k_intra.cu", "k_sched.cu", "k_inter.cu", "k_inter2.cu", "k_inter3.cu", "k_orch.cu",
            "k_misc.cu", "k_exhaustive.cu", "k_ingest.cu", "k_peer.cu"]
 
 

@@ -1164,7 +1164,9 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ia.table = table;
   ia.err = ctx->err;
   const bool inter_tok = mode->inter && inter_tok_applies(ia);
-  const size_t inter_bytes = mode->inter && !inter_tok ? inter_scratch(ia) : 0;
+  // many stages / long sequences: warp per problem, problem in shared memory
+  const bool inter_warp = mode->inter && !inter_tok && inter_warp_applies(ia);
+  const size_t inter_bytes = mode->inter && !inter_tok && !inter_warp ? inter_scratch(ia) : 0;
   CU(scr.alloc(std::max(sim_bytes, inter_bytes), s));
   CU(launch_group_sims(ga, scr.p, s));
   CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, tb, s));
@@ -1180,6 +1182,8 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
       CU(launch_table_fz(tab_eg.as<double4>(), tab_fz.as<double2>(), tsize, s));
       ia.table.fz = tab_fz.as<double2>();
       CU(launch_inter_tok(ia, s));
+    } else if (inter_warp) {
+      CU(launch_inter_warp(ia, s));
     } else {
       CU(launch_inter(ia, scr.p, inter_bytes, s));
     }
@@ -1644,6 +1648,10 @@ dtb_status dtb_solve_subproblem(dtb_context* ctx, const dtb_cost_model* cm,
   a.out = o.as<dtb_candidate>();
   a.block_best = bb.as<dtb_candidate>();
   a.err = ctx->err;
+  DBuf lst;
+  CU(lst.alloc(8ull * n + 16, ctx->stream));
+  a.list = lst.as<long long>();
+  a.list_count = reinterpret_cast<unsigned*>(a.list + n);
   CU(launch_orchestration(a, grid, ctx->stream));
   TRY(download(out, o, n, ctx->stream));
   DevErr e;
@@ -1685,6 +1693,10 @@ static dtb_status search(dtb_context* ctx, const dtb_cost_model* cm,
   a.out = table_dev;
   a.block_best = bb.as<dtb_candidate>();
   a.err = ctx->err;
+  DBuf lst;
+  CU(lst.alloc(8ull * std::max<long long>(mine, 1) + 16, s));
+  a.list = lst.as<long long>();
+  a.list_count = reinterpret_cast<unsigned*>(a.list + std::max<long long>(mine, 1));
   CU(launch_orchestration(a, grid, s));
   CU(launch_best_reduce(bb.as<dtb_candidate>(), grid, best_dev, s));
   if (evaluated_dev)

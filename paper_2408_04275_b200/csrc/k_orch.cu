@@ -267,9 +267,13 @@ __device__ __forceinline__ double objective(const Cont& k, double bound, double*
 
 // solve_subproblem (orchestrator.cpp:303-378) incl. tuple_costs (:65-113)
 // and solve_continuous (:130-209).  Returns an E_* code; fills `out`.
+// screen_only: stop after tuple_costs; a tuple that passes its early
+// infeasibility exits is marked reason = kNeedsSolve (the caller solves it
+// in a second, compacted pass).
+constexpr int kNeedsSolve = -1;
 __device__ int dev_solve(const DevCM& cm, const dtb_workload_stats& stats,
                          const dtb_tuple& t, long long bs, int vpp, int* fail_unit,
-                         dtb_candidate* out) {
+                         dtb_candidate* out, bool screen_only = false) {
   dtb_candidate& r = *out;
   r.tuple = t;
   r.feasible = 0;
@@ -313,6 +317,10 @@ __device__ int dev_solve(const DevCM& cm, const dtb_workload_stats& stats,
   for (int u = 0; u < 3; ++u) floor_sum += floor_g[u];
   if (floor_sum > cm.cluster.total_gpus) {
     r.reason = DTB_REASON_MEMORY_FLOOR;
+    return 0;
+  }
+  if (screen_only) {
+    r.reason = kNeedsSolve;
     return 0;
   }
   // ---- solve_continuous
@@ -417,15 +425,58 @@ __device__ int dev_solve(const DevCM& cm, const dtb_workload_stats& stats,
 
 constexpr int kOrchT = 128;
 
+// Pass 1: tuple_costs of every tuple of the shard.  About a third of the
+// tuples stop there (dp does not divide, activation memory, memory floor);
+// their records are final.  The others are appended to a compact list
+// (warp-aggregated) so the continuous solve runs on full warps.  The order
+// of the list does not matter: the winner is a total-order minimum and
+// records / errors are keyed by tuple index.
+__global__ void __launch_bounds__(kOrchT)
+orch_screen_kernel(OrchArgs a) {
+  const long long stride = static_cast<long long>(gridDim.x) * kOrchT;
+  const long long mine = a.n > a.shard_index
+                             ? (a.n - a.shard_index + a.shard_count - 1) / a.shard_count
+                             : 0;
+  for (long long x0 = blockIdx.x * static_cast<long long>(kOrchT); x0 < mine; x0 += stride) {
+    const long long x = x0 + threadIdx.x;
+    const long long idx = a.shard_index + x * a.shard_count;
+    bool survive = false;
+    if (x < mine) {
+      dtb_candidate c;
+      int unit = 0;
+      const int e = dev_solve(a.cm, a.stats, a.tuples[idx], a.bs, a.vpp, &unit, &c, true);
+      if (e) {
+        dev_fail_ordered(a.err, static_cast<unsigned long long>(idx * 3 + unit), e);
+      } else if (c.reason == kNeedsSolve) {
+        survive = true;
+      } else if (a.out) {
+        a.out[idx] = c;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, survive);
+    unsigned base = 0;
+    if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(a.list_count, static_cast<unsigned>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (survive) a.list[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = idx;
+  }
+}
+
 __global__ void __launch_bounds__(kOrchT)
 orch_kernel(OrchArgs a) {
   __shared__ dtb_candidate s_best[kOrchT];
   const long long stride = static_cast<long long>(gridDim.x) * kOrchT;
   dtb_candidate mine;
   mine.feasible = 0;
+  const long long listed = a.list ? static_cast<long long>(*a.list_count) : 0;
   for (long long x = blockIdx.x * static_cast<long long>(kOrchT) + threadIdx.x;; x += stride) {
-    const long long idx = a.shard_index + x * a.shard_count;
-    if (idx >= a.n) break;
+    long long idx;
+    if (a.list) {
+      if (x >= listed) break;
+      idx = a.list[x];
+    } else {
+      idx = a.shard_index + x * a.shard_count;
+      if (idx >= a.n) break;
+    }
     dtb_candidate c;
     int unit = 0;
     const int e = dev_solve(a.cm, a.stats, a.tuples[idx], a.bs, a.vpp, &unit, &c);
@@ -448,6 +499,11 @@ orch_kernel(OrchArgs a) {
 }
 
 cudaError_t launch_orchestration(const OrchArgs& a, int grid, cudaStream_t stream) {
+  if (a.list != nullptr) {
+    cudaError_t e = cudaMemsetAsync(a.list_count, 0, sizeof(unsigned), stream);
+    if (e != cudaSuccess) return e;
+    orch_screen_kernel<<<grid, kOrchT, 0, stream>>>(a);
+  }
   orch_kernel<<<grid, kOrchT, 0, stream>>>(a);
   return cudaGetLastError();
 }

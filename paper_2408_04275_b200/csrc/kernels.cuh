@@ -294,6 +294,10 @@ cudaError_t launch_inter(const InterArgs& a, void* scratch, size_t bytes,
 // layouts); cudaErrorNotSupported when it does not apply.
 cudaError_t launch_inter_tok(const InterArgs& a, cudaStream_t stream);
 bool inter_tok_applies(const InterArgs& a);
+// Warp per problem, problem resident in shared memory (k_inter3.cu): stream
+// token form, vpp == 1, any stage count, l up to the shared-memory limit.
+bool inter_warp_applies(const InterArgs& a);
+cudaError_t launch_inter_warp(const InterArgs& a, cudaStream_t stream);
 size_t inter_scratch(const InterArgs& a);
 
 // --------------------------------------------------------- orchestration
@@ -308,6 +312,10 @@ struct OrchArgs {
   dtb_candidate* out;                  // per-tuple results or null
   dtb_candidate* block_best;           // [grid] winners
   DevErr* err;
+  // optional compaction (launch_orchestration): list [n] of the tuples that
+  // pass tuple_costs, list_count (device) their number
+  long long* list;
+  unsigned* list_count;
 };
 cudaError_t launch_enumerate(const dtb_cluster_spec& c, long long bs,
                              const long long* divs, int n_divs,

@@ -275,6 +275,8 @@ STREAM_CASES = [  # (n_batches, bs, dp_lm, dp_me, pp triple, inter)
     (6, 4096, 32, 32, (1, 2, 1), False, "dense"),   # greedy kept: counting scatter
     (4, 1000, 8, 8, (1, 2, 1), False, "dense"),     # n % 8 != 0: 32-bit path
     (5, 2048, 16, 16, (1, 2, 1), True, "dense"),
+    (2, 4096, 8, 8, (1, 2, 1), True),      # l = 512 > 255: warp-per-problem inter
+    (2, 1024, 4, 4, (2, 9, 3), True),      # p = 14 > 8: warp-per-problem inter
 ]
 
 
