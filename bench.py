@@ -397,6 +397,19 @@ def main():
         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650",
         "stream": "mixed (BASELINE config 4): the greedy split loses on most batches"}
     if not args.no_extras and world == 1:
+        # descending order (the LPT variant, ReorderMode::sort_order) on the
+        # same stream: the averaging bound does not apply, every batch runs
+        # the histogram greedy and most keep it
+        def sort_partition_desc():
+            pl._check(lib.intra_stream_dev(pl.ctx, BS, DP, 1, C.byref(ds), my_batches,
+                                           ptr(out_order), ptr(lb), ptr(la), ptr(kept), sh))
+        spx = timed(sort_partition_desc, max(3, args.steps // 2), args.warmup)
+        ach_x = algo / (spx / 1e3) / 1e9
+        out["roofline_descending"] = {
+            "bound": "hbm", "kernel": kernels, "achieved": ach_x, "peak": hbm, "unit": "GB/s",
+            "frac": ach_x / hbm, "ms_per_launch": spx,
+            "stream": f"mixed, descending sort order: greedy split kept on "
+                      f"{float(kept.float().mean().item()):.0%} of the batches"}
         # the same path on the dense family (every sample has an image): the
         # greedy split is KEPT on every batch, so the stable sort and the
         # permutation run on all of them

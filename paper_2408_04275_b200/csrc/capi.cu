@@ -1012,6 +1012,7 @@ static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBu
               (fa.aud_off == nullptr || (al(fa.aud_off) && al(fa.aud_tok))) && fa.n % 4 == 0;
   ca.tok16 = const_cast<unsigned short*>(fa.tok16);
   ca.order_out = fa.order_out;
+  ca.tok16_staged = fa.tok16_staged;
   ca.blk_ident = cscr.as<unsigned>();
   ca.bstat = ca.blk_ident + n_batches * fa.m;
   ca.list = ca.bstat + 4 * n_batches;
@@ -1021,6 +1022,7 @@ static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBu
   ca.load_after = fa.load_after;
   ca.kept = fa.kept;
   ca.div_pg = fa.div_pg;
+  ca.err = fa.err;
   e = launch_cost_stream(ca, s);
   if (e != cudaSuccess) return e;
   fa.state = ca.state;

@@ -156,6 +156,107 @@ __device__ __forceinline__ bool chunk_prefix(int* tk, int len, int* tmp) {
   return bad;
 }
 
+// A whole small batch (n <= kSmallN samples, m <= kSmallN groups) in one
+// warp, exactly as the reference: stable order by (cost, index) — descending:
+// (-cost, index) — (src/reorder.cpp:30-42), the equal-count greedy (each
+// item to the least loaded group with room, ties to the lowest group,
+// src/reorder.cpp:70-90; integer loads: exact), its block loads and the
+// keep decision (src/reorder.cpp:340-354).  Batches of a few dozen samples
+// (BASELINE config 2: 32 per iteration) need no partition kernel.
+constexpr int kSmallN = 128;
+__device__ __noinline__ void small_batch(const CostArgs& a, long long b, unsigned short* tk,
+                                         unsigned short* sorted, unsigned* load,
+                                         unsigned char* cnt, unsigned short* flat_of,
+                                         unsigned* blk) {
+  const int n = a.n, m = a.m, lane = threadIdx.x & 31;
+  const long long first = b * n;
+  const bool desc = a.order == DTB_DESCENDING;
+  for (int i = lane; i < n; i += 32) tk[i] = a.tok16[first + i];
+  for (int g = lane; g < m; g += 32) load[g] = 0u, cnt[g] = 0, blk[g] = 0u;
+  __syncwarp();
+  // stable rank of every item
+  for (int i = lane; i < n; i += 32) {
+    const unsigned ki = tk[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) {
+      const unsigned kj = tk[j];
+      r += desc ? (kj > ki || (kj == ki && j < i)) : (kj < ki || (kj == ki && j < i));
+    }
+    sorted[r] = static_cast<unsigned short>(i);
+  }
+  __syncwarp();
+  // equal-count greedy, item by item; the group of every sorted item
+  const int cap = (n + m - 1) / m;
+  unsigned char* group_of = reinterpret_cast<unsigned char*>(flat_of);  // reused below
+  for (int k = 0; k < n; ++k) {
+    const unsigned size = 2u * tk[sorted[k]];
+    unsigned bl = 0xffffffffu;
+    int bg = 0x7fffffff;
+    for (int g = lane; g < m; g += 32)
+      if (cnt[g] < cap && (load[g] < bl || (load[g] == bl && g < bg))) bl = load[g], bg = g;
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      const int og = __shfl_xor_sync(0xffffffffu, bg, o);
+      if (ol < bl || (ol == bl && og < bg)) bl = ol, bg = og;
+    }
+    if (lane == 0) {
+      load[bg] += size;
+      ++cnt[bg];
+      group_of[k] = static_cast<unsigned char>(bg);
+    }
+    __syncwarp();
+  }
+  // flat order (IntraPartition::flat): groups in order, items in sorted order
+  if (lane == 0) {
+    int off = 0;
+    for (int g = 0; g < m; ++g) {
+      const int c = cnt[g];
+      cnt[g] = static_cast<unsigned char>(0);
+      load[g] = static_cast<unsigned>(off);  // group offset (loads are no longer needed)
+      off += c;
+    }
+  }
+  __syncwarp();
+  unsigned short* flat = tk + kSmallN;  // tk[kSmallN .. 2 kSmallN): flat order (sample indices)
+  if (lane == 0)
+    for (int k = 0; k < n; ++k) {
+      const int g = group_of[k];
+      flat[load[g] + cnt[g]] = sorted[k];
+      ++cnt[g];
+    }
+  __syncwarp();
+  // block loads of the greedy flat order and of the identity
+  const int per = n / m;
+  unsigned mg = 0u, mi = 0u;
+  for (int g = lane; g < m; g += 32) {
+    const int lo = g * per, hi = g == m - 1 ? n : lo + per;
+    unsigned sg = 0u, si = 0u;
+    for (int q = lo; q < hi; ++q) {
+      sg += 2u * tk[flat[q]];
+      si += 2u * tk[q];
+    }
+    blk[g] = sg;
+    mg = max(mg, sg);
+    mi = max(mi, si);
+    if (a.load_before) a.load_before[b * m + g] = static_cast<double>(si);
+  }
+  mg = __reduce_max_sync(0xffffffffu, mg);
+  mi = __reduce_max_sync(0xffffffffu, mi);
+  const bool keep = mg <= mi;
+  for (int g = lane; g < m; g += 32) {
+    const int lo = g * per, hi = g == m - 1 ? n : lo + per;
+    unsigned si = 0u;
+    for (int q = lo; q < hi; ++q) si += 2u * tk[q];
+    if (a.load_after) a.load_after[b * m + g] = static_cast<double>(keep ? blk[g] : si);
+  }
+  for (int q = lane; q < n; q += 32) {
+    const int src = keep ? flat[q] : q;
+    a.order_out[first + q] = src;
+    if (a.tok16_staged != nullptr && keep) a.tok16_staged[first + q] = tk[src];
+  }
+  if (lane == 0 && a.kept) a.kept[b] = keep ? 1 : 0;
+}
+
 // Per batch, after the cost pass: identity loads, averaging bound, batch
 // state; batches the partition kernel must process are appended to `list`.
 __global__ void __launch_bounds__(kCostT) cost_finalize_kernel(const __grid_constant__ CostArgs a) {
@@ -184,6 +285,16 @@ __global__ void __launch_bounds__(kCostT) cost_finalize_kernel(const __grid_cons
       if (a.load_before) a.load_before[b * m + g] = l;
       if (a.load_after) a.load_after[b * m + g] = l;
     }
+  } else if (!wide && a.order_out != nullptr && a.n <= kSmallN && m <= kSmallN) {
+    __shared__ unsigned short s_tk[2 * kSmallN], s_sorted[kSmallN], s_flat[kSmallN];
+    __shared__ unsigned s_load[kSmallN], s_blk[kSmallN];
+    __shared__ unsigned char s_cnt[kSmallN];
+    if (tid < 32) small_batch(a, b, s_tk, s_sorted, s_load, s_cnt, s_flat, s_blk);
+    if (tid == 0) {  // decided and all outputs written
+      a.wide_flag[b] = 0u;
+      a.state[b] = kBatchDecided;
+    }
+    return;
   }
   if (tid == 0) {
     if (decided && a.kept) a.kept[b] = 0;
@@ -288,6 +399,10 @@ __device__ __forceinline__ void cost_chunk(const CostArgs& a, CostSmem& S) {
           if (audio)
             for (int y = ao_s[j]; y < ao_s[j + 1]; ++y) t += __ldg(a.aud_tok + y);
         }
+        // the 32-bit path orders 2 * tokens as u32 keys: a negative sum or one
+        // of 2^31 or more is rejected (Sample::valid, src/core.cpp:97, never
+        // admits negative tokens) instead of silently misordered
+        if (t < 0 || t >= (1ll << 31)) dev_fail(a.err, E_COST_RANGE, static_cast<int>(b));
         t4[k] = t < 0 ? 0xffffffffu : t > 0xfffffffell ? 0xfffffffeu : static_cast<unsigned>(t);
       }
     }

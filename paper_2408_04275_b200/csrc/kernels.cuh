@@ -69,6 +69,7 @@ struct CostArgs {
   int staged;  // 16-byte aligned CSR and n % 4 == 0: bulk copies
   unsigned short* tok16;   // [n_batches * n]
   int* order_out;          // [n_batches * n] batch-local identity
+  unsigned short* tok16_staged;  // [n_batches * n] tokens in the kept order (small batches)
   unsigned* blk_ident;     // [n_batches * m]  zeroed
   unsigned* bstat;         // [n_batches * 4]  zeroed: zeros, sum of cost_size, flags, -
   unsigned* list;          // [1 + n_batches]: count (zeroed), batches left to the partition kernel
@@ -78,6 +79,7 @@ struct CostArgs {
   double* load_after;
   unsigned char* kept;     // [n_batches] or null
   FastDiv div_pg;
+  DevErr* err;             // a negative or >= 2^31 token sum (E_COST_RANGE)
 };
 size_t cost_scratch_bytes(long long n_batches, int m);  // blk_ident, bstat, list, state
 cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream);

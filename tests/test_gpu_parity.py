@@ -80,3 +80,19 @@ def test_gpu_config5_chosen_plan(gpu, oracle_best):
     rb = oracle_best.reorder_stream(co, r["best"], s, 1, inter=False)
     for k in ("output_order", "load_before", "load_after", "t_iter_before", "t_iter_after"):
         assert_same(ra[k], rb[k], k)
+
+
+@pytest.mark.gpu
+def test_gpu_rejects_costs_outside_the_key_range(gpu):
+    """A negative modality-token sum (Sample::valid never admits one,
+    src/core.cpp:97) or one of 2^31 or more is reported, not misordered."""
+    from parity_cases import H
+    from paper_2408_04275_b200.api import InvalidArgument, SampleBatch
+    model, cluster, book = H.desk_model(), H.desk_cluster(64), H.desk_book()
+    ci = gpu.cost_model(model, cluster, book)
+    pl = H.plan((1, 2, 1), (1, 2, 2), (1, 2, 1), 8)
+    for bad in (-5, 2**30, 2**30):
+        rows = [(1, [10]), (1, [bad, bad if bad > 0 else 0]), (1, [3])] + [(1, [7])] * 5
+        s = SampleBatch.from_lists(rows)
+        with pytest.raises(InvalidArgument):
+            gpu.reorder_stream(ci, pl, s, 1, inter=False)
