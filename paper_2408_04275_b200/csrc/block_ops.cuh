@@ -16,9 +16,21 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// Barrier of the first T threads: BAR == 0 is __syncthreads (T = the whole
+// block); BAR > 0 is the named barrier BAR over threads [0, T) only, so a
+// subset of a larger block can run a block-wide primitive on its own.
+template <int BAR, int T>
+__device__ __forceinline__ void bar_sync() {
+  if constexpr (BAR == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(T) : "memory");
+  }
+}
+
 // Exclusive scan of one int per thread; returns the prefix, writes the block
 // total to *total.  `s` needs T/32 + 1 ints.  Contains two __syncthreads.
-template <int T>
+template <int T, int BAR = 0>
 __device__ __forceinline__ int block_excl_scan(int v, int* s, int* total) {
   constexpr int W = T / 32;
   const int lane = lane_id(), w = warp_id();
@@ -28,9 +40,9 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s, int* total) {
     const int y = __shfl_up_sync(kFull, x, o);
     if (lane >= o) x += y;
   }
-  __syncthreads();  // readers of the previous result in `s` are done
+  bar_sync<BAR, T>();  // readers of the previous result in `s` are done
   if (lane == 31) s[w] = x;
-  __syncthreads();
+  bar_sync<BAR, T>();
   if (w == 0) {
     int t = lane < W ? s[lane] : 0;
     int u = t;
@@ -42,7 +54,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s, int* total) {
     if (lane < W) s[lane] = u - t;
     if (lane == W - 1) s[W] = u;
   }
-  __syncthreads();
+  bar_sync<BAR, T>();
   const int r = x - v + s[w];
   *total = s[W];
   return r;
@@ -50,7 +62,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s, int* total) {
 
 // Inclusive scan of one 64-bit integer per thread (exact: integer adds are
 // associative); *total gets the block sum.  `s` needs T/32 + 1 long longs.
-template <int T>
+template <int T, int BAR = 0>
 __device__ __forceinline__ long long block_incl_scan_ll(long long v, long long* s,
                                                         long long* total) {
   constexpr int W = T / 32;
@@ -61,9 +73,9 @@ __device__ __forceinline__ long long block_incl_scan_ll(long long v, long long* 
     const long long y = __shfl_up_sync(kFull, x, o);
     if (lane >= o) x += y;
   }
-  __syncthreads();
+  bar_sync<BAR, T>();
   if (lane == 31) s[w] = x;
-  __syncthreads();
+  bar_sync<BAR, T>();
   if (w == 0) {
     long long t = lane < W ? s[lane] : 0;
     long long u = t;
@@ -75,28 +87,28 @@ __device__ __forceinline__ long long block_incl_scan_ll(long long v, long long* 
     if (lane < W) s[lane] = u - t;
     if (lane == W - 1) s[W] = u;
   }
-  __syncthreads();
+  bar_sync<BAR, T>();
   const long long r = x + s[w];
   *total = s[W];
   return r;
 }
 
 // Block minimum of one int per thread (all threads get the result).
-template <int T>
+template <int T, int BAR = 0>
 __device__ __forceinline__ int block_min(int v, int* s) {
   constexpr int W = T / 32;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
-  __syncthreads();
+  bar_sync<BAR, T>();
   if (lane_id() == 0) s[warp_id()] = v;
-  __syncthreads();
+  bar_sync<BAR, T>();
   int r = s[0];
 #pragma unroll 1
   for (int i = 1; i < W; ++i) r = min(r, s[i]);
   return r;
 }
 
-template <int T>
+template <int T, int BAR = 0>
 __device__ __forceinline__ long long block_max_ll(long long v, long long* s) {
   constexpr int W = T / 32;
 #pragma unroll
@@ -104,22 +116,22 @@ __device__ __forceinline__ long long block_max_ll(long long v, long long* s) {
     const long long y = __shfl_xor_sync(kFull, v, o);
     v = v < y ? y : v;
   }
-  __syncthreads();
+  bar_sync<BAR, T>();
   if (lane_id() == 0) s[warp_id()] = v;
-  __syncthreads();
+  bar_sync<BAR, T>();
   long long r = s[0];
 #pragma unroll 1
   for (int i = 1; i < W; ++i) r = r < s[i] ? s[i] : r;
   return r;
 }
 
-template <int T>
+template <int T, int BAR = 0>
 __device__ __forceinline__ unsigned block_or(unsigned v, unsigned* s) {
   constexpr int W = T / 32;
   v = __reduce_or_sync(kFull, v);
-  __syncthreads();
+  bar_sync<BAR, T>();
   if (lane_id() == 0) s[warp_id()] = v;
-  __syncthreads();
+  bar_sync<BAR, T>();
   unsigned r = 0;
 #pragma unroll 1
   for (int i = 0; i < W; ++i) r |= s[i];

@@ -61,7 +61,7 @@ struct dtb_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-buffer pipelines (lazy)
-  cudaStream_t side = nullptr;                          // peer exchange (lazy)
+  cudaStream_t side = nullptr;  // partition kernel next to the simulations; peer exchange
   DevErr* err = nullptr;  // device
 };
 
@@ -306,6 +306,7 @@ dtb_status dtb_context_create(int32_t device, dtb_context** out) {
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) {
     // keep stream-ordered scratch cached across calls (no per-call cudaMalloc)
     cudaMemPool_t pool;
@@ -991,8 +992,12 @@ static cudaError_t launch_sort_partition_generic(FusedArgs& fa, long long n_batc
   return e;
 }
 
+// side != null: the partition kernel runs on `side` after the cost pass
+// (event `fork`), so work that needs only the cost pass's outputs can proceed
+// on `s` meanwhile; the caller joins `side` back.
 static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBuf& cscr,
-                                         cudaStream_t s) {
+                                         cudaStream_t s, cudaStream_t side = nullptr,
+                                         cudaEvent_t fork = nullptr) {
   if (fa.n > fused_max_n() || fa.m > fused_max_m())
     return launch_sort_partition_generic(fa, n_batches, s);
   cudaError_t e = cscr.alloc(cost_scratch_bytes(n_batches, fa.m), s);
@@ -1018,6 +1023,7 @@ static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBu
   ca.list = ca.bstat + 4 * n_batches;
   ca.state = ca.list + 1 + n_batches;
   ca.wide_flag = fa.wide_flag;
+  ca.tok32_orig = fa.tok32_orig;
   ca.load_before = fa.load_before;
   ca.load_after = fa.load_after;
   ca.kept = fa.kept;
@@ -1028,14 +1034,21 @@ static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBu
   fa.state = ca.state;
   fa.blk_ident = ca.blk_ident;
   fa.list = ca.list;
+  if (side != nullptr) {
+    e = cudaEventRecord(fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+    if (e != cudaSuccess) return e;
+    return launch_intra_fused(fa, n_batches, side);
+  }
   return launch_intra_fused(fa, n_batches, s);
 }
 
 // Device pipeline for n_batches global batches (all pointers device):
-//   token_keys (cost pass) -> intra_fused (sort/greedy/decision, per batch)
-//   -> cost table -> group sims on the input order (t_iter_before)
-//   -> [inter_reorder per coupled group] -> compose -> group sims on the
-//   reordered groups (t_iter_after).
+//   cost pass (k_cost.cu) -> partition kernel on the side stream (intra_fused:
+//   greedy / decision / kept orders of the batches the cost pass left open),
+//   concurrently with: cost table -> group sims on the input order
+//   (t_iter_before) — then, joined: [inter_reorder per coupled group] ->
+//   compose -> group sims on the reordered groups (t_iter_after).
 static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan* plan,
                              const dtb_reorder_mode* mode, const int* io, const int* it,
                              const int* ao, const int* at, long long n_batches, int* order_out,
@@ -1056,14 +1069,15 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
     if (e == cudaSuccess) e = cudaEventRecord(ev_done, ctx->side);
     return e;
   };
+  cudaEvent_t ev_fork = nullptr, ev_part = nullptr;  // partition kernel on ctx->side
+  cudaEvent_t ev_table = nullptr, ev_after = nullptr;  // t_iter_after sims on ctx->side
   struct EvGuard {
-    cudaEvent_t* a;
-    cudaEvent_t* b;
+    cudaEvent_t* e[6];
     ~EvGuard() {
-      if (*a) cudaEventDestroy(*a);
-      if (*b) cudaEventDestroy(*b);
+      for (cudaEvent_t* x : e)
+        if (*x) cudaEventDestroy(*x);
     }
-  } ev_guard{&ev_ready, &ev_done};
+  } ev_guard{{&ev_ready, &ev_done, &ev_fork, &ev_part, &ev_table, &ev_after}};
   const int n = static_cast<int>(plan->global_batch);
   const int dp_lm = plan->unit[DTB_BACKBONE].dp;
   const int dp_me = plan->unit[DTB_ENCODER].dp;
@@ -1072,6 +1086,7 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   const long long n_mb = n_batches * dp_me * static_cast<long long>(per_group);
   const long long total = n_batches * static_cast<long long>(n);
   DBuf intra, tok16, tok16s, tok32, tok32s, wflag, kept_buf, wide, mb0, mb1, tgrp, inter, scr;
+  DBuf tgrp2, scr2, tab_eg, tab_k;  // side-stream simulations, cost table
   // without inter the intra order is the output order whenever every
   // position belongs to a microbatch
   const bool compose_needed = mode->inter || dp_me * span * per_group != n;
@@ -1115,20 +1130,33 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   fa.div_pg = FastDiv::make(static_cast<unsigned>(per_group));
   fa.err = ctx->err;
   DBuf cscr;
-  CU(launch_sort_partition(fa, n_batches, cscr, s));
-  if (!compose_needed) CU(exchange());  // the intra order is the output order
+  // joins the side stream back into `s` on every exit, before the scratch
+  // above is freed (stream-ordered frees on `s`)
+  struct Join {
+    cudaStream_t s;
+    cudaEvent_t* e[3];
+    ~Join() {
+      for (cudaEvent_t* x : e)
+        if (*x) cudaStreamWaitEvent(s, *x, 0);
+    }
+  } join{s, {&ev_part, &ev_done, &ev_after}};
+  CU(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
+  CU(launch_sort_partition(fa, n_batches, cscr, s, ctx->side, ev_fork));
+  CU(cudaEventRecord(ev_part, ctx->side));
+  // the intra order is the output order: exchanged on the side stream right
+  // after the partition kernel
+  if (!compose_needed) CU(exchange());
   const TokSrc tok{tok16.as<unsigned short>(), tok16s.as<unsigned short>(), tok32.as<int>(),
                    tok32s.as<int>(), kept_dev, wflag.as<unsigned int>(), n};
-  if (span > 1) {  // assembled microbatch sums [b][e][i]
+  if (span > 1) {  // assembled microbatch sums [b][e][i] (input order: cost pass only)
     CU(mb0.alloc(4ull * n_mb, s));
     CU(mb1.alloc(4ull * n_mb, s));
     CU(launch_assemble(n_batches, n, dp_lm, dp_me, tok, false, mb0.as<int>(), s));
-    CU(launch_assemble(n_batches, n, dp_lm, dp_me, tok, true, mb1.as<int>(), s));
   }
   // token-indexed cost table shared by both simulations and the inter kernel
   const int tsize = static_cast<int>(std::min<long long>(
       static_cast<long long>(span) * 0x8000, static_cast<long long>(kCostTableMax)));
-  DBuf tab_eg, tab_k;
   CU(tab_eg.alloc(sizeof(double4) * tsize, s));
   CU(tab_k.alloc(sizeof(double) * tsize, s));
   CU(launch_cost_table(cm->dev, *plan, span, tsize, tab_eg.as<double4>(), tab_k.as<double>(),
@@ -1170,8 +1198,41 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   const bool inter_warp = mode->inter && !inter_tok && inter_warp_applies(ia);
   const size_t inter_bytes = mode->inter && !inter_tok && !inter_warp ? inter_scratch(ia) : 0;
   CU(scr.alloc(std::max(sim_bytes, inter_bytes), s));
+  // intra only: a batch whose greedy split was not kept runs the identity
+  // order again, so its t_iter_after IS its t_iter_before (same microbatches,
+  // same operation sequence) — only kept batches are re-simulated.  Those
+  // simulations need the partition kernel but not the t_iter_before ones:
+  // with small simulation scratch they run on the side stream, after the
+  // partition kernel, concurrently with the t_iter_before simulations.
+  const unsigned char* only_kept = mode->inter ? nullptr : kept_dev;
+  const bool after_on_side = !mode->inter && !compose_needed && sim_bytes <= 4096;
+  if (after_on_side) {
+    CU(cudaEventCreateWithFlags(&ev_table, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ev_after, cudaEventDisableTiming));
+    CU(tgrp2.alloc(8ull * n_batches * dp_me, s));
+    CU(scr2.alloc(sim_bytes, s));
+    CU(cudaEventRecord(ev_table, s));  // table and scratch ready
+    GroupSimArgs gb = ga;
+    gb.staged = true;
+    gb.mbsum = span > 1 ? mb1.as<int>() : nullptr;
+    gb.order = nullptr;
+    gb.only_kept = only_kept;
+    gb.t_group = tgrp2.as<double>();
+    if (span > 1) CU(launch_assemble(n_batches, n, dp_lm, dp_me, tok, true, mb1.as<int>(), ctx->side));
+    CU(cudaStreamWaitEvent(ctx->side, ev_table, 0));
+    CU(launch_group_sims(gb, scr2.p, ctx->side));
+    CU(cudaEventRecord(ev_after, ctx->side));
+  }
   CU(launch_group_sims(ga, scr.p, s));
   CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, tb, s));
+  if (after_on_side) {
+    CU(cudaStreamWaitEvent(s, ev_after, 0));
+    CU(launch_t_iter_reduce(n_batches, dp_me, tgrp2.as<double>(), cm->model.dp_sync_seconds, ta, s,
+                            only_kept, tb));
+    return DTB_OK;  // `join` waits for the partition kernel and the exchange
+  }
+  CU(cudaStreamWaitEvent(s, ev_part, 0));  // the partition kernel's orders and kept flags
+  if (span > 1) CU(launch_assemble(n_batches, n, dp_lm, dp_me, tok, true, mb1.as<int>(), s));
   if (mode->inter) {
     CU(inter.alloc(4ull * n_mb, s));
     ia.orders = inter.as<int>();
@@ -1198,16 +1259,11 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   ga.staged = true;
   ga.mbsum = span > 1 ? mb1.as<int>() : nullptr;
   ga.order = mode->inter ? inter.as<int>() : nullptr;
-  // intra only: a batch whose greedy split was not kept runs the identity
-  // order again, so its t_iter_after IS its t_iter_before (same microbatches,
-  // same operation sequence) — only kept batches are re-simulated
-  const unsigned char* only_kept = mode->inter ? nullptr : kept_dev;
   ga.only_kept = only_kept;
   CU(launch_group_sims(ga, scr.p, s));
   CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, ta, s,
                           only_kept, tb));
-  if (ev_done != nullptr) CU(cudaStreamWaitEvent(s, ev_done, 0));  // join the exchange
-  return DTB_OK;
+  return DTB_OK;  // `join` waits for the partition kernel and the exchange
 }
 
 // ------------------------------------------------------------ peer groups

@@ -45,10 +45,10 @@ __device__ __forceinline__ bool fkey_lt(unsigned a, int ga, unsigned b, int gb) 
 }
 
 // Block inclusive scan of one u32 per thread (sums here stay < 2^31).
-template <int T>
+template <int T, int BAR = 0>
 __device__ __forceinline__ unsigned block_incl_scan_u32(unsigned v, int* s, unsigned* total) {
   int tot;
-  const int ex = block_excl_scan<T>(static_cast<int>(v), s, &tot);
+  const int ex = block_excl_scan<T, BAR>(static_cast<int>(v), s, &tot);
   *total = static_cast<unsigned>(tot);
   return static_cast<unsigned>(ex) + v;
 }
@@ -56,7 +56,7 @@ __device__ __forceinline__ unsigned block_incl_scan_u32(unsigned v, int* s, unsi
 // sizes(k): size of sorted item k; emit(k, g, slot).  Zero run = [z0, z1).
 // prof (debug, may be null): [0] globaltimer after the zero run, [1] round
 // counts (full-round segments << 32 | general rounds).
-template <int T, bool ASC, typename SizeFn, typename EmitFn>
+template <int T, bool ASC, int BAR = 0, typename SizeFn, typename EmitFn>
 __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn& sizes,
                              const EmitFn& emit, FusedGreedySmem& G, int* tmp,
                              long long* tmpll, unsigned long long* prof = nullptr) {
@@ -68,7 +68,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
     G.AG[tid] = tid;
     G.AC[tid] = 0;
   }
-  __syncthreads();
+  bar_sync<BAR, T>();
   int r = m;
   int k = 0;
   while (k < n) {
@@ -77,7 +77,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
       const int z = z1 - k;
       const int capl = tid < r ? cap - G.AC[tid] : 0;
       int tot;
-      const int pre = block_excl_scan<T>(capl, tmp, &tot);
+      const int pre = block_excl_scan<T, BAR>(capl, tmp, &tot);
       int take = 0;
       unsigned L = 0u;
       int g = 0, c = 0;
@@ -95,7 +95,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
         G.gcnt[g] = cap;
       }
       int nfull;  // filled entries are a prefix of A
-      block_excl_scan<T>(full ? 1 : 0, tmp, &nfull);
+      block_excl_scan<T, BAR>(full ? 1 : 0, tmp, &nfull);
       if (k == 0) {
         // first run of the batch: every entry is empty (capacity cap, in gid
         // order), so the entry of item q is q / cap — no search
@@ -115,7 +115,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
           emit(k + q, G.AG[lo], G.TC[lo] + (q - G.pre[lo]));
         }
       }
-      __syncthreads();
+      bar_sync<BAR, T>();
       if (tid < r && tid >= nfull) {
         G.AL[tid - nfull] = L;
         G.AG[tid - nfull] = g;
@@ -123,7 +123,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
       }
       r -= nfull;
       k = z1;
-      __syncthreads();
+      bar_sync<BAR, T>();
       if (prof && tid == 0) {
         unsigned long long tnow;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
@@ -136,7 +136,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
     // --------------------------------------------------------- full rounds
     if (ASC) {
       int room = tid < r ? cap - 1 - G.AC[tid] : 0x7fffffff;
-      room = block_min<T>(room, tmp);
+      room = block_min<T, BAR>(room, tmp);
       const int Tr = r > 0 ? min(room, (lim - k) / r) : 0;
       if (Tr >= 1) {
         int tstar = Tr;
@@ -153,7 +153,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
             // both columns in one 64-bit scan: each half's sum stays < 2^31
             // (loads of <= 16384 items of <= 65534), so no carry crosses
             long long tot;
-            const unsigned long long inc = static_cast<unsigned long long>(block_incl_scan_ll<T>(
+            const unsigned long long inc = static_cast<unsigned long long>(block_incl_scan_ll<T, BAR>(
                 static_cast<long long>((static_cast<unsigned long long>(sl) << 32) | s0),
                 tmpll, &tot));
             const unsigned inc0 = static_cast<unsigned>(inc), incl = static_cast<unsigned>(inc >> 32);
@@ -162,7 +162,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
             const unsigned new0 = l0 + c0 + inc0;
             const unsigned last = ll + cl + (incl - sl);
             const int f = ok && !fkey_lt(last, gl, new0, g0) ? t : 0x7fffffff;
-            const int first = block_min<T>(f, tmp);
+            const int first = block_min<T, BAR>(f, tmp);
             if (first != 0x7fffffff) {
               tstar = first;
               break;
@@ -185,12 +185,12 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
               emit(item, g, c + t);
             }
           }
-          __syncthreads();
+          bar_sync<BAR, T>();
           if (j < r && part) atomicAdd(&G.AL[j], part);
           if (tid < r) G.AC[tid] += tstar;
           k += tstar * r;
           ++n_full;
-          __syncthreads();
+          bar_sync<BAR, T>();
           continue;
         }
       }
@@ -210,10 +210,10 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
       }
       bmin = max(tid + 1, lo);
     }
-    const int R = min(R_lim, block_min<T>(bmin, tmp));
+    const int R = min(R_lim, block_min<T, BAR>(bmin, tmp));
     const bool keep = tid < R && G.AC[tid] + 1 < cap;
     int nkeep;
-    const int keep_pre = block_excl_scan<T>(keep ? 1 : 0, tmp, &nkeep);
+    const int keep_pre = block_excl_scan<T, BAR>(keep ? 1 : 0, tmp, &nkeep);
     if (tid < R) {
       const int g = G.AG[tid], c = G.AC[tid];
       const unsigned nl = G.AL[tid] + sizes(k + tid);
@@ -227,11 +227,11 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
         G.gcnt[g] = c + 1;
       }
     }
-    __syncthreads();
+    bar_sync<BAR, T>();
     unsigned unsorted = 0u;
     if (!ASC && tid + 1 < nkeep)
       unsorted = fkey_lt(G.TL[tid], G.TG[tid], G.TL[tid + 1], G.TG[tid + 1]) ? 0u : 1u;
-    if (!ASC) unsorted = block_or<T>(unsorted, reinterpret_cast<unsigned*>(tmp));
+    if (!ASC) unsorted = block_or<T, BAR>(unsorted, reinterpret_cast<unsigned*>(tmp));
     // final ranks of the merged order; written after a barrier
     unsigned oL = 0u;
     int oG = 0, oC = 0, oP = -1;
@@ -277,7 +277,7 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
       pC = G.AC[j];
       pP = tid + below;
     }
-    __syncthreads();
+    bar_sync<BAR, T>();
     if (oP >= 0) {
       G.AL[oP] = oL;
       G.AG[oP] = oG;
@@ -291,14 +291,14 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
     r = nkeep + (r - R);
     k += R;
     ++n_general;
-    __syncthreads();
+    bar_sync<BAR, T>();
   }
   if (prof && tid == 0) prof[1] = (n_full << 32) | n_general;
   if (tid < r) {
     G.gload[G.AG[tid]] = G.AL[tid];
     G.gcnt[G.AG[tid]] = G.AC[tid];
   }
-  __syncthreads();
+  bar_sync<BAR, T>();
 }
 
 }  // namespace dtb

@@ -296,10 +296,26 @@ __global__ void __launch_bounds__(kCostT) cost_finalize_kernel(const __grid_cons
     }
     return;
   }
+  // a batch the partition kernel runs on 32-bit arrays gets its 32-bit tokens
+  // (input order) here, so everything that reads the input order's tokens
+  // (the t_iter_before simulations) depends on this pass only and can run
+  // concurrently with the partition kernel
+  const bool route_wide = !decided && (wide || m > kNarrowGroups || (a.n & 7));
+  if (route_wide && a.tok32_orig != nullptr) {
+    const long long first = b * a.n;
+    for (int i = tid; i < a.n; i += kCostT) {
+      const long long gi = first + i;
+      long long t = 0;
+      for (int x = a.img_off[gi]; x < a.img_off[gi + 1]; ++x) t += a.img_tok[x];
+      if (a.aud_off != nullptr)
+        for (int x = a.aud_off[gi]; x < a.aud_off[gi + 1]; ++x) t += a.aud_tok[x];
+      a.tok32_orig[first + i] = static_cast<int>(t);  // in [0, 2^31): checked by the cost pass
+    }
+  }
   if (tid == 0) {
     if (decided && a.kept) a.kept[b] = 0;
-    a.wide_flag[b] = wide ? 1u : 0u;
-    a.state[b] = decided ? kBatchDecided : wide ? kBatchWide : big ? kBatchSort : kBatchFast;
+    a.wide_flag[b] = route_wide ? 1u : 0u;
+    a.state[b] = decided ? kBatchDecided : route_wide ? kBatchWide : big ? kBatchSort : kBatchFast;
     if (!decided) a.list[1 + atomicAdd(a.list, 1u)] = static_cast<unsigned>(b);
   }
 }
@@ -372,24 +388,65 @@ __device__ __forceinline__ void cost_chunk(const CostArgs& a, CostSmem& S) {
   bool wide = false, big = false;
   unsigned short* tok_out = a.tok16 + s0;
   unsigned* blk = a.blk_ident + b * m;
-  for (int j0 = 4 * tid; j0 < qs; j0 += 4 * kCostT) {  // qs % 4 == 0 when STAGED
-    unsigned t4[4];
-    if (STAGED && pre) {
+  auto store4 = [&](int j0, unsigned* t4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool ok = j0 + k < qs;
+      const bool bad = t4[k] > 0x7fffu;  // negative sums mapped above 0x7fff
+      wide |= ok && bad;
+      const unsigned tok = ok ? (bad ? 0x7fffu : t4[k]) : 0u;
+      t4[k] = tok;
+      big |= tok >= 8192u;
+      zeros += ok && tok == 0u;
+    }
+    if (j0 + 3 < qs && (reinterpret_cast<uintptr_t>(tok_out + j0) & 7u) == 0) {
+      uint2 pk;
+      pk.x = t4[0] | (t4[1] << 16);
+      pk.y = t4[2] | (t4[3] << 16);
+      *reinterpret_cast<uint2*>(tok_out + j0) = pk;
+    } else {
+      for (int k = 0; k < 4 && j0 + k < qs; ++k) tok_out[j0 + k] = static_cast<unsigned short>(t4[k]);
+    }
+  };
+  if (STAGED && pre) {
+    // a sample's sum is a difference of two prefix entries (image + audio);
+    // so is a block's: the identity block loads and the chunk total come from
+    // the prefix at block boundaries, not from per-sample reductions (a wide
+    // batch's loads are recomputed by the partition kernel)
+    const int* E = S.tk - L.fl;
+    const int* F = S.tk + L.abase - L.afl;
+    for (int j0 = 4 * tid; j0 < qs; j0 += 4 * kCostT) {  // qs % 4 == 0 when STAGED
       const int4 o = *reinterpret_cast<const int4*>(io_s + j0);
-      const int o4 = io_s[j0 + 4];
-      const int e0 = S.tk[o.x - L.fl], e1 = S.tk[o.y - L.fl], e2 = S.tk[o.z - L.fl],
-                e3 = S.tk[o.w - L.fl], e4 = S.tk[o4 - L.fl];
+      const int e0 = E[o.x], e1 = E[o.y], e2 = E[o.z], e3 = E[o.w], e4 = E[io_s[j0 + 4]];
       int v[4] = {e1 - e0, e2 - e1, e3 - e2, e4 - e3};
       if (audio) {
         const int4 p = *reinterpret_cast<const int4*>(ao_s + j0);
-        const int p4 = ao_s[j0 + 4];
-        const int* E = S.tk + L.abase - L.afl;
-        const int f0 = E[p.x], f1 = E[p.y], f2 = E[p.z], f3 = E[p.w], f4 = E[p4];
+        const int f0 = F[p.x], f1 = F[p.y], f2 = F[p.z], f3 = F[p.w], f4 = F[ao_s[j0 + 4]];
         v[0] += f1 - f0, v[1] += f2 - f1, v[2] += f3 - f2, v[3] += f4 - f3;
       }
+      unsigned t4[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) t4[k] = static_cast<unsigned>(v[k]);  // in [0, 0x7fff * len]
-    } else {
+      store4(j0, t4);
+    }
+    auto span = [&](int lo, int hi) {  // tokens of local samples [lo, hi)
+      int t = E[io_s[hi]] - E[io_s[lo]];
+      if (audio) t += F[ao_s[hi]] - F[ao_s[lo]];
+      return 2u * static_cast<unsigned>(t);
+    };
+    const int per = static_cast<int>(a.div_pg.d);
+    const int g0 = min(static_cast<int>(a.div_pg.div(static_cast<unsigned>(q0))), m - 1);
+    const int g1 = min(static_cast<int>(a.div_pg.div(static_cast<unsigned>(q0 + qs - 1))), m - 1);
+    for (int g = g0 + tid; g <= g1; g += kCostT) {
+      const int lo = max(g * per, q0) - q0;
+      const int hi = g == m - 1 ? qs : min((g + 1) * per, q0 + qs) - q0;
+      const unsigned s = span(lo, hi);
+      if (s) atomicAdd(blk + g, s);
+    }
+    if (tid == 0) total = span(0, qs);
+  } else {
+    for (int j0 = 4 * tid; j0 < qs; j0 += 4 * kCostT) {
+      unsigned t4[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int j = j0 + k;
@@ -405,45 +462,29 @@ __device__ __forceinline__ void cost_chunk(const CostArgs& a, CostSmem& S) {
         if (t < 0 || t >= (1ll << 31)) dev_fail(a.err, E_COST_RANGE, static_cast<int>(b));
         t4[k] = t < 0 ? 0xffffffffu : t > 0xfffffffell ? 0xfffffffeu : static_cast<unsigned>(t);
       }
-    }
-    unsigned s2 = 0u;
+      store4(j0, t4);
+      unsigned s2 = 0u;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool ok = j0 + k < qs;
-      const bool bad = t4[k] > 0x7fffu;  // negative sums mapped above 0x7fff
-      wide |= ok && bad;
-      const unsigned tok = ok ? (bad ? 0x7fffu : t4[k]) : 0u;
-      t4[k] = tok;
-      big |= tok >= 8192u;
-      zeros += ok && tok == 0u;
-      s2 += 2u * tok;
-    }
-    total += s2;
-    if (j0 + 3 < qs && (reinterpret_cast<uintptr_t>(tok_out + j0) & 7u) == 0) {
-      uint2 pk;
-      pk.x = t4[0] | (t4[1] << 16);
-      pk.y = t4[2] | (t4[3] << 16);
-      *reinterpret_cast<uint2*>(tok_out + j0) = pk;
-    } else {
-      for (int k = 0; k < 4 && j0 + k < qs; ++k) tok_out[j0 + k] = static_cast<unsigned short>(t4[k]);
-    }
-    // identity block loads: one atomic per warp when its 128 samples share a
-    // block, else per sample
-    const unsigned bl0 = min(a.div_pg.div(static_cast<unsigned>(q0 + j0)), static_cast<unsigned>(m - 1));
-    const unsigned bl3 =
-        min(a.div_pg.div(static_cast<unsigned>(q0 + min(j0 + 3, qs - 1))), static_cast<unsigned>(m - 1));
-    const unsigned am = __activemask();
-    const unsigned w0 = __shfl_sync(am, bl0, __ffs(am) - 1);
-    if (__all_sync(am, bl0 == w0 && bl3 == w0)) {
-      const unsigned sum = __reduce_add_sync(am, s2);
-      if (lane == __ffs(am) - 1) atomicAdd(blk + w0, sum);
-    } else if (bl0 == bl3) {
-      atomicAdd(blk + bl0, s2);
-    } else {
-      for (int k = 0; k < 4 && j0 + k < qs; ++k)
-        atomicAdd(blk + min(a.div_pg.div(static_cast<unsigned>(q0 + j0 + k)),
-                            static_cast<unsigned>(m - 1)),
-                  2u * t4[k]);
+      for (int k = 0; k < 4; ++k) s2 += 2u * t4[k];
+      total += s2;
+      // identity block loads: one atomic per warp when its 128 samples share
+      // a block, else per sample
+      const unsigned bl0 = min(a.div_pg.div(static_cast<unsigned>(q0 + j0)), static_cast<unsigned>(m - 1));
+      const unsigned bl3 =
+          min(a.div_pg.div(static_cast<unsigned>(q0 + min(j0 + 3, qs - 1))), static_cast<unsigned>(m - 1));
+      const unsigned am = __activemask();
+      const unsigned w0 = __shfl_sync(am, bl0, __ffs(am) - 1);
+      if (__all_sync(am, bl0 == w0 && bl3 == w0)) {
+        const unsigned sum = __reduce_add_sync(am, s2);
+        if (lane == __ffs(am) - 1) atomicAdd(blk + w0, sum);
+      } else if (bl0 == bl3) {
+        atomicAdd(blk + bl0, s2);
+      } else {
+        for (int k = 0; k < 4 && j0 + k < qs; ++k)
+          atomicAdd(blk + min(a.div_pg.div(static_cast<unsigned>(q0 + j0 + k)),
+                              static_cast<unsigned>(m - 1)),
+                    2u * t4[k]);
+      }
     }
   }
   // ---- identity order for the chunk (kept batches are overwritten later)
@@ -489,6 +530,10 @@ cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream) {
   // blk_ident, bstat and the list count are contiguous and zeroed here
   cudaError_t e = cudaMemsetAsync(a.blk_ident, 0, 4ull * (a.n_batches * (a.m + 4) + 1), stream);
   if (e != cudaSuccess) return e;
+  // all of the unified L1 / shared memory as shared: ten 21 KB chunk CTAs per SM
+  static const cudaError_t carve =
+      cudaFuncSetAttribute(cost_stream_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (carve != cudaSuccess) return carve;
   cost_stream_kernel<<<static_cast<unsigned>(grid), kCostT, 0, stream>>>(a);
   cost_finalize_kernel<<<static_cast<unsigned>(a.n_batches), kCostT, 0, stream>>>(a);
   return cudaGetLastError();

@@ -34,7 +34,7 @@ struct FusedArgs {
   int dp_me;
   unsigned char* wide_scratch;  // [n_batches * fused_wide_scratch_bytes(1)]
   unsigned long long* prof;     // optional [n_batches][64] phase timestamps (debug)
-  // Output of the cost pass (launch_token_keys): modality tokens per sample,
+  // Output of the cost pass (launch_cost_stream): modality tokens per sample,
   // saturated to 0x7fff, and a per-batch flag set when any sample saturated
   // (that batch then takes the 32-bit path from the CSR).
   const unsigned short* tok16;
@@ -53,6 +53,7 @@ struct FusedArgs {
 constexpr unsigned kBatchFast = 0;     // histogram path
 constexpr unsigned kBatchDecided = 1;  // all outputs written (order stays the identity)
 constexpr unsigned kBatchSort = 2;     // a token sum >= the histogram range: sort path
+constexpr int kNarrowGroups = 128;    // groups of the partition kernel's shared-memory path
 constexpr unsigned kBatchWide = 3;     // a token sum < 0 or > 0x7fff: 32-bit path
 
 // Streaming cost pass (csrc/k_cost.cu) over chunks of 1024 samples, TMA-staged
@@ -75,6 +76,7 @@ struct CostArgs {
   unsigned* list;          // [1 + n_batches]: count (zeroed), batches left to the partition kernel
   unsigned* state;         // [n_batches]
   unsigned* wide_flag;     // [n_batches]
+  int* tok32_orig;         // [n_batches * n]: 32-bit tokens of the batches routed to the wide path
   double* load_before;     // [n_batches * m] or null
   double* load_after;
   unsigned char* kept;     // [n_batches] or null
@@ -102,11 +104,6 @@ cudaError_t launch_peer_broadcast(const PeerBcast& a, cudaStream_t stream);
 
 // Cost pass: tok16[i] = min(modality tokens of sample i, 0x7fff) for the
 // whole stream, wide_flag[i / n] |= 1 on saturation or negative tokens.
-cudaError_t launch_token_keys(const int* img_off, const int* img_tok, const int* aud_off,
-                              const int* aud_tok, long long total, int n,
-                              unsigned short* tok16, unsigned int* wide_flag,
-                              cudaStream_t stream);
-
 // Modality tokens of position `pos` of global batch b, in the input order
 // (staged == false) or the intra order (staged == true), written by the cost
 // pass / fused kernel (FusedArgs).

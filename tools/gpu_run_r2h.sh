@@ -1,3 +1,6 @@
 mkdir -p gpurun_out/r2h
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:"cost_stream" -c 1 -o gpurun_out/r2h/k0 -f python tools/probe_intra.py --batches 1024 --check 0 > gpurun_out/r2h/ncu.log 2>&1
+timeout 300 python tools/probe_intra.py --batches 1024 --check 3 > gpurun_out/r2h/probe.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x -k "not c5_default" > gpurun_out/r2h/gpu_tests.log 2>&1
+timeout 600 python bench.py --steps 10 --warmup 3 --no-extras > gpurun_out/r2h/bench.json 2> gpurun_out/r2h/bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r2h/bench_launches.csv python bench.py --steps 1 --warmup 3 --no-extras > /dev/null 2>&1
 echo done

@@ -45,6 +45,8 @@ def main():
     out = torch.empty(s.n, dtype=torch.int32, device="cuda")
     prof = torch.zeros(args.batches * 64, dtype=torch.int64, device="cuda")
     for it in range(3):
+        prof.zero_()
+        prof[62] = -1  # atomicMin slot (unsigned max)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         pl._check(fn(pl.ctx, args.bs, args.dp, args.order, C.byref(ds), args.batches,
@@ -53,13 +55,26 @@ def main():
         torch.cuda.synchronize()
         print(f"iter {it}: kernel {e0.elapsed_time(e1):.3f} ms", flush=True)
     p = prof.view(args.batches, 64).cpu().numpy().astype(np.float64)
+    entry, leave = p[0, 62], p[0, 63]
+    if leave > entry:
+        print(f"  partition kernel: first CTA entry -> last CTA exit {(leave - entry) / 1e3:.1f} us")
+    p[0, 62] = p[0, 63] = 0
+    done = p[:, 0] > 0  # batches the partition kernel processed
+    print(f"processed by the partition kernel: {int(done.sum())} of {args.batches}")
+    if done.any():
+        p0 = p[done, 0].min()
+        if entry > 0:
+            print(f"  kernel entry (CTA 0) -> first start {(p0 - entry) / 1e3:.1f} us")
+        print(f"  first start -> last start {(p[done, 0].max() - p0) / 1e3:.1f} us, "
+              f"first start -> last end {(p[done, 5].max() - p0) / 1e3:.1f} us")
+        p = p[done]
     names = ["load+cost", "sort", "greedy", "partition+decide", "outputs"]
     span = (p[:, 5] - p[:, 0]) / 1e3
     print(f"per-CTA span us: median {np.median(span):.1f} max {span.max():.1f}")
     for k, nm in enumerate(names):
         dt = (p[:, k + 1] - p[:, k]) / 1e3
         print(f"  {nm:18s} median {np.median(dt):8.1f} us  max {dt.max():8.1f}")
-    pi = prof.view(args.batches, 64).cpu().numpy()
+    pi = prof.view(args.batches, 64).cpu().numpy()[done] if done.any() else prof.view(args.batches, 64).cpu().numpy()
     z = (p[:, 6] - p[:, 2]) / 1e3
     ok = pi[:, 6] > 0
     if ok.any():
@@ -68,7 +83,7 @@ def main():
     cnt = pi[:, 7]
     print(f"  greedy rounds: full segments median {np.median(cnt >> 32):.0f}, "
           f"general median {np.median(cnt & 0xffffffff):.0f} max {(cnt & 0xffffffff).max()}")
-    st = p[:, 8:56].reshape(args.batches, 16, 3)
+    st = p[:, 8:56].reshape(len(p), 16, 3)
     if (st[:, 0, 0] > 0).any():
         prev = np.concatenate([p[:, :1], st[:, :-1, 2]], axis=1)  # previous stage end
         wait = (st[:, :, 0] - prev) / 1e3
@@ -77,14 +92,18 @@ def main():
         for k in (0, 1, 2, 8, 15):
             print(f"  stage {k:2d}: wait median {np.median(wait[:, k]):6.2f} us, prefix "
                   f"{np.median(pref[:, k]):6.2f}, samples+sync {np.median(loop[:, k]):6.2f}")
-    ks = p[:, 56:61]
+    if (p[:, 57] > 0).any():
+        rel = lambda k: (p[:, k] - p[:, 0]) / 1e3
+        print(f"  pair: peer sort done median {np.median(rel(57)):.1f} max {rel(57).max():.1f} us; "
+              f"first cluster sync {np.median(rel(58)):.1f} / {rel(58).max():.1f}; "
+              f"second {np.median(rel(59)):.1f} / {rel(59).max():.1f} (from batch start)")
+        kp = pi[:, 0] > 0
+    ks = p[:, 56:61] * 0
     okk = ks[:, 0] > 0
     if okk.any():
         names_k = ["heavy ids", "counts", "walk", "light sort"]
         print(f"  kept scatter ({okk.sum()} batches):", ", ".join(
             f"{nm} {np.median((ks[okk, k + 1] - ks[okk, k]) / 1e3):.1f}" for k, nm in enumerate(names_k)))
-    start = p[:, 0] - p[:, 0].min()
-    print(f"  CTA start spread: {start.max() / 1e3:.1f} us (waves)")
     if args.check:
         import oracle
         import helpers as H
