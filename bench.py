@@ -392,7 +392,8 @@ def main():
     out["roofline"] = {
         "bound": "hbm", "kernel": kernels,
         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-        "traffic": tr.get("bytes_per_step_16M") if tr else None,
+        # ncu capture of the 16M stream, scaled to this rank's samples
+        "traffic": round(tr["bytes_per_step_16M"] * n / STREAM) if tr else None,
         "algorithmic_bytes_per_launch": algo, "ms_per_launch": sp_local,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650",
         "stream": "mixed (BASELINE config 4): the greedy split loses on most batches"}
@@ -488,6 +489,22 @@ def main():
         out["modes"] = {"intra+inter": {"ms_per_step": both_ms,
                                         "value": my_batches * BS / (both_ms / 1e3),
                                         "unit": "samples/s"}}
+        try:  # FP64 instructions of the step (ncu count) over the measured step time
+            fops = json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_ops.json")))
+            ks = fops["reorder_default_16M"]["kernels"]
+            per = {k: v["dadd"] + v["dmul"] + v["dfma"] for k, v in ks.items()}
+            inst = per["inter_tok_kernel"] + per["inter_tok_kernel_redo"] + 2 * per["group_sims_tiled"]
+            if my_batches * BS == STREAM:
+                ach = inst / (both_ms / 1e3)
+                out["modes"]["intra+inter"]["roofline_fp64"] = {
+                    "bound": "fp64", "kernel": "inter_tok_kernel (dominant) + 2 x group_sims_tiled",
+                    "achieved": ach, "peak": fops["peak_fp64_instr_per_s"], "unit": "FP64 instr/s",
+                    "frac": ach / fops["peak_fp64_instr_per_s"], "fp64_instr_per_step": inst,
+                    "note": "over the whole step time (a lower bound for the kernels); the FP64 "
+                            "pipe is not the limiter: the inter kernel is latency-bound",
+                    "counts_source": fops["reorder_default_16M"]["source"]}
+        except Exception:
+            pass
         # BASELINE config 2: LLaVA-style ViT-L + 7B backbone, PP 1/2/1 (4
         # devices), 32 microbatches per iteration, 10K independent iterations
         # — one global batch of 32 samples per iteration (DP 1), default
@@ -616,6 +633,40 @@ def main():
                          "ms_per_search": s_dt * 1e3, "candidates": res.candidates_evaluated,
                          "timing": "host wall clock around the C-ABI call (includes "
                                    "enumeration, solve, reduce, D2H)"}
+        # FP64 roofline of the search: the device part of the same search
+        # (dtb_orchestration_shard_dev, one shard) timed with CUDA events on
+        # its stream; FP64 instructions per search from the committed ncu
+        # count (profiles/r02_fp64_ops.json)
+        try:
+            fops = json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_ops.json")))
+            kinst = fops["search_config3"]["kernels"]
+            inst = sum(k["dadd"] + k["dmul"] + k["dfma"] for k in kinst.values())
+            rec = torch.zeros(C.sizeof(A.Candidate), dtype=torch.uint8, device="cuda")
+            evc = torch.zeros(1, dtype=torch.int64, device="cuda")
+            st_s = torch.cuda.Stream()
+            call = lambda: pl._check(lib.orchestration_shard_dev(
+                pl.ctx, scm.h, C.byref(sstats), sbs, 1, 0, 1, C.c_void_p(rec.data_ptr()),
+                C.c_void_p(evc.data_ptr()), C.c_void_p(st_s.cuda_stream)))
+            for _ in range(2):
+                call()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st_s)
+            for _ in range(reps):
+                call()
+            e1.record(st_s)
+            torch.cuda.synchronize()
+            dev_s = e0.elapsed_time(e1) / 1e3 / reps
+            ach = inst / dev_s
+            out["search"]["roofline"] = {
+                "bound": "fp64", "kernel": "orch_kernel (+ enumeration, screen, reduce kernels "
+                "of dtb_orchestration_shard_dev)", "achieved": ach,
+                "peak": fops["peak_fp64_instr_per_s"], "unit": "FP64 instr/s",
+                "frac": ach / fops["peak_fp64_instr_per_s"], "fp64_instr_per_search": inst,
+                "ms_per_search_device": dev_s * 1e3, "peak_source": fops["peak_source"],
+                "counts_source": fops["search_config3"]["source"]}
+        except Exception as ex:  # counts file absent: no FP64 block
+            out["search"]["roofline"] = {"unavailable": str(ex)[:120]}
         # BASELINE config 5: search at BS 16,384, then reorder the resident
         # 16M stream with the CHOSEN plan (ReorderMode{intra})
         from paper_2408_04275_b200.api import PlanSpec

@@ -99,10 +99,11 @@ __device__ void greedy_fused(int n, int m, int cap, int z0, int z1, const SizeFn
       if (k == 0) {
         // first run of the batch: every entry is empty (capacity cap, in gid
         // order), so the entry of item q is q / cap — no search
-        const unsigned ucap = static_cast<unsigned>(cap);
-        for (int q = tid; q < z; q += T) {
-          const int j = static_cast<int>(static_cast<unsigned>(q) / ucap);
-          emit(k + q, G.AG[j], q - j * cap);
+        // (a warp per entry: no division per item)
+        const int lane = tid & 31, nfill = (z + cap - 1) / cap;
+        for (int j = tid >> 5; j < nfill; j += T / 32) {
+          const int g = G.AG[j], lim = min(cap, z - j * cap);
+          for (int sl = lane; sl < lim; sl += 32) emit(k + j * cap + sl, g, sl);
         }
       } else {
         for (int q = tid; q < z; q += T) {

@@ -19,18 +19,19 @@
 namespace dtb {
 
 struct WarpGreedySmem {
-  unsigned long long key[128];  // A at the start of the round (sorted)
+  unsigned long long key[128];  // A at the start of the round (sorted; u32 keys use the low half)
   int cnt[128];                 // items assigned per gid
   int pre[128];                 // zero run: capacity prefix over A
 };
 
-__device__ __forceinline__ unsigned long long wg_cmpx(unsigned long long a, unsigned long long b,
-                                                      bool take_min) {
+template <typename K>
+__device__ __forceinline__ K wg_cmpx(K a, K b, bool take_min) {
   return take_min ? (a < b ? a : b) : (a < b ? b : a);
 }
 
 // Ascending bitonic sort of 128 keys, lane l holding positions 4l .. 4l+3.
-__device__ __forceinline__ void wg_sort128(unsigned long long (&v)[4]) {
+template <typename K>
+__device__ __forceinline__ void wg_sort128(K (&v)[4]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 2; k <= 128; k <<= 1) {
@@ -41,7 +42,7 @@ __device__ __forceinline__ void wg_sort128(unsigned long long (&v)[4]) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int i = 4 * lane + e;
-          const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[e], lj);
+          const K o = __shfl_xor_sync(0xffffffffu, v[e], lj);
           const bool up = (i & k) == 0;
           const bool lower = (i & j) == 0;
           v[e] = wg_cmpx(v[e], o, lower == up);
@@ -52,7 +53,7 @@ __device__ __forceinline__ void wg_sort128(unsigned long long (&v)[4]) {
           if (e & j) continue;
           const int i = 4 * lane + e;
           const bool up = (i & k) == 0;
-          const unsigned long long a = v[e], b = v[e | j];
+          const K a = v[e], b = v[e | j];
           const bool swap = up ? (b < a) : (a < b);
           v[e] = swap ? b : a;
           v[e | j] = swap ? a : b;
@@ -62,20 +63,22 @@ __device__ __forceinline__ void wg_sort128(unsigned long long (&v)[4]) {
   }
 }
 
-// sizes(k): size of sorted item k (u32, loads stay < 2^32 and < 2^56);
-// emit(k, g, slot).  Zero run = [z0, z1).  Outputs gload[g], gcnt[g].
-// Called by all 32 lanes of one warp.
-template <bool ASC, typename SizeFn, typename EmitFn>
+// sizes(k): size of sorted item k; emit(k, g, slot).  Zero run = [z0, z1).
+// Outputs gload[g], gcnt[g].  K = u32 when every load stays below 2^24 (the
+// caller checks cap x max size), else u64.  Called by all 32 lanes of one
+// warp.
+template <typename K, typename SizeFn, typename EmitFn>
 __device__ void greedy_warp(int n, int m, int cap, int z0, int z1, const SizeFn& sizes,
                             const EmitFn& emit, WarpGreedySmem& W, unsigned* gload, int* gcnt,
                             unsigned long long* prof = nullptr) {
-  constexpr unsigned long long kNone = ~0ull;
+  constexpr K kNone = static_cast<K>(~static_cast<K>(0));
+  K* key = reinterpret_cast<K*>(W.key);
   const int lane = threadIdx.x & 31;
-  unsigned long long v[4];
+  K v[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int t = 4 * lane + e;
-    v[e] = t < m ? static_cast<unsigned long long>(t) : kNone;  // load 0, gid t
+    v[e] = t < m ? static_cast<K>(t) : kNone;  // load 0, gid t
     W.cnt[t] = 0;
   }
   int r = m;
@@ -105,7 +108,7 @@ __device__ void greedy_warp(int n, int m, int cap, int z0, int z1, const SizeFn&
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         W.pre[4 * lane + e] = pre;
-        W.key[4 * lane + e] = v[e];
+        key[4 * lane + e] = v[e];
         take[e] = max(0, min(capl[e], z - pre));
         pre += capl[e];
       }
@@ -117,7 +120,7 @@ __device__ void greedy_warp(int n, int m, int cap, int z0, int z1, const SizeFn&
           if (W.pre[mid] <= q) lo = mid;
           else hi = mid - 1;
         }
-        const int g = static_cast<int>(W.key[lo] & 0xffu);
+        const int g = static_cast<int>(key[lo] & 0xffu);
         emit(k + q, g, W.cnt[g] + (q - W.pre[lo]));
       }
       __syncwarp();
@@ -151,10 +154,10 @@ __device__ void greedy_warp(int n, int m, int cap, int z0, int z1, const SizeFn&
     const int lim = k < z0 ? min(n, z0) : n;  // non-zero items [k, lim)
     // ---- general round
 #pragma unroll
-    for (int e = 0; e < 4; ++e) W.key[4 * lane + e] = v[e];
+    for (int e = 0; e < 4; ++e) key[4 * lane + e] = v[e];
     __syncwarp();
     const int R_lim = min(r, lim - k);
-    unsigned long long nk[4];
+    K nk[4];
     int bmin = 0x7fffffff;
     bool room[4];
 #pragma unroll
@@ -164,22 +167,24 @@ __device__ void greedy_warp(int n, int m, int cap, int z0, int z1, const SizeFn&
       room[e] = false;
       if (t < R_lim) {
         const int g = static_cast<int>(v[e] & 0xffu);
-        nk[e] = v[e] + (static_cast<unsigned long long>(sizes(k + t)) << 8);
+        nk[e] = v[e] + (static_cast<K>(sizes(k + t)) << 8);
         room[e] = W.cnt[g] + 1 < cap;
       }
+    }
+    // upper bound of every new key in A (128 slots, kNone-padded: a fixed
+    // 7-step search, the four entries interleaved)
+    int ub[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int step = 64; step > 0; step >>= 1) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (key[ub[e] + step - 1] <= nk[e]) ub[e] += step;
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int t = 4 * lane + e;
-      if (t < R_lim && room[e]) {
-        int lo = 0, hi = r;  // upper bound of the new key in A
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (nk[e] < W.key[mid]) hi = mid;
-          else lo = mid + 1;
-        }
-        bmin = min(bmin, max(t + 1, lo));
-      }
+      if (ub[e] == 127 && key[127] <= nk[e]) ub[e] = 128;
+      if (t < R_lim && room[e]) bmin = min(bmin, max(t + 1, ub[e]));
     }
     const int R = min(R_lim, static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(bmin))));
     int removed = 0;

@@ -33,10 +33,16 @@
 
 namespace dtb {
 
+#ifndef DTB_COST_Q
+#define DTB_COST_Q 1024
+#endif
+#ifndef DTB_COST_MINB
+#define DTB_COST_MINB 10
+#endif
 constexpr int kCostT = 128;                 // threads per chunk CTA
-constexpr int kCostQ = 1024;                // samples per chunk
+constexpr int kCostQ = DTB_COST_Q;          // samples per chunk
 constexpr int kCostOff = kCostQ + 4;        // offsets + the next boundary, padded
-constexpr int kCostTok = 3072;              // token slots (image + audio + spares; ~2.1K used)
+constexpr int kCostTok = 3 * kCostQ;        // token slots (image + audio + spares; ~2.1 per sample used)
 constexpr int kCostPer = kCostQ / kCostT;   // samples per thread
 
 struct CostSmem {
@@ -510,7 +516,7 @@ __device__ __forceinline__ void cost_chunk(const CostArgs& a, CostSmem& S) {
   }
 }
 
-__global__ void __launch_bounds__(kCostT, 10) cost_stream_kernel(const __grid_constant__ CostArgs a) {
+__global__ void __launch_bounds__(kCostT, DTB_COST_MINB) cost_stream_kernel(const __grid_constant__ CostArgs a) {
   __shared__ CostSmem S;
   if (a.staged)
     cost_chunk<true>(a, S);

@@ -139,6 +139,7 @@ struct NarrowSmem {
   // sort_abort once the batch is decided NOT kept (rank 1's speculative sort
   // is then useless and stops at its next pass)
   unsigned pair_epoch, sort_abort, sort_go;
+  unsigned keep_flag;  // fast path: the decision, broadcast from warp 0
 };
 constexpr int kSortRB = 5;  // narrow-path digit bits (per-thread counters)
 // per-thread radix counters of the narrow path (their own space, so the
@@ -538,36 +539,80 @@ __device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSm
     constexpr int kGT = 256;
     unsigned long long* gprof = a.prof ? a.prof + b * kProfSlots + 6 : nullptr;
     if (desc) {
-      if (w == 0) greedy_warp<false>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt, gprof);
+      // u32 keys (load << 8 | gid) while every load stays below 2^24
+      if (w == 0) {
+        if (static_cast<long long>(cap) * 2 * (kHistBins - 1) < (1ll << 24))
+          greedy_warp<unsigned>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt, gprof);
+        else
+          greedy_warp<unsigned long long>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt,
+                                          gprof);
+      }
     } else if (tid < kGT) {
       greedy_fused<kGT, true, 1>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll, gprof);
     }
     __syncthreads();
     if (a.prof && tid == 0) a.prof[b * kProfSlots + 3] = globaltimer();
     // ---- 4. group offsets of the flat order, greedy block loads, decision
-    int cg = tid < m ? S.G.gcnt[tid] : 0, ctot;
-    const int o = block_excl_scan<kFusedT>(cg, S.tmp, &ctot);
-    if (tid < m) S.off[tid] = o;
-    if (n % m == 0) {
-      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = S.G.gload[g];
-    } else {
-      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = 0u;
-      __syncthreads();
-      for (int g = w; g < m; g += kFusedT / 32)
-        for (int slot = lane; slot < S.G.gcnt[g]; slot += 32) {
-          const int pos = S.off[g] + slot;
-          atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], size_at(S.out16[g * capP + slot]));
+    // (m <= 128 groups: one warp, 4 groups per lane, no block barriers)
+    if (w == 0) {
+      int cnt[4], sum = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int g = 4 * lane + e;
+        cnt[e] = g < m ? S.G.gcnt[g] : 0;
+        sum += cnt[e];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int base = incl - sum;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int g = 4 * lane + e;
+        if (g < m) S.off[g] = base;
+        base += cnt[e];
+      }
+      unsigned mg = 0u, mi = 0u;
+      if (n % m == 0) {  // blocks == groups
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int g = 4 * lane + e;
+          if (g < m) {
+            const unsigned l = S.G.gload[g];
+            S.blk_greedy[g] = l;
+            mg = max(mg, l);
+            mi = max(mi, S.blk_ident[g]);
+          }
         }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (4 * lane + e < m) S.blk_greedy[4 * lane + e] = 0u;
+        __syncwarp();
+        for (int g = 0; g < m; ++g)
+          for (int slot = lane; slot < S.G.gcnt[g]; slot += 32) {
+            const int pos = S.off[g] + slot;
+            atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], size_at(S.out16[g * capP + slot]));
+          }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int g = 4 * lane + e;
+          if (g < m) {
+            mg = max(mg, S.blk_greedy[g]);
+            mi = max(mi, S.blk_ident[g]);
+          }
+        }
+      }
+      mg = __reduce_max_sync(kFull, mg);
+      mi = __reduce_max_sync(kFull, mi);
+      if (lane == 0) S.keep_flag = mg <= mi ? 1u : 0u;  // src/reorder.cpp:350-353 (exact integer loads)
     }
     __syncthreads();
-    unsigned mg = 0u, mi = 0u;
-    for (int g = tid; g < m; g += kFusedT) {
-      mg = max(mg, S.blk_greedy[g]);
-      mi = max(mi, S.blk_ident[g]);
-    }
-    mg = static_cast<unsigned>(block_max_ll<kFusedT>(mg, S.tmpll));
-    mi = static_cast<unsigned>(block_max_ll<kFusedT>(mi, S.tmpll));
-    keep = mg <= mi;  // src/reorder.cpp:350-353 (exact integer loads)
+    keep = S.keep_flag != 0u;
   }
   if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
   for (int g = tid; g < m; g += kFusedT)
@@ -706,7 +751,14 @@ __device__ __noinline__ void narrow_sort_path(const FusedArgs& a, long long b, N
     constexpr int kGT = 256;
     unsigned long long* gprof = a.prof ? a.prof + b * kProfSlots + 6 : nullptr;
     if (desc) {
-      if (w == 0) greedy_warp<false>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt, gprof);
+      // u32 keys (load << 8 | gid) while every load stays below 2^24
+      if (w == 0) {
+        if (static_cast<long long>(cap) * 2 * 0x7fff < (1ll << 24))
+          greedy_warp<unsigned>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt, gprof);
+        else
+          greedy_warp<unsigned long long>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt,
+                                          gprof);
+      }
     } else if (tid < kGT) {
       greedy_fused<kGT, true, 1>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll, gprof);
     }
@@ -887,7 +939,19 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
     cl.sync();  // the peer's sorted indices and this CTA's cells are ready
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 58] = globaltimer();
     if (rank == 0 && S.deferred) {
-      kept_output(a, b, S, cl.map_shared_rank(S.idx16, 1), cl.map_shared_rank(S.kbi, 1));
+      // the peer's sorted indices and keys, copied whole over DSMEM (16-byte
+      // coalesced reads) into this CTA's idx16 / kbi (the histogram and the
+      // sorted sizes there are no longer needed), then gathered locally
+      const uint4* pi = reinterpret_cast<const uint4*>(cl.map_shared_rank(S.idx16, 1));
+      const uint4* pk = reinterpret_cast<const uint4*>(cl.map_shared_rank(S.kbi, 1));
+      constexpr int kWords = kFusedSlots / 8;
+      for (int q = threadIdx.x; q < kWords; q += kFusedT) {
+        const uint4 x = pi[q], y = pk[q];
+        reinterpret_cast<uint4*>(S.idx16)[q] = x;
+        reinterpret_cast<uint4*>(S.kbi)[q] = y;
+      }
+      __syncthreads();
+      kept_output(a, b, S, S.idx16, S.kbi);
     }
     cl.sync();  // the peer's shared memory is free again
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 59] = globaltimer();

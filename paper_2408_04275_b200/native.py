@@ -11,7 +11,8 @@ from . import _capi
 from .api import Planner
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdisttrain_b200.so")
+# DTB_LIB_PATH: an experiment build (build.py with DTB_DEFINES) for tools/
+LIB_PATH = os.environ.get("DTB_LIB_PATH") or os.path.join(HERE, "libdisttrain_b200.so")
 _lib = None
 
 

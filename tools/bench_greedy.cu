@@ -29,16 +29,28 @@ __global__ void k_greedy(const unsigned short* sizes, int n, int m, int zc, int 
   const int cap = (n + m - 1) / m, capP = ((cap + 1) | 3) - 1;
   auto size_at = [&](int k) -> unsigned { return 2u * S.sz[k]; };
   auto emit = [&](int k, int g, int slot) { S.out[g * capP + slot] = (unsigned short)k; };
-  const int z0 = n - zc, z1 = n;
+  const int z0 = which >= 3 ? 0 : n - zc, z1 = which >= 3 ? (which == 4 ? 0 : zc) : n;
   long long c0 = clock64();
-  if (which == 0) {
-    if (threadIdx.x < 32) greedy_warp<false>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt);
+  if (which == 3 || which == 4) {  // ascending (sizes reversed: read from the end)
+    auto size_asc = [&](int k) -> unsigned { return 2u * S.sz[n - 1 - k]; };
+    if (threadIdx.x < 256) greedy_fused<256, true, 1>(n, m, cap, z0, z1, size_asc, emit, S.G, S.tmp, S.tmpll);
+  } else if (which == 5) {
+    if (threadIdx.x < 256) {
+      int tot = 0, acc = 0;
+      for (int it = 0; it < 100; ++it) acc += block_excl_scan<256, 1>(threadIdx.x + it, S.tmp, &tot);
+      if (acc == 12345) cyc[7] = tot;
+    }
+  } else if (which == 6) {
+    if (threadIdx.x < 256)
+      for (int it = 0; it < 100; ++it) bar_sync<1, 256>();
+  } else if (which == 0) {
+    if (threadIdx.x < 32) greedy_warp<unsigned>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt);
   } else if (which == 1) {
     if (threadIdx.x < 256) greedy_fused<256, false, 1>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll);
   } else {
     if (threadIdx.x < 32) {
-      unsigned long long v[4];
-      for (int e = 0; e < 4; ++e) v[e] = (unsigned long long)((threadIdx.x * 2654435761u + e * 97u) & 0xffffu);
+      unsigned v[4];
+      for (int e = 0; e < 4; ++e) v[e] = (threadIdx.x * 2654435761u + e * 97u) & 0xffffu;
       for (int it = 0; it < 100; ++it) { wg_sort128(v); v[0] ^= it; }
       if (v[0] == 12345) cyc[5] = 1;
     }
@@ -46,6 +58,7 @@ __global__ void k_greedy(const unsigned short* sizes, int n, int m, int zc, int 
   __syncthreads();
   long long c1 = clock64();
   if (threadIdx.x == 0) cyc[which] = c1 - c0;
+  if (which >= 3) return;
   for (int g = threadIdx.x; g < m; g += blockDim.x) { gl[which * 128 + g] = S.G.gload[g]; gc[which * 128 + g] = S.G.gcnt[g]; }
   for (int i = threadIdx.x; i < m * capP; i += blockDim.x) out[which * 17000 + i] = S.out[i];
 }
@@ -62,16 +75,16 @@ int main() {
   std::sort(h.begin(), h.end(), [](unsigned short a, unsigned short b) { return a > b; });
   for (int i = 0; i < n; ++i) zc += h[i] == 0;
   unsigned short* d; long long* cyc; unsigned* gl; int* gc; unsigned short* out;
-  cudaMalloc(&d, 2 * n); cudaMalloc(&cyc, 64); cudaMalloc(&gl, 4 * 3 * 128); cudaMalloc(&gc, 4 * 3 * 128);
+  cudaMalloc(&d, 2 * n); cudaMalloc(&cyc, 128); cudaMalloc(&gl, 4 * 3 * 128); cudaMalloc(&gc, 4 * 3 * 128);
   cudaMalloc(&out, 2 * 3 * 17000);
   cudaMemcpy(d, h.data(), 2 * n, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Sm));
   for (int rep = 0; rep < 3; ++rep)
-    for (int which = 0; which < 3; ++which)
+    for (int which = 0; which < 7; ++which)
       k_greedy<<<1, 1024, sizeof(Sm)>>>(d, n, m, zc, which, cyc, gl, gc, out);
   cudaError_t e = cudaDeviceSynchronize();
-  long long c[6];
-  cudaMemcpy(c, cyc, 48, cudaMemcpyDeviceToHost);
+  long long c[16];
+  cudaMemcpy(c, cyc, 128, cudaMemcpyDeviceToHost);
   std::vector<unsigned> hg(3 * 128); std::vector<int> hc(3 * 128); std::vector<unsigned short> ho(3 * 17000);
   cudaMemcpy(hg.data(), gl, 4 * 3 * 128, cudaMemcpyDeviceToHost);
   cudaMemcpy(hc.data(), gc, 4 * 3 * 128, cudaMemcpyDeviceToHost);
@@ -80,7 +93,9 @@ int main() {
   for (int g = 0; g < m; ++g) same &= hg[g] == hg[128 + g] && hc[g] == hc[128 + g];
   for (int i = 0; i < 17000; ++i) same &= ho[i] == ho[17000 + i];
   printf("{\"err\": \"%s\", \"zeros\": %d, \"warp_greedy_cycles\": %lld, \"block_greedy_cycles\": %lld, "
-         "\"sort128_cycles_per_call\": %.1f, \"agree\": %s}\n", cudaGetErrorString(e), zc, c[0], c[1],
-         c[2] / 100.0, same ? "true" : "false");
+         "\"sort128_cycles_per_call\": %.1f, \"agree\": %s, \"asc_block_greedy_cycles\": %lld, "
+         "\"asc_block_greedy_no_zero_run_cycles\": %lld, \"block_excl_scan_256_cycles\": %.1f, "
+         "\"bar_sync_256_cycles\": %.1f}\n", cudaGetErrorString(e), zc, c[0], c[1],
+         c[2] / 100.0, same ? "true" : "false", c[3], c[4], c[5] / 100.0, c[6] / 100.0);
   return 0;
 }
