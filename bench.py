@@ -489,6 +489,16 @@ def main():
         out["modes"] = {"intra+inter": {"ms_per_step": both_ms,
                                         "value": my_batches * BS / (both_ms / 1e3),
                                         "unit": "samples/s"}}
+        # the reference's default mode on a bounded sample (one global batch per
+        # host thread, ~1 s per batch on one core)
+        thr = os.cpu_count() or 1
+        kind_d, times_d = cpu_reference(samples, plan_c, mode_both, min(my_batches, thr), 1, 0, thr,
+                                        (model, cluster, book))
+        out["modes"]["intra+inter"]["cpu_baseline"] = {
+            "value": min(my_batches, thr) * BS / float(np.median(times_d)), "unit": "samples/s",
+            "cores": thr, "kind": kind_d, "cpu_model": cpu_model(),
+            "sample": f"first {min(my_batches, thr)} global batches x {BS} samples, default mode, "
+                      "std::thread fan-out over batches"}
         try:  # FP64 instructions of the step (ncu count) over the measured step time
             fops = json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_ops.json")))
             ks = fops["reorder_default_16M"]["kernels"]

@@ -310,4 +310,69 @@ __device__ void tile_pass_blocked(unsigned short* idx, const unsigned short* key
   __syncthreads();
 }
 
+// The same stable blocked pass over packed (key << 16 | index) items: the
+// digit comes from the item itself (no indirect key lookups in shared
+// memory), the scatter moves the 32-bit item.  ITEMS % 4 == 0 (128-bit loads
+// of a thread's slots).
+template <int T, int ITEMS, int RB, bool SWZ, typename DigitFn>
+__device__ void tile_pass_kv(unsigned* kv, const DigitFn& digit, unsigned* cntw, int* scan_tmp) {
+  constexpr int D = 1 << RB;
+  constexpr int WORDS = D * T / 2;
+  constexpr int PER = WORDS / T;
+  constexpr int G = 4;
+  static_assert(ITEMS % G == 0 && WORDS % T == 0 && PER % 16 == 0, "shape");
+  const int t = threadIdx.x;
+  auto word_of = [&](unsigned d) -> int {
+    const int e = static_cast<int>(d) * T + t;
+    return (e >> 1) + (e >> 5);
+  };
+  const unsigned half = (t & 1) * 16;
+  for (int i = t; i < blocked_cnt_words(T, RB); i += T) cntw[i] = 0u;
+  uint4 it[ITEMS / G];
+  const uint4* mine = reinterpret_cast<const uint4*>(kv + t * ITEMS);
+#pragma unroll
+  for (int g = 0; g < ITEMS / G; ++g) it[g] = mine[g];
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < ITEMS / G; ++g) {
+    const unsigned v[G] = {it[g].x, it[g].y, it[g].z, it[g].w};
+#pragma unroll
+    for (int j = 0; j < G; ++j) atomicAdd(cntw + word_of(static_cast<unsigned>(digit(v[j] >> 16))), 1u << half);
+  }
+  __syncthreads();
+  // (the thread's counter words are re-read after the scan instead of held:
+  // the items already occupy 16 registers)
+  unsigned* seg = cntw + t * (PER + PER / 16);
+  int sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const unsigned c = seg[j + j / 16];
+    sum += static_cast<int>((c & 0xffffu) + (c >> 16));
+  }
+  int total;
+  int base = block_excl_scan<T>(sum, scan_tmp, &total);
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const unsigned c = seg[j + j / 16];
+    const unsigned lo = c & 0xffffu, hi = c >> 16;
+    seg[j + j / 16] = static_cast<unsigned>(base) | (static_cast<unsigned>(base + lo) << 16);
+    base += static_cast<int>(lo + hi);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < ITEMS / G; ++g) {
+    const unsigned v[G] = {it[g].x, it[g].y, it[g].z, it[g].w};
+    unsigned old[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+      old[j] = atomicAdd(cntw + word_of(static_cast<unsigned>(digit(v[j] >> 16))), 1u << half);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int dst = static_cast<int>((old[j] >> half) & 0xffffu);
+      kv[SWZ ? swz(dst) : dst] = v[j];
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace dtb

@@ -61,7 +61,8 @@ struct dtb_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-buffer pipelines (lazy)
-  cudaStream_t side = nullptr;  // partition kernel next to the simulations; peer exchange
+  cudaStream_t side = nullptr;  // partition kernel next to the simulations
+  cudaStream_t xchg = nullptr;  // peer exchange of the final order
   DevErr* err = nullptr;  // device
 };
 
@@ -307,6 +308,7 @@ dtb_status dtb_context_create(int32_t device, dtb_context** out) {
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->xchg, cudaStreamNonBlocking);
   if (e == cudaSuccess) {
     // keep stream-ordered scratch cached across calls (no per-call cudaMalloc)
     cudaMemPool_t pool;
@@ -333,6 +335,7 @@ dtb_status dtb_context_destroy(dtb_context* ctx) {
   if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
   if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->xchg) cudaStreamDestroy(ctx->xchg);
   delete ctx;
   return DTB_OK;
 }
@@ -1054,19 +1057,20 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
                              const int* ao, const int* at, long long n_batches, int* order_out,
                              double* lb, double* la, double* tb, double* ta, unsigned char* kept,
                              cudaStream_t s, const PeerBcast* peer = nullptr) {
-  // Peer exchange of the final order on the side stream, joined at the end:
+  // Peer exchange of the final order on its own stream, joined at the end:
   // it overlaps everything after the order is final (the simulations).
+  // `after`: the stream on which the order became final.
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
-  auto exchange = [&]() -> cudaError_t {
+  auto exchange = [&](cudaStream_t after) -> cudaError_t {
     if (peer == nullptr) return cudaSuccess;
     cudaError_t e = cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_ready, s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->side, ev_ready, 0);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_ready, after);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->xchg, ev_ready, 0);
     PeerBcast pb = *peer;
     pb.src = order_out;
-    if (e == cudaSuccess) e = launch_peer_broadcast(pb, ctx->side);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_done, ctx->side);
+    if (e == cudaSuccess) e = launch_peer_broadcast(pb, ctx->xchg);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_done, ctx->xchg);
     return e;
   };
   cudaEvent_t ev_fork = nullptr, ev_part = nullptr;  // partition kernel on ctx->side
@@ -1144,9 +1148,9 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   CU(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   CU(launch_sort_partition(fa, n_batches, cscr, s, ctx->side, ev_fork));
   CU(cudaEventRecord(ev_part, ctx->side));
-  // the intra order is the output order: exchanged on the side stream right
-  // after the partition kernel
-  if (!compose_needed) CU(exchange());
+  // the intra order is the output order: exchanged right after the partition
+  // kernel, next to everything that follows it
+  if (!compose_needed) CU(exchange(ctx->side));
   const TokSrc tok{tok16.as<unsigned short>(), tok16s.as<unsigned short>(), tok32.as<int>(),
                    tok32s.as<int>(), kept_dev, wflag.as<unsigned int>(), n};
   if (span > 1) {  // assembled microbatch sums [b][e][i] (input order: cost pass only)
@@ -1254,7 +1258,7 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   if (compose_needed) {
     CU(launch_compose(n_batches, n, dp_lm, dp_me, intra_out, mode->inter ? inter.as<int>() : nullptr,
                       order_out, s));
-    CU(exchange());
+    CU(exchange(s));
   }
   ga.staged = true;
   ga.mbsum = span > 1 ? mb1.as<int>() : nullptr;

@@ -345,32 +345,41 @@ __device__ __forceinline__ void identity_order_out(const FusedArgs& a, long long
 // idx16, counters in their own space so the greedy's cells in out16
 // survive.  Sorted position k (the greedy's k: the same stable order of the
 // sizes) is then idx16[swz(k)].
+// Stable sort of a batch's samples by key (u16 tokens from the cost pass;
+// descending: 0x7fff - tokens) as packed (key << 16 | index) items in the
+// 64 KB of kbi + idx16 (`batch_kv`): 3 blocked passes of 5-bit digits over
+// the 13-bit keys; the last writes swizzled positions.  abort_epoch != 0: a
+// cluster peer's speculative sort, stopped between passes once the peer
+// decided the batch is not kept.
+__device__ __forceinline__ unsigned* batch_kv(NarrowSmem& S) { return reinterpret_cast<unsigned*>(S.kbi); }
+static_assert(offsetof(NarrowSmem, idx16) == sizeof(NarrowSmem::kbi) &&
+                  sizeof(NarrowSmem::kbi) + sizeof(NarrowSmem::idx16) == 4 * kFusedSlots,
+              "kbi and idx16 form one array of packed (key, index) items");
 __device__ __noinline__ void sort_batch_keys(const FusedArgs& a, long long b, NarrowSmem&,
                                              unsigned abort_epoch = 0u) {
   NarrowSmem& S = shared_state();
   const int n = a.n, tid = threadIdx.x;
   const long long first = b * n;
   const bool desc = a.order == DTB_DESCENDING;
+  unsigned* kv = batch_kv(S);
   const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
   for (int q = tid; q < (n >> 3); q += kFusedT) {
     const uint4 v = __ldg(src + q);
     const unsigned wd[4] = {v.x, v.y, v.z, v.w};
-    unsigned kw[4], iw[4];
+    unsigned o[8];
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
       const unsigned t0 = wd[h] & 0xffffu, t1 = wd[h] >> 16;
       const unsigned k0 = desc ? 0x7fffu - t0 : t0, k1 = desc ? 0x7fffu - t1 : t1;
-      kw[h] = k0 | (k1 << 16);
       const unsigned i0 = static_cast<unsigned>(8 * q + 2 * h);
-      iw[h] = i0 | ((i0 + 1) << 16);
+      o[2 * h] = (k0 << 16) | i0;
+      o[2 * h + 1] = (k1 << 16) | (i0 + 1);
     }
-    reinterpret_cast<uint4*>(S.kbi)[q] = make_uint4(kw[0], kw[1], kw[2], kw[3]);
-    reinterpret_cast<uint4*>(S.idx16)[q] = make_uint4(iw[0], iw[1], iw[2], iw[3]);
+    reinterpret_cast<uint4*>(kv)[2 * q] = make_uint4(o[0], o[1], o[2], o[3]);
+    reinterpret_cast<uint4*>(kv)[2 * q + 1] = make_uint4(o[4], o[5], o[6], o[7]);
   }
-  for (int i = n + tid; i < kFusedSlots; i += kFusedT) {  // padding: largest digits
-    S.kbi[i] = 0xffffu;
-    S.idx16[i] = static_cast<unsigned short>(i);
-  }
+  for (int i = n + tid; i < kFusedSlots; i += kFusedT)  // padding: largest digits
+    kv[i] = 0xffff0000u | static_cast<unsigned>(i);
   __syncthreads();
   // every token < kHistBins: ascending keys vary in bits [0, 13), descending
   // keys (0x7fff - tok > 0x5fff) in bits [0, 13) too; padding is 0xffff
@@ -387,18 +396,17 @@ __device__ __noinline__ void sort_batch_keys(const FusedArgs& a, long long b, Na
     const unsigned mask = (1u << bits) - 1u;
     auto dig = [&](unsigned key) { return (key >> sh) & mask; };
     if (sh + kSortRB >= kKeyBits)
-      tile_pass_blocked<kFusedT, kFusedItems, kSortRB, true>(S.idx16, S.kbi, dig, cw, S.tmp);
+      tile_pass_kv<kFusedT, kFusedItems, kSortRB, true>(kv, dig, cw, S.tmp);
     else
-      tile_pass_blocked<kFusedT, kFusedItems, kSortRB, false>(S.idx16, S.kbi, dig, cw, S.tmp);
+      tile_pass_kv<kFusedT, kFusedItems, kSortRB, false>(kv, dig, cw, S.tmp);
   }
 }
 
 // Outputs of a kept batch from the greedy's cells (this CTA) and the sorted
-// indices / keys (`idx`, `key`: this CTA's or, in a cluster pair, the peer's
-// shared memory through DSMEM): the intra order and its staged tokens,
-// coalesced per group.
+// (key, index) items `kv` (this CTA's, or a copy of the cluster peer's): the
+// intra order and its staged tokens, coalesced per group.
 __device__ __noinline__ void kept_output(const FusedArgs& a, long long b, NarrowSmem&,
-                                         const unsigned short* idx, const unsigned short* key) {
+                                         const unsigned* kv) {
   NarrowSmem& S = shared_state();
   const int n = a.n, m = a.m, lane = lane_id(), w = warp_id();
   const long long first = b * n;
@@ -408,10 +416,10 @@ __device__ __noinline__ void kept_output(const FusedArgs& a, long long b, Narrow
   for (int g = w; g < m; g += kFusedT / 32) {
     const int base = S.off[g], cnt = S.G.gcnt[g];
     for (int slot = lane; slot < cnt; slot += 32) {
-      const unsigned i = idx[swz(S.out16[g * capP + slot])];
-      a.order_out[first + base + slot] = static_cast<int>(i);
+      const unsigned item = kv[swz(S.out16[g * capP + slot])];
+      a.order_out[first + base + slot] = static_cast<int>(item & 0xffffu);
       if (a.tok16_staged != nullptr) {
-        const unsigned k = key[i];
+        const unsigned k = item >> 16;
         a.tok16_staged[first + base + slot] = static_cast<unsigned short>(desc ? 0x7fffu - k : k);
       }
     }
@@ -630,7 +638,7 @@ __device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSm
     } else {
       __syncthreads();
       sort_batch_keys(a, b, S);
-      kept_output(a, b, S, S.idx16, S.kbi);
+      kept_output(a, b, S, batch_kv(S));
     }
   }
   if (a.prof) {
@@ -939,19 +947,15 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
     cl.sync();  // the peer's sorted indices and this CTA's cells are ready
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 58] = globaltimer();
     if (rank == 0 && S.deferred) {
-      // the peer's sorted indices and keys, copied whole over DSMEM (16-byte
-      // coalesced reads) into this CTA's idx16 / kbi (the histogram and the
-      // sorted sizes there are no longer needed), then gathered locally
-      const uint4* pi = reinterpret_cast<const uint4*>(cl.map_shared_rank(S.idx16, 1));
-      const uint4* pk = reinterpret_cast<const uint4*>(cl.map_shared_rank(S.kbi, 1));
-      constexpr int kWords = kFusedSlots / 8;
-      for (int q = threadIdx.x; q < kWords; q += kFusedT) {
-        const uint4 x = pi[q], y = pk[q];
-        reinterpret_cast<uint4*>(S.idx16)[q] = x;
-        reinterpret_cast<uint4*>(S.kbi)[q] = y;
-      }
+      // the peer's sorted (key, index) items, copied whole over DSMEM
+      // (16-byte coalesced reads) into this CTA's kbi + idx16 (the histogram
+      // and the sorted sizes there are no longer needed), gathered locally
+      unsigned* kv = batch_kv(S);
+      const uint4* pk = reinterpret_cast<const uint4*>(cl.map_shared_rank(kv, 1));
+      constexpr int kWords = kFusedSlots / 4;
+      for (int q = threadIdx.x; q < kWords; q += kFusedT) reinterpret_cast<uint4*>(kv)[q] = pk[q];
       __syncthreads();
-      kept_output(a, b, S, S.idx16, S.kbi);
+      kept_output(a, b, S, kv);
     }
     cl.sync();  // the peer's shared memory is free again
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 59] = globaltimer();
