@@ -247,6 +247,25 @@ typedef struct dtb_cost_model dtb_cost_model; /* CostModel (cost_model.hpp:152) 
 dtb_status dtb_context_create(int32_t device, dtb_context** out);
 dtb_status dtb_context_destroy(dtb_context* ctx);
 
+/* Warning log — the reference's CostModel warning sink
+ * (CostModel::set_warning_sink, include/cost_model.hpp:147,184; strings of
+ * src/cost_model.cpp:84-95 and :248-251).  While enabled (enable also
+ * clears), every successful call below appends, in the reference's query
+ * order, the strings the reference's CostModel would append to its sink:
+ *   "token load X below profile range; clamped",
+ *   "token load X above profile range; clamped"   (X = std::to_string(load)),
+ *   "module 'K' has no profile; using analytic estimate".
+ * Covered: dtb_unit_times (per load: forward then backward query),
+ * dtb_build_stage_times, dtb_microbatch_fwd_keys, dtb_simulate_iteration,
+ * dtb_disaggregated_reorder and the stream calls (per batch, as
+ * disaggregated_reorder; not inside CUDA graph captures).  Not covered: the
+ * orchestration search's queries.  dtb_warning_at returns NULL out of range;
+ * its pointer is valid until the log changes. */
+dtb_status dtb_warnings_enable(dtb_context* ctx, int32_t on);
+int64_t dtb_warnings_count(const dtb_context* ctx);
+const char* dtb_warning_at(const dtb_context* ctx, int64_t i);
+dtb_status dtb_warnings_clear(dtb_context* ctx);
+
 /* CostModel(model, cluster, book) — include/cost_model.hpp:154. Applies
  * add_row to every row (ConfigError on a bad row, cost_model.cpp:39-48) and
  * uploads the flattened book to the device. */

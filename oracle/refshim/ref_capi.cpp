@@ -248,10 +248,36 @@ void parallel_for(int64_t n, F&& fn) {
 
 struct dtb_context {
   int device = -1;
+  bool warn_on = false;
+  std::vector<std::string> warnings;  // the reference CostModel's warning sink
 };
 struct dtb_cost_model {
   std::unique_ptr<CostModel> cm;
 };
+
+namespace {
+// While the context's warning log is on, the call's CostModel appends to it
+// (CostModel::set_warning_sink; the sink makes the model non-reentrant, so
+// the batch fan-out runs on one thread meanwhile).
+struct Sink {
+  CostModel* cm = nullptr;
+  int saved_threads = 0;
+  Sink(dtb_context* ctx, const dtb_cost_model* h) {
+    if (ctx != nullptr && ctx->warn_on) {
+      cm = h->cm.get();
+      cm->set_warning_sink(&ctx->warnings);
+      saved_threads = g_threads;
+      g_threads = 1;
+    }
+  }
+  ~Sink() {
+    if (cm != nullptr) {
+      cm->set_warning_sink(nullptr);
+      g_threads = saved_threads;
+    }
+  }
+};
+}  // namespace
 
 extern "C" {
 
@@ -267,6 +293,23 @@ dtb_status API(context_create)(int32_t device, dtb_context** out) {
 }
 dtb_status API(context_destroy)(dtb_context* ctx) {
   delete ctx;
+  return DTB_OK;
+}
+
+dtb_status API(warnings_enable)(dtb_context* ctx, int32_t on) {
+  ctx->warn_on = on != 0;
+  ctx->warnings.clear();
+  return DTB_OK;
+}
+int64_t API(warnings_count)(const dtb_context* ctx) {
+  return static_cast<int64_t>(ctx->warnings.size());
+}
+const char* API(warning_at)(const dtb_context* ctx, int64_t i) {
+  if (i < 0 || i >= static_cast<int64_t>(ctx->warnings.size())) return nullptr;
+  return ctx->warnings[static_cast<std::size_t>(i)].c_str();
+}
+dtb_status API(warnings_clear)(dtb_context* ctx) {
+  ctx->warnings.clear();
   return DTB_OK;
 }
 
@@ -302,9 +345,10 @@ dtb_status API(cost_sizes)(dtb_context*, const dtb_samples* s, int64_t* out) {
   });
 }
 
-dtb_status API(unit_times)(dtb_context*, const dtb_cost_model* cm,
+dtb_status API(unit_times)(dtb_context* ctx, const dtb_cost_model* cm,
                            int32_t module, int32_t tp, int64_t n,
                            const double* loads, double* fwd, double* bwd) {
+  const Sink sink(ctx, cm);
   return guarded([&] {
     for (int64_t i = 0; i < n; ++i) {
       if (fwd) fwd[i] = cm->cm->unit_forward_time(kind_of(module), tp, loads[i]);
@@ -327,10 +371,11 @@ dtb_status API(memory_check)(dtb_context*, const dtb_cost_model* cm,
   });
 }
 
-dtb_status API(build_stage_times)(dtb_context*, const dtb_cost_model* cm,
+dtb_status API(build_stage_times)(dtb_context* ctx, const dtb_cost_model* cm,
                                   const dtb_plan* plan,
                                   const dtb_microbatches* mbs, double* fwd,
                                   double* bwd) {
+  const Sink sink(ctx, cm);
   return guarded([&] {
     const auto v = to_microbatches(*mbs, 0, mbs->n);
     const StageTimes t = cm->cm->build_stage_times(to_plan(*plan), v);
@@ -339,9 +384,10 @@ dtb_status API(build_stage_times)(dtb_context*, const dtb_cost_model* cm,
   });
 }
 
-dtb_status API(microbatch_fwd_keys)(dtb_context*, const dtb_cost_model* cm,
+dtb_status API(microbatch_fwd_keys)(dtb_context* ctx, const dtb_cost_model* cm,
                                     const dtb_plan* plan,
                                     const dtb_microbatches* mbs, double* keys) {
+  const Sink sink(ctx, cm);
   return guarded([&] {
     const auto v = to_microbatches(*mbs, 0, mbs->n);
     const auto k = microbatch_fwd_keys(to_plan(*plan), *cm->cm, v);
@@ -521,12 +567,13 @@ dtb_status API(exhaustive_order)(dtb_context*, const double* fwd, const double* 
   });
 }
 
-dtb_status API(simulate_iteration)(dtb_context*, const dtb_cost_model* cm,
+dtb_status API(simulate_iteration)(dtb_context* ctx, const dtb_cost_model* cm,
                                    const dtb_plan* plan, int32_t n_groups,
                                    const int64_t* group_offsets,
                                    const dtb_microbatches* mbs, double* t_iter,
                                    double* group_times, int32_t* slowest_group,
                                    double* slowest_time, double* bubble) {
+  const Sink sink(ctx, cm);
   return guarded([&] {
     std::vector<std::vector<Microbatch>> groups;
     for (int32_t g = 0; g < n_groups; ++g) {
@@ -584,11 +631,12 @@ static ReorderMode to_mode(const dtb_reorder_mode* m) {
   return mode;
 }
 
-dtb_status API(disaggregated_reorder)(dtb_context*, const dtb_cost_model* cm,
+dtb_status API(disaggregated_reorder)(dtb_context* ctx, const dtb_cost_model* cm,
                                       const dtb_plan* plan,
                                       const dtb_reorder_mode* mode,
                                       const dtb_samples* batch,
                                       dtb_reorder_report* report) {
+  const Sink sink(ctx, cm);
   return guarded([&] {
     const auto samples = to_samples(*batch, 0, batch->n);
     const DisaggregatedResult r = disaggregated_reorder(
@@ -662,13 +710,14 @@ dtb_status API(stream_run)(mmref_stream* h, const dtb_cost_model* cm,
   });
 }
 
-dtb_status API(reorder_stream)(dtb_context*, const dtb_cost_model* cm,
+dtb_status API(reorder_stream)(dtb_context* ctx, const dtb_cost_model* cm,
                                const dtb_plan* plan,
                                const dtb_reorder_mode* mode,
                                const dtb_samples* samples, int64_t n_batches,
                                int32_t* output_order, double* load_before,
                                double* load_after, double* t_before,
                                double* t_after, uint8_t* greedy_kept) {
+  const Sink sink(ctx, cm);
   mmref_stream* h = nullptr;
   dtb_status st = API(stream_prepare)(samples, n_batches, &h);
   if (st != DTB_OK) return st;

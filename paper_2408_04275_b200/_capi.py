@@ -136,6 +136,10 @@ _SIGS = {
     "last_error": (C.c_char_p, []),
     "abi_version": (C.c_int, []),
     "context_create": (c_i32, [c_i32, P(VP)]),
+    "warnings_enable": (c_i32, [VP, c_i32]),
+    "warnings_count": (c_i64, [VP]),
+    "warning_at": (C.c_char_p, [VP, c_i64]),
+    "warnings_clear": (c_i32, [VP]),
     "context_destroy": (c_i32, [VP]),
     "cost_model_create": (c_i32, [VP, P(ModelSpec), P(ClusterSpec),
                                   P(CostBook), P(VP)]),

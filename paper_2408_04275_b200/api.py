@@ -423,6 +423,17 @@ class Planner:
             msg = self.lib.last_error().decode(errors="replace")
             raise _ERRORS.get(status, MmplanError)(msg)
 
+    # ---- warning log (CostModel::set_warning_sink) ------------------------
+    def warnings_enable(self, on: bool = True):
+        """Start (and clear) or stop the context's warning log."""
+        self._check(self.lib.warnings_enable(self.ctx, 1 if on else 0))
+
+    def warnings(self) -> list:
+        """The strings the reference's CostModel would have appended to its
+        warning sink since warnings_enable, in the reference's order."""
+        n = self.lib.warnings_count(self.ctx)
+        return [self.lib.warning_at(self.ctx, i).decode() for i in range(n)]
+
     # ---- cost model ------------------------------------------------------
     def cost_model(self, model: Model, cluster: Cluster, book: Book) -> CostModelHandle:
         return CostModelHandle(self, model, cluster, book)

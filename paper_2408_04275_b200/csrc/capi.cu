@@ -64,6 +64,10 @@ struct dtb_context {
   cudaStream_t side = nullptr;  // partition kernel next to the simulations
   cudaStream_t xchg = nullptr;  // peer exchange of the final order
   DevErr* err = nullptr;  // device
+  // warning log (dtb_warnings_enable): the strings the reference's CostModel
+  // appends to its sink, in the reference's query order
+  bool warn_on = false;
+  std::vector<std::string> warnings;
 };
 
 struct dtb_peer_group {
@@ -226,6 +230,70 @@ dtb_status check_stage_queries(const dtb_cost_model* cm, const dtb_plan& p) {
 dtb_status check_key_queries(const dtb_cost_model* cm, const dtb_plan& p) {
   TRY(check_fwd_query(cm, DTB_ENCODER, p.unit[DTB_ENCODER].tp));
   return check_fwd_query(cm, DTB_GENERATOR, p.unit[DTB_GENERATOR].tp);
+}
+
+// ---- warning log.  One unit_forward_time / unit_backward_time query at
+// `load` appends what the reference appends (src/cost_model.cpp:84-95 via
+// CostProfile::forward_seconds / backward_seconds — both interpolate over
+// rows_for(tp), so the clamp condition is the same — and :248-251 via
+// analytic_forward): "token load X below|above profile range; clamped" with
+// X = std::to_string(load), or "module 'K' has no profile; using analytic
+// estimate".  Called on successful calls only (a query that throws appends
+// nothing in the reference either).
+void warn_query(dtb_context* ctx, const dtb_cost_model* cm, int kind, int tp, double load) {
+  if (!cm->nonempty[kind]) {
+    ctx->warnings.push_back(std::string("module '") + kind_name(kind) +
+                            "' has no profile; using analytic estimate");
+    return;
+  }
+  const int ti = tp_index(tp);
+  if (ti < 0 || cm->rows[kind][ti].empty()) return;
+  const auto& rows = cm->rows[kind][ti];
+  if (load < rows.front().load)
+    ctx->warnings.push_back("token load " + std::to_string(load) + " below profile range; clamped");
+  else if (load > rows.back().load)
+    ctx->warnings.push_back("token load " + std::to_string(load) + " above profile range; clamped");
+}
+
+// build_stage_times (src/cost_model.cpp:334-362) over microbatches given by
+// their encoder / generator token sums and sample counts: per microbatch,
+// per unit (encoder, backbone, generator), forward then backward.
+template <typename TokFn>
+void warn_stage_times(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan& p, long long l,
+                      const TokFn& mb) {
+  for (long long i = 0; i < l; ++i) {
+    int64_t te, tg;
+    int cnt;
+    mb(i, &te, &tg, &cnt);
+    const double loads[3] = {mb_mean(te, cnt), static_cast<double>(cm->model.seq_len),
+                             mb_mean(tg, cnt)};
+    for (int u = 0; u < 3; ++u) {
+      warn_query(ctx, cm, u, p.unit[u].tp, loads[u]);
+      warn_query(ctx, cm, u, p.unit[u].tp, loads[u]);
+    }
+  }
+}
+
+// microbatch_fwd_keys (src/reorder.cpp:300-317): per microbatch, the
+// encoder then the generator forward query.
+template <typename TokFn>
+void warn_fwd_keys(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan& p, long long l,
+                   const TokFn& mb) {
+  for (long long i = 0; i < l; ++i) {
+    int64_t te, tg;
+    int cnt;
+    mb(i, &te, &tg, &cnt);
+    warn_query(ctx, cm, DTB_ENCODER, p.unit[DTB_ENCODER].tp, mb_mean(te, cnt));
+    warn_query(ctx, cm, DTB_GENERATOR, p.unit[DTB_GENERATOR].tp, mb_mean(tg, cnt));
+  }
+}
+
+auto host_mbs(const dtb_microbatches* m, long long first = 0) {
+  return [m, first](long long i, int64_t* te, int64_t* tg, int* cnt) {
+    *te = m->encoder_tokens[first + i];
+    *tg = m->generator_tokens[first + i];
+    *cnt = m->sample_count[first + i];
+  };
 }
 
 // schedule_interleaved's divisibility checks (pipeline_sim.cpp:237-253).
@@ -471,7 +539,13 @@ dtb_status dtb_unit_times(dtb_context* ctx, const dtb_cost_model* cm, int32_t mo
                        bwd ? db.as<double>() : nullptr, ctx->err, ctx->stream));
   TRY(download(fwd, df, n, ctx->stream));
   TRY(download(bwd, db, n, ctx->stream));
-  return sync_and_check(ctx);
+  TRY(sync_and_check(ctx));
+  if (ctx->warn_on)  // per load: the forward query, then the backward one
+    for (int64_t i = 0; i < n; ++i) {
+      if (fwd) warn_query(ctx, cm, module, tp, loads[i]);
+      if (bwd) warn_query(ctx, cm, module, tp, loads[i]);
+    }
+  return DTB_OK;
 }
 
 dtb_status dtb_memory_check(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan* plan,
@@ -509,7 +583,9 @@ dtb_status dtb_build_stage_times(dtb_context* ctx, const dtb_cost_model* cm,
                         c.as<int>(), f.as<double>(), b.as<double>(), ctx->err, ctx->stream));
   TRY(download(fwd, f, mbs->n * p, ctx->stream));
   TRY(download(bwd, b, mbs->n * p, ctx->stream));
-  return sync_and_check(ctx);
+  TRY(sync_and_check(ctx));
+  if (ctx->warn_on) warn_stage_times(ctx, cm, *plan, mbs->n, host_mbs(mbs));
+  return DTB_OK;
 }
 
 dtb_status dtb_microbatch_fwd_keys(dtb_context* ctx, const dtb_cost_model* cm,
@@ -525,7 +601,9 @@ dtb_status dtb_microbatch_fwd_keys(dtb_context* ctx, const dtb_cost_model* cm,
   CU(launch_fwd_keys(cm->dev, *plan, mbs->n, e.as<long long>(), g.as<long long>(), c.as<int>(),
                      k.as<double>(), ctx->err, ctx->stream));
   TRY(download(keys, k, mbs->n, ctx->stream));
-  return sync_and_check(ctx);
+  TRY(sync_and_check(ctx));
+  if (ctx->warn_on) warn_fwd_keys(ctx, cm, *plan, mbs->n, host_mbs(mbs));
+  return DTB_OK;
 }
 
 dtb_status dtb_compute_stats(dtb_context* ctx, const dtb_samples* s, int64_t seq_len,
@@ -817,6 +895,8 @@ dtb_status dtb_simulate_iteration(dtb_context* ctx, const dtb_cost_model* cm,
   for (int32_t gi = 0; gi < n_groups; ++gi) {
     const long long l = group_offsets[gi + 1] - group_offsets[gi];
     if (l > 0) TRY(check_stage_queries(cm, *plan));
+    // simulate.cpp:31: build_stage_times of the group, then its simulation
+    if (ctx->warn_on) warn_stage_times(ctx, cm, *plan, l, host_mbs(mbs, group_offsets[gi]));
     TRY(check_vpp(static_cast<int>(l), p, plan->vpp));
     TRY(reset_err(ctx));
     GroupSimArgs a{};
@@ -1046,6 +1126,53 @@ static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBu
   return launch_intra_fused(fa, n_batches, s);
 }
 
+// Warning log of a stream call: the queries disaggregated_reorder makes per
+// batch (src/reorder.cpp:319-396), in order — build_stage_times of every
+// coupled group in the input order (simulate_iteration, t_iter_before); with
+// inter, per group build_stage_times then microbatch_fwd_keys in the intra
+// order; build_stage_times of every group in the final order (t_iter_after).
+// The microbatch token sums of each phase come from the device
+// (launch_mb_tokens), the strings are built here.
+static dtb_status warn_stream(dtb_context* ctx, const dtb_cost_model* cm, const dtb_plan* plan,
+                              const dtb_reorder_mode* mode, const GroupSimArgs& base,
+                              const int* mb0, const int* mb1, const int* inter_orders,
+                              cudaStream_t s) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(s, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return DTB_OK;  // graphs: no warning log
+  const long long n_batches = base.n_batches, groups = base.groups, l = base.l;
+  const long long n_mb = n_batches * groups * l;
+  const int phases = mode->inter ? 3 : 2;
+  DBuf d;
+  CU(d.alloc(4ull * n_mb * phases, s));
+  for (int ph = 0; ph < phases; ++ph) {
+    GroupSimArgs a = base;
+    const bool last = ph == phases - 1;
+    a.staged = ph > 0;
+    a.mbsum = base.span > 1 ? (ph == 0 ? mb0 : mb1) : nullptr;
+    a.order = last && mode->inter ? inter_orders : nullptr;
+    CU(launch_mb_tokens(a, d.as<int>() + ph * n_mb, s));
+  }
+  std::vector<int> h(static_cast<size_t>(n_mb) * phases);
+  TRY(download(h.data(), d, n_mb * phases, s));
+  CU(cudaStreamSynchronize(s));
+  const int cnt = base.span;
+  for (long long b = 0; b < n_batches; ++b) {
+    for (int ph = 0; ph < phases; ++ph) {
+      for (long long e = 0; e < groups; ++e) {
+        const int* t = h.data() + ph * n_mb + (b * groups + e) * l;
+        auto mb = [t, cnt](long long i, int64_t* te, int64_t* tg, int* c) {
+          *te = *tg = t[i];
+          *c = cnt;
+        };
+        warn_stage_times(ctx, cm, *plan, l, mb);
+        if (mode->inter && ph == 1) warn_fwd_keys(ctx, cm, *plan, l, mb);
+      }
+    }
+  }
+  return DTB_OK;
+}
+
 // Device pipeline for n_batches global batches (all pointers device):
 //   cost pass (k_cost.cu) -> partition kernel on the side stream (intra_fused:
 //   greedy / decision / kept orders of the batches the cost pass left open),
@@ -1233,6 +1360,8 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
     CU(cudaStreamWaitEvent(s, ev_after, 0));
     CU(launch_t_iter_reduce(n_batches, dp_me, tgrp2.as<double>(), cm->model.dp_sync_seconds, ta, s,
                             only_kept, tb));
+    if (ctx->warn_on)
+      TRY(warn_stream(ctx, cm, plan, mode, ga, mb0.as<int>(), mb1.as<int>(), nullptr, s));
     return DTB_OK;  // `join` waits for the partition kernel and the exchange
   }
   CU(cudaStreamWaitEvent(s, ev_part, 0));  // the partition kernel's orders and kept flags
@@ -1267,6 +1396,12 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   CU(launch_group_sims(ga, scr.p, s));
   CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, ta, s,
                           only_kept, tb));
+  if (ctx->warn_on) {
+    GroupSimArgs base = ga;
+    base.only_kept = nullptr;
+    TRY(warn_stream(ctx, cm, plan, mode, base, mb0.as<int>(), mb1.as<int>(),
+                    mode->inter ? inter.as<int>() : nullptr, s));
+  }
   return DTB_OK;  // `join` waits for the partition kernel and the exchange
 }
 
@@ -1276,6 +1411,29 @@ size_t replica_bytes(int64_t n_samples) {
   return (static_cast<size_t>(n_samples) * 2 + 255) / 256 * 256;
 }
 }  // namespace
+
+// ------------------------------------------------------------ warning log
+dtb_status dtb_warnings_enable(dtb_context* ctx, int32_t on) {
+  if (ctx == nullptr) return fail(DTB_ERR_INVALID_ARGUMENT, "null context");
+  ctx->warn_on = on != 0;
+  ctx->warnings.clear();
+  return DTB_OK;
+}
+
+int64_t dtb_warnings_count(const dtb_context* ctx) {
+  return ctx == nullptr ? 0 : static_cast<int64_t>(ctx->warnings.size());
+}
+
+const char* dtb_warning_at(const dtb_context* ctx, int64_t i) {
+  if (ctx == nullptr || i < 0 || i >= static_cast<int64_t>(ctx->warnings.size())) return nullptr;
+  return ctx->warnings[static_cast<size_t>(i)].c_str();
+}
+
+dtb_status dtb_warnings_clear(dtb_context* ctx) {
+  if (ctx == nullptr) return fail(DTB_ERR_INVALID_ARGUMENT, "null context");
+  ctx->warnings.clear();
+  return DTB_OK;
+}
 
 dtb_status dtb_peer_buffer_create(dtb_context* ctx, int64_t n_samples, uint16_t** replica,
                                   dtb_peer_handle* handle) {

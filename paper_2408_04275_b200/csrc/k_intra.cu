@@ -134,7 +134,7 @@ struct NarrowSmem {
   int tmp[kFusedT / 32 + 3];
   long long tmpll[kFusedT / 32 + 1];
   unsigned int s_and, s_or;
-  unsigned deferred;  // fast path: a kept batch's permutation is left to the cluster peer
+  unsigned deferred;  // cluster pair (rank 1): epoch of a kept batch whose order this CTA writes
   // cluster pair: rank 0 stores the pair's batch epoch into rank 1's
   // sort_abort once the batch is decided NOT kept (rank 1's speculative sort
   // is then useless and stops at its next pass)
@@ -634,7 +634,21 @@ __device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSm
   } else {
     // ---- 5. kept: the permutation (here, or by the cluster peer)
     if (defer_kept) {
-      if (tid == 0) S.deferred = 1u;
+      // hand this CTA's cells, group offsets and counts to the cluster peer,
+      // which holds the sorted items (DSMEM stores: no round trips), and mark
+      // the batch there; the peer writes the kept order after the cluster sync
+      cg::cluster_group cl = cg::this_cluster();
+      uint4* dst = reinterpret_cast<uint4*>(cl.map_shared_rank(S.out16, 1));
+      const uint4* src = reinterpret_cast<const uint4*>(S.out16);
+      constexpr int kCellWords = static_cast<int>(sizeof(NarrowSmem::out16) / 16);
+      for (int q = tid; q < kCellWords; q += kFusedT) dst[q] = src[q];
+      int* doff = cl.map_shared_rank(S.off, 1);
+      int* dcnt = cl.map_shared_rank(S.G.gcnt, 1);
+      for (int g = tid; g < m; g += kFusedT) {
+        doff[g] = S.off[g];
+        dcnt[g] = S.G.gcnt[g];
+      }
+      if (tid == 0) *cl.map_shared_rank(&S.deferred, 1) = S.pair_epoch;
     } else {
       __syncthreads();
       sort_batch_keys(a, b, S);
@@ -921,22 +935,18 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   }
   // Few batches (latency-bound): the two CTAs of a cluster share one.  Rank 0
   // runs the histogram, greedy and keep decision while rank 1 runs the
-  // stable radix sort; a kept batch's order is then written by rank 0 from
-  // its cells and rank 1's sorted indices, read through distributed shared
-  // memory.
+  // stable radix sort; for a kept batch rank 0 stores its (group, slot)
+  // cells into rank 1's shared memory (DSMEM) and rank 1 writes the order.
   cg::cluster_group cl = cg::this_cluster();
   const unsigned rank = cl.block_rank();
   if (blockIdx.x / 2 >= count) return;  // the whole pair is idle
-  if (threadIdx.x == 0) S.sort_abort = 0u;
+  if (threadIdx.x == 0) S.sort_abort = S.deferred = 0u;
   cl.sync();
   for (unsigned q = blockIdx.x / 2; q < count; q += pairs) {
     const long long b = a.list[1 + q];
     const bool fast = a.state[b] == kBatchFast && a.m <= kNarrowMaxM && a.n <= kFusedMaxN &&
                       (a.n & 7) == 0;
-    if (threadIdx.x == 0) {
-      S.deferred = 0u;
-      S.pair_epoch = q + 1;
-    }
+    if (threadIdx.x == 0) S.pair_epoch = q + 1;
     __syncthreads();
     if (rank == 1) {
       if (fast) sort_batch_keys(a, b, S, q + 1);
@@ -944,20 +954,11 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
     } else {
       process_batch(a, b, S, fast);
     }
-    cl.sync();  // the peer's sorted indices and this CTA's cells are ready
+    cl.sync();  // rank 1: its sorted items and (kept) rank 0's cells are ready
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 58] = globaltimer();
-    if (rank == 0 && S.deferred) {
-      // the peer's sorted (key, index) items, copied whole over DSMEM
-      // (16-byte coalesced reads) into this CTA's kbi + idx16 (the histogram
-      // and the sorted sizes there are no longer needed), gathered locally
-      unsigned* kv = batch_kv(S);
-      const uint4* pk = reinterpret_cast<const uint4*>(cl.map_shared_rank(kv, 1));
-      constexpr int kWords = kFusedSlots / 4;
-      for (int q = threadIdx.x; q < kWords; q += kFusedT) reinterpret_cast<uint4*>(kv)[q] = pk[q];
-      __syncthreads();
-      kept_output(a, b, S, kv);
-    }
-    cl.sync();  // the peer's shared memory is free again
+    if (rank == 1 && S.deferred == q + 1) kept_output(a, b, S, batch_kv(S));
+    cl.sync();  // rank 1's shared memory is free for the next batch's cells
+    if (a.prof && rank == 1 && threadIdx.x == 0) a.prof[b * kProfSlots + 59] = globaltimer();
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 59] = globaltimer();
   }
   if (a.prof && threadIdx.x == 0) atomicMax(a.prof + 63, globaltimer());

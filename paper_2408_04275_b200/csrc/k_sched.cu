@@ -3,6 +3,8 @@
 // (reference: src/pipeline_sim.cpp, src/simulate.cpp, src/cost_model.cpp).
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "sched.cuh"
 
@@ -1264,6 +1266,39 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
   } else {
     group_sims_kernel<<<grid, T, 0, stream>>>(a, static_cast<double*>(scratch));
   }
+  return cudaGetLastError();
+}
+
+// Per-microbatch token sums of a stream's groups as a simulation reads them
+// (warning log only): out[gid * l + i] = the token sum of microbatch i of
+// coupled group gid in a's order (input / intra / inter, assembled sums when
+// span > 1).  Thread per (group, microbatch).
+__global__ void mb_tokens_kernel(const __grid_constant__ GroupSimArgs a, int* out) {
+  const long long total = a.n_batches * a.groups * static_cast<long long>(a.l);
+  for (long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long gid = x / a.l;
+    const int i = static_cast<int>(x - gid * a.l);
+    const long long b = gid / a.groups;
+    const int grp = static_cast<int>(gid - b * a.groups);
+    const int src = a.order ? a.order[gid * a.l + i] : i;
+    int t;
+    if (a.span == 1) {
+      const long long x0 = b * a.tok.n + static_cast<long long>(grp) * a.l + src;
+      if (a.tok.wide[b]) t = (a.staged ? a.tok.t32_staged : a.tok.t32)[x0];
+      else t = (a.staged && a.tok.kept[b] ? a.tok.t16_staged : a.tok.t16)[x0];
+    } else {
+      t = a.mbsum[gid * a.l + src];
+    }
+    out[x] = t;
+  }
+}
+
+cudaError_t launch_mb_tokens(const GroupSimArgs& a, int* out, cudaStream_t stream) {
+  const long long total = a.n_batches * a.groups * static_cast<long long>(a.l);
+  if (total == 0) return cudaSuccess;
+  const unsigned grid = static_cast<unsigned>(std::min<long long>((total + 255) / 256, 148 * 16));
+  mb_tokens_kernel<<<grid, 256, 0, stream>>>(a, out);
   return cudaGetLastError();
 }
 

@@ -249,6 +249,8 @@ struct GroupSimArgs {
   double* busy;
   DevErr* err;
 };
+// Per-microbatch token sums in a's order (warning log), out[groups * l].
+cudaError_t launch_mb_tokens(const GroupSimArgs& a, int* out, cudaStream_t stream);
 __device__ __forceinline__ bool sim_skipped(const GroupSimArgs& a, long long gid) {
   return a.only_kept != nullptr && a.only_kept[gid / a.groups] == 0;
 }

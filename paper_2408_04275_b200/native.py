@@ -41,7 +41,7 @@ REQUIRED = [
     "model_orchestration", "orchestration_shard_dev", "best_reduce_dev",
     "peer_buffer_create", "peer_buffer_destroy", "peer_group_open", "peer_group_close",
     "shard_range", "reorder_stream_shard_dev", "reorder_stream_graph_create", "graph_launch",
-    "graph_destroy",
+    "graph_destroy", "warnings_enable", "warnings_count", "warning_at", "warnings_clear",
 ]
 
 

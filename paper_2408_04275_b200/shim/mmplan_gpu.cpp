@@ -56,6 +56,17 @@ struct Expose {
 };
 template struct Expose<RowsTag, &CostProfile::rows_>;
 
+// ---- CostModel's warning sink (private member; same technique)
+struct SinkTag {
+  using type = std::vector<std::string>* CostModel::*;
+  friend type sink_member(SinkTag);
+};
+template <typename Tag, typename Tag::type M>
+struct ExposeSink {
+  friend typename Tag::type sink_member(Tag) { return M; }
+};
+template struct ExposeSink<SinkTag, &CostModel::warnings_>;
+
 // ---- one context per process (device 0, or DTB_SHIM_DEVICE)
 dtb_context* ctx() {
   static dtb_context* c = [] {
@@ -192,6 +203,24 @@ struct CM {
   CM& operator=(const CM&) = delete;
 };
 
+// While a call runs, a sink attached to its CostModel receives what the
+// device path logs (dtb_warnings_*): the reference's strings in the
+// reference's query order (SURVEY.md §8(b) Warnings).
+struct SinkBridge {
+  std::vector<std::string>* sink;
+  explicit SinkBridge(const CostModel& costs) : sink(costs.*sink_member(SinkTag{})) {
+    if (sink != nullptr) dtb_warnings_enable(ctx(), 1);
+  }
+  ~SinkBridge() {
+    if (sink == nullptr) return;
+    const int64_t n = dtb_warnings_count(ctx());
+    for (int64_t i = 0; i < n; ++i) sink->emplace_back(dtb_warning_at(ctx(), i));
+    dtb_warnings_enable(ctx(), 0);
+  }
+  SinkBridge(const SinkBridge&) = delete;
+  SinkBridge& operator=(const SinkBridge&) = delete;
+};
+
 struct CSR {
   std::vector<int32_t> text, io, it, ao, at;
   dtb_samples view{};
@@ -325,6 +354,7 @@ std::vector<int> inter_reorder(const StageTimes& times, std::span<const double> 
 
 std::vector<double> microbatch_fwd_keys(const Plan& plan, const CostModel& costs,
                                         std::span<const Microbatch> microbatches) {
+  const SinkBridge warnings(costs);
   MBs mbs;
   for (const Microbatch& mb : microbatches) mbs.add(mb);
   mbs.seal();
@@ -338,6 +368,7 @@ std::vector<double> microbatch_fwd_keys(const Plan& plan, const CostModel& costs
 
 DisaggregatedResult disaggregated_reorder(std::span<const Sample> batch, const Plan& plan,
                                           const CostModel& costs, const ReorderMode& mode) {
+  const SinkBridge warnings(costs);
   CSR csr(batch);
   CM cm(costs);
   const dtb_plan p = to_c(plan);
@@ -412,6 +443,7 @@ std::vector<double> interval_windows(const StageTimes& times) {
 // ------------------------------------------------------------ simulate.hpp
 IterationResult simulate_iteration(const Plan& plan, const CostModel& costs,
                                    const std::vector<std::vector<Microbatch>>& groups) {
+  const SinkBridge warnings(costs);
   MBs mbs;
   std::vector<int64_t> offs{0};
   for (const auto& g : groups) {

@@ -5,7 +5,10 @@ unmodified and linked against the mmplan:: GPU shim
 reorder / pipeline_sim / simulate / orchestrator implementations, so every
 hot-path call they make runs on the B200 through libdisttrain_b200.so
 (oracle/refcheck/Makefile builds oracle/_ref/refcheck in the build
-container; the binary travels to the GPU box)."""
+container; the binary travels to the GPU box).  One more TEST_CASE of our own
+(oracle/refcheck/shim_warnings.cpp) checks that the shim forwards a
+CostModel's warning sink string for string against the reference functions
+linked into the same binary."""
 import os
 import subprocess
 
