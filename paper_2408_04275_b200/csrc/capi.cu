@@ -1286,6 +1286,8 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
     CU(launch_assemble(n_batches, n, dp_lm, dp_me, tok, false, mb0.as<int>(), s));
   }
   // token-indexed cost table shared by both simulations and the inter kernel
+  // (built on the side stream before the cost pass it measured slower: its
+  // CTAs delay the cost pass's first wave)
   const int tsize = static_cast<int>(std::min<long long>(
       static_cast<long long>(span) * 0x8000, static_cast<long long>(kCostTableMax)));
   CU(tab_eg.alloc(sizeof(double4) * tsize, s));
@@ -1354,8 +1356,15 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
     CU(launch_group_sims(gb, scr2.p, ctx->side));
     CU(cudaEventRecord(ev_after, ctx->side));
   }
-  CU(launch_group_sims(ga, scr.p, s));
-  CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, tb, s));
+  if (group_sims_fuse_reduce(ga)) {  // the kernel writes t_iter_before itself
+    GroupSimArgs gr = ga;
+    gr.t_iter = tb;
+    gr.dp_sync = cm->model.dp_sync_seconds;
+    CU(launch_group_sims(gr, scr.p, s));
+  } else {
+    CU(launch_group_sims(ga, scr.p, s));
+    CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, tb, s));
+  }
   if (after_on_side) {
     CU(cudaStreamWaitEvent(s, ev_after, 0));
     CU(launch_t_iter_reduce(n_batches, dp_me, tgrp2.as<double>(), cm->model.dp_sync_seconds, ta, s,

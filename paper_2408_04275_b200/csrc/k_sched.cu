@@ -868,14 +868,35 @@ template <int PE, int PB, int PG, bool BUSY>
 __global__ void __launch_bounds__(kSimT, 4)
 group_sims_tiled(const __grid_constant__ GroupSimArgs a) {
   const long long gid = blockIdx.x * static_cast<long long>(kSimT) + threadIdx.x;
-  if (gid >= a.n_batches * a.groups || sim_skipped(a, gid)) return;
-  // u16 token sums are < 0x8000 <= table.size; assembled sums of u16 batches
-  // are < span * 0x8000 — inside the table unless it was capped
-  const long long b = gid / a.groups;
-  const bool direct = a.tok.wide[b] ||
-                      (a.span > 1 && static_cast<long long>(a.span) * 0x8000 > a.table.size);
-  if (direct) sim_group_direct<PE, PB, PG, BUSY>(&a, gid);
-  else sim_group<PE, PB, PG, BUSY, false>(a, gid);
+  const bool live = gid < a.n_batches * a.groups && !sim_skipped(a, gid);
+  if (live) {
+    // u16 token sums are < 0x8000 <= table.size; assembled sums of u16
+    // batches are < span * 0x8000 — inside the table unless it was capped
+    const long long b = gid / a.groups;
+    const bool direct = a.tok.wide[b] ||
+                        (a.span > 1 && static_cast<long long>(a.span) * 0x8000 > a.table.size);
+    if (direct) sim_group_direct<PE, PB, PG, BUSY>(&a, gid);
+    else sim_group<PE, PB, PG, BUSY, false>(a, gid);
+  }
+  if (a.t_iter == nullptr) return;
+  // fused t_iter_reduce (groups == kSimT: this CTA is batch blockIdx.x):
+  // slowest group (max is exact in any order for these non-negative,
+  // non-NaN makespans) + dp_sync
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const long long b = blockIdx.x;
+    double worst = 0.0;
+    for (int g = threadIdx.x; g < kSimT; g += 32) {
+      const double t = a.t_group[b * kSimT + g];
+      if (t > worst) worst = t;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, worst, o);
+      if (y > worst) worst = y;
+    }
+    if (threadIdx.x == 0) a.t_iter[b] = worst + a.dp_sync;
+  }
 }
 
 using TiledFn = void (*)(GroupSimArgs);
@@ -1209,6 +1230,11 @@ size_t group_sims_scratch(const GroupSimArgs& a) {
   if (fast_sims(a)) return 256;
   const long long per = sim_scratch_per(a.l, plan_stages(a.plan), a.plan.vpp);
   return static_cast<size_t>(a.n_batches * a.groups * per) * sizeof(double) + 256;
+}
+
+bool group_sims_fuse_reduce(const GroupSimArgs& a) {
+  return a.stream && a.plan.vpp == 1 && a.groups == kSimT && a.only_kept == nullptr &&
+         tiled_for<false>(a.plan.unit[0].pp, a.plan.unit[1].pp, a.plan.unit[2].pp) != nullptr;
 }
 
 cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,

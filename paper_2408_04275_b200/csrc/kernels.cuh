@@ -248,12 +248,18 @@ struct GroupSimArgs {
   double* t_group;
   double* busy;
   DevErr* err;
+  // optional [n_batches]: t_iter of each batch (max over its groups +
+  // dp_sync, simulate.cpp:31-46) written by the simulation kernel itself when
+  // group_sims_fuse_reduce(a) (one CTA per batch)
+  double* t_iter;
+  double dp_sync;
 };
 // Per-microbatch token sums in a's order (warning log), out[groups * l].
 cudaError_t launch_mb_tokens(const GroupSimArgs& a, int* out, cudaStream_t stream);
 __device__ __forceinline__ bool sim_skipped(const GroupSimArgs& a, long long gid) {
   return a.only_kept != nullptr && a.only_kept[gid / a.groups] == 0;
 }
+bool group_sims_fuse_reduce(const GroupSimArgs& a);
 cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
                               cudaStream_t stream);
 size_t group_sims_scratch(const GroupSimArgs& a);

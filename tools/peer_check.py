@@ -107,8 +107,21 @@ def main():
             pl._check(lib.reorder_stream_graph_create(pl.ctx, cm.h, C.byref(plan), C.byref(mode),
                                                       C.byref(ds), nb, group, None,
                                                       *[ptr(x) for x in mine], C.byref(g)))
+            # this rank's batch range alone on this GPU (no exchange)
+            first, count = pl.shard_range(nb, rank, world)
+            # (offsets are absolute into the whole CSR: only the offset arrays move)
+            dsh = A.Samples(count * bs, None,
+                            C.cast(d[0].data_ptr() + 4 * first * bs, C.POINTER(C.c_int32)),
+                            C.cast(d[1].data_ptr(), C.POINTER(C.c_int32)),
+                            C.cast(d[2].data_ptr() + 4 * first * bs, C.POINTER(C.c_int32)),
+                            C.cast(d[3].data_ptr(), C.POINTER(C.c_int32)))
+            half = [torch.empty(count * bs, dtype=torch.int32, device="cuda"), f64(count * dp),
+                    f64(count * dp), f64(count), f64(count), torch.empty(count, dtype=torch.uint8, device="cuda")]
+            local = lambda: pl._check(lib.reorder_stream_dev(pl.ctx, cm.h, C.byref(plan), C.byref(mode),
+                                                             C.byref(dsh), count, *[ptr(x) for x in half], sh))
             with torch.cuda.stream(stream):
                 t_one = timed(one)
+                t_local = timed(local)
                 t_shard = timed(shard)
                 t_graph = timed(lambda: pl._check(lib.graph_launch(g, sh)))
             pl._check(lib.graph_destroy(g))
@@ -116,6 +129,7 @@ def main():
             dist.all_reduce(res, op=dist.ReduceOp.MIN)
             results[f"{fam} inter={inter}"] = {
                 "batches": nb, "all_ranks_bit_exact": bool(res.item()), "ms_single_gpu": t_one,
+                "ms_own_range_no_exchange": t_local,
                 "ms_sharded_with_exchange": t_shard, "speedup": t_one / t_shard,
                 "ms_sharded_graph": t_graph, "speedup_graph": t_one / t_graph}
             pl.peer_group_close(group)
