@@ -593,9 +593,10 @@ cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream) {
   // (a persistent double-buffered variant — 5 CTAs of two stages per SM,
   // copies of chunk i + 1 in flight while chunk i computes — measured
   // slower: 95 µs at 128 threads, 101-105 µs at 256, vs 80 µs)
-  static const cudaError_t carve =
-      cudaFuncSetAttribute(cost_stream_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (carve != cudaSuccess) return carve;
+  // (set on every launch: the attribute is per device, like the partition
+  // kernel's shared-memory opt-in)
+  e = cudaFuncSetAttribute(cost_stream_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
   cost_stream_kernel<<<static_cast<unsigned>(grid), kCostT, 0, stream>>>(a);
   cost_finalize_kernel<<<static_cast<unsigned>(a.n_batches), kCostT, 0, stream>>>(a);
   return cudaGetLastError();
