@@ -1188,16 +1188,23 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   // it overlaps everything after the order is final (the simulations).
   // `after`: the stream on which the order became final.
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
-  auto exchange = [&](cudaStream_t after) -> cudaError_t {
+  // phase 0: the whole range, then the flag barrier; phase 1: the batches
+  // the cost pass decided (after the cost pass, next to the partition
+  // kernel); phase 2: the rest and the barrier.
+  auto exchange = [&](cudaStream_t after, int phase, const unsigned* state) -> cudaError_t {
     if (peer == nullptr) return cudaSuccess;
-    cudaError_t e = cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+    cudaError_t e = cudaSuccess;
+    if (ev_ready == nullptr) e = cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess && ev_done == nullptr)
+      e = cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(ev_ready, after);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->xchg, ev_ready, 0);
     PeerBcast pb = *peer;
     pb.src = order_out;
+    pb.phase = phase;
+    pb.state = state;
     if (e == cudaSuccess) e = launch_peer_broadcast(pb, ctx->xchg);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_done, ctx->xchg);
+    if (e == cudaSuccess && phase != 1) e = cudaEventRecord(ev_done, ctx->xchg);
     return e;
   };
   cudaEvent_t ev_fork = nullptr, ev_part = nullptr;  // partition kernel on ctx->side
@@ -1275,9 +1282,17 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   CU(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   CU(launch_sort_partition(fa, n_batches, cscr, s, ctx->side, ev_fork));
   CU(cudaEventRecord(ev_part, ctx->side));
-  // the intra order is the output order: exchanged right after the partition
-  // kernel, next to everything that follows it
-  if (!compose_needed) CU(exchange(ctx->side));
+  // the intra order is the output order: the batches the cost pass decided
+  // are exchanged right after it (their order is the identity, final), the
+  // rest right after the partition kernel — both next to the simulations
+  if (!compose_needed) {
+    if (fa.state != nullptr) {
+      CU(exchange(s, 1, fa.state));
+      CU(exchange(ctx->side, 2, fa.state));
+    } else {
+      CU(exchange(ctx->side, 0, nullptr));
+    }
+  }
   const TokSrc tok{tok16.as<unsigned short>(), tok16s.as<unsigned short>(), tok32.as<int>(),
                    tok32s.as<int>(), kept_dev, wflag.as<unsigned int>(), n};
   if (span > 1) {  // assembled microbatch sums [b][e][i] (input order: cost pass only)
@@ -1396,7 +1411,7 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
   if (compose_needed) {
     CU(launch_compose(n_batches, n, dp_lm, dp_me, intra_out, mode->inter ? inter.as<int>() : nullptr,
                       order_out, s));
-    CU(exchange(s));
+    CU(exchange(s, 0, nullptr));
   }
   ga.staged = true;
   ga.mbsum = span > 1 ? mb1.as<int>() : nullptr;
@@ -1569,7 +1584,8 @@ dtb_status dtb_reorder_stream_shard_dev(dtb_context* ctx, const dtb_cost_model* 
     pb.flags[p] = group->flags[p];
     al = al && (reinterpret_cast<uintptr_t>(pb.dst[p]) & 15u) == 0;
   }
-  pb.aligned = al ? 1 : 0;
+  pb.aligned = al && n % 8 == 0 ? 1 : 0;
+  pb.n = static_cast<int>(n);
   if (count == 0) {  // nothing to reorder; still take part in the barrier
     CU(launch_peer_broadcast(pb, s));
     return DTB_OK;

@@ -23,12 +23,20 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 }
 
 __global__ void __launch_bounds__(256) peer_broadcast_kernel(const __grid_constant__ PeerBcast a) {
+  // this phase's batches (a packet of 8 samples never straddles two batches:
+  // the packed path requires n % 8 == 0)
+  auto mine = [&](long long i) -> bool {
+    if (a.phase == 0) return true;
+    const bool decided = a.state[i / a.n] == kBatchDecided;
+    return a.phase == 1 ? decided : !decided;
+  };
   // ---- data: 8 samples per thread and step (two 16-byte loads, one 16-byte
   // store per replica)
   const long long n8 = a.aligned ? a.count >> 3 : 0;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   const long long t0 = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   for (long long q = t0; q < n8; q += stride) {
+    if (!mine(8 * q)) continue;
     const int4 x0 = reinterpret_cast<const int4*>(a.src)[2 * q];
     const int4 x1 = reinterpret_cast<const int4*>(a.src)[2 * q + 1];
     const uint4 v = make_uint4(static_cast<unsigned>(x0.x) | (static_cast<unsigned>(x0.y) << 16),
@@ -39,7 +47,9 @@ __global__ void __launch_bounds__(256) peer_broadcast_kernel(const __grid_consta
     for (int p = 0; p < a.world; ++p) reinterpret_cast<uint4*>(a.dst[p])[q] = v;
   }
   for (long long i = (n8 << 3) + t0; i < a.count; i += stride)  // tail / unaligned
-    for (int p = 0; p < a.world; ++p) a.dst[p][i] = static_cast<unsigned short>(a.src[i]);
+    if (mine(i))
+      for (int p = 0; p < a.world; ++p) a.dst[p][i] = static_cast<unsigned short>(a.src[i]);
+  if (a.phase == 1) return;  // the barrier closes phase 2
   // ---- barrier: every thread's peer stores precede its CTA's arrival; the
   // last CTA releases this rank's flag in every replica and acquires every
   // peer's flag in the local one

@@ -99,6 +99,12 @@ struct PeerBcast {
   unsigned* done;                   // CTA counter (zeroed by the launcher)
   unsigned* epoch;                  // this rank's call counter (device; graph-replay safe)
   int world, rank, aligned;         // aligned: src / dst 16-byte aligned
+  // phase 0: every batch, then the flag barrier.  With the cost pass's
+  // per-batch state: phase 1 sends the batches it decided (their order is
+  // final before the partition kernel runs), phase 2 the rest, then the
+  // barrier.  n: samples per global batch.
+  const unsigned* state;
+  int n, phase;
 };
 cudaError_t launch_peer_broadcast(const PeerBcast& a, cudaStream_t stream);
 
