@@ -122,15 +122,25 @@ constexpr int kRB = 7;                              // radix digit bits
 //              slot `slot` of group g (capP = cap padded to 2 mod 4: bank
 //              spread); the sort passes park their per-item ranks here.
 constexpr int kFusedSlots = kFusedT * kFusedItems;  // sort slots incl. padding
-struct NarrowSmem {
-  unsigned short kbi[kFusedSlots];
-  alignas(16) unsigned short idx16[kFusedSlots];
-  alignas(16) unsigned short out16[kFusedMaxN + 4 * kNarrowMaxM];
-  int radix_cnt[(1 << kRB) * (kFusedT / 32) + 1];
+constexpr int kCells = kFusedMaxN + 4 * kNarrowMaxM;  // (group, slot) cells, padded groups
+// Per-batch state of the histogram path's greedy and decision.
+struct BatchState {
   FusedGreedySmem G;
   WarpGreedySmem WG;
   unsigned blk_ident[kNarrowMaxM], blk_greedy[kNarrowMaxM];
   int off[kNarrowMaxM];
+  unsigned keep_flag;  // the decision, broadcast from warp 0
+  int zc;              // zero-cost samples
+};
+struct NarrowSmem {
+  unsigned short kbi[kFusedSlots];
+  alignas(16) unsigned short idx16[kFusedSlots];
+  alignas(16) unsigned short out16[kCells];
+  BatchState A;  // every single-batch path
+  // a second batch whose greedy runs next to A's (descending order, one
+  // warp each): its cells, its state
+  alignas(16) unsigned short cellsB[kCells];
+  BatchState B;
   int tmp[kFusedT / 32 + 3];
   long long tmpll[kFusedT / 32 + 1];
   unsigned int s_and, s_or;
@@ -139,7 +149,6 @@ struct NarrowSmem {
   // sort_abort once the batch is decided NOT kept (rank 1's speculative sort
   // is then useless and stops at its next pass)
   unsigned pair_epoch, sort_abort, sort_go;
-  unsigned keep_flag;  // fast path: the decision, broadcast from warp 0
 };
 constexpr int kSortRB = 5;  // narrow-path digit bits (per-thread counters)
 // per-thread radix counters of the narrow path (their own space, so the
@@ -150,6 +159,7 @@ struct SortSmem {
 };
 
 constexpr size_t kFusedSmem = sizeof(SortSmem);
+static_assert(kFusedSmem + 1024 <= 227 * 1024, "one partition CTA per SM: 227 KB of shared memory");
 
 // The kernel's dynamic shared memory as NarrowSmem.  Non-inlined device
 // functions re-derive it here instead of taking a reference argument, so the
@@ -247,7 +257,7 @@ __device__ __noinline__ void fused_wide(const FusedArgs& a, long long b, NarrowS
   if (a.intra) {
     const int lo = varying ? __ffs(static_cast<int>(varying)) - 1 : 0;
     const int hi = varying ? 32 - __clz(static_cast<int>(varying)) : 0;
-    tile_radix_sort<kFusedT, kFusedItems, kRB>(keys, vals, n, lo, hi, S.radix_cnt, S.tmp);
+    tile_radix_sort<kFusedT, kFusedItems, kRB>(keys, vals, n, lo, hi, reinterpret_cast<int*>(sort_counters()), S.tmp);
     const int z0 = desc ? n - tot_zeros : 0;
     const int z1 = desc ? n : tot_zeros;
     const int cap = (n + m - 1) / m;
@@ -402,21 +412,50 @@ __device__ __noinline__ void sort_batch_keys(const FusedArgs& a, long long b, Na
   }
 }
 
-// Outputs of a kept batch from the greedy's cells (this CTA) and the sorted
-// (key, index) items `kv` (this CTA's, or a copy of the cluster peer's): the
-// intra order and its staged tokens, coalesced per group.
-__device__ __noinline__ void kept_output(const FusedArgs& a, long long b, NarrowSmem&,
-                                         const unsigned* kv) {
-  NarrowSmem& S = shared_state();
+// The histogram path's buffers of batch slot W (0: A — every
+// single-batch path; 1: B — the second batch of a two-batch descending step):
+// token histogram (8,192 bins as u16 pairs), sorted sizes, the greedy's
+// (group, slot) cells, the batch state.  B's histogram and sorted sizes live
+// where A's are dead by then (the sort counters, A's histogram).
+template <int W>
+__device__ __forceinline__ unsigned* fp_hist_buf() {
+  if constexpr (W) return sort_counters();
+  else return reinterpret_cast<unsigned*>(shared_state().kbi);
+}
+template <int W>
+__device__ __forceinline__ unsigned short* fp_skey() {
+  if constexpr (W) return shared_state().kbi;
+  else return shared_state().idx16;
+}
+template <int W>
+__device__ __forceinline__ unsigned short* fp_cells() {
+  if constexpr (W) return shared_state().cellsB;
+  else return shared_state().out16;
+}
+template <int W>
+__device__ __forceinline__ BatchState& fp_state() {
+  if constexpr (W) return shared_state().B;
+  else return shared_state().A;
+}
+static_assert(kHistBins * 2 <= 4 * blocked_cnt_words(kFusedT, kSortRB),
+              "batch B's histogram fits the sort counters");
+
+// Outputs of a kept batch from the greedy's cells of slot W and the
+// sorted (key, index) items `kv` (this CTA's, or a cluster peer's handed
+// over): the intra order and its staged tokens, coalesced per group.
+template <int W>
+__device__ __noinline__ void kept_output(const FusedArgs& a, long long b, const unsigned* kv) {
+  const unsigned short* cells = fp_cells<W>();
+  BatchState& T = fp_state<W>();
   const int n = a.n, m = a.m, lane = lane_id(), w = warp_id();
   const long long first = b * n;
   const bool desc = a.order == DTB_DESCENDING;
   const int cap = (n + m - 1) / m;
   const int capP = ((cap + 1) | 3) - 1;
   for (int g = w; g < m; g += kFusedT / 32) {
-    const int base = S.off[g], cnt = S.G.gcnt[g];
+    const int base = T.off[g], cnt = T.G.gcnt[g];
     for (int slot = lane; slot < cnt; slot += 32) {
-      const unsigned item = kv[swz(S.out16[g * capP + slot])];
+      const unsigned item = kv[swz(cells[g * capP + slot])];
       a.order_out[first + base + slot] = static_cast<int>(item & 0xffffu);
       if (a.tok16_staged != nullptr) {
         const unsigned k = item >> 16;
@@ -431,143 +470,190 @@ __device__ __noinline__ void kept_output(const FusedArgs& a, long long b, Narrow
 // the sorted size sequence is the histogram's expansion: the greedy, its
 // block loads and the keep decision (src/reorder.cpp:340-354) need no
 // permutation.  Only a batch whose greedy split is kept needs the stable
-// sort, and then only as a counting scatter (the histogram's starts are the
-// cursors): two warps walk the batch halves in index order, ranking equal
-// tokens within 32 samples with MATCH, so ties keep index order
-// (src/reorder.cpp:34-40).
-__device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSmem&,
-                                      bool defer_kept) {
-  NarrowSmem& S = shared_state();  // shared address space: LDS/STS, not generic
-  const int n = a.n, m = a.m, tid = threadIdx.x, lane = lane_id(), w = warp_id();
+// sort of its samples (sort_batch_keys; src/reorder.cpp:30-42).
+//
+// Phases (slot W): fp_hist (histogram of the cost pass's u16 tokens,
+// identity block loads), fp_prep (sorted sizes), the greedy (ascending: 8
+// warps over named barrier 1; descending: one warp), fp_decide (keep
+// decision), fp_output (loads, kept flag, kept order).
+
+// Token histogram of batch b and its identity block loads (from the cost
+// pass).  All threads.
+template <int W>
+__device__ __forceinline__ void fp_hist(const FusedArgs& a, long long b) {
+  unsigned* hist = fp_hist_buf<W>();
+  BatchState& T = fp_state<W>();
+  const int n = a.n, m = a.m, tid = threadIdx.x;
   const long long first = b * n;
-  const int pg = n / m;
+  for (int q = tid; q < kHistBins / 8; q += kFusedT)
+    reinterpret_cast<uint4*>(hist)[q] = make_uint4(0, 0, 0, 0);
+  for (int g = tid; g < m; g += kFusedT) T.blk_ident[g] = a.blk_ident[b * m + g];
+  __syncthreads();
+  constexpr int V = 3;  // 128-bit loads in flight per thread and round
+  const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
+  const int nv = n >> 3;
+  unsigned z = 0u;
+  for (int v0 = 0; v0 * kFusedT < nv; v0 += V) {
+    uint4 q[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int idx = tid + (v0 + v) * kFusedT;
+      q[v] = idx < nv ? __ldg(src + idx) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int idx = tid + (v0 + v) * kFusedT;
+      if (idx >= nv) break;
+      const unsigned words[4] = {q[v].x, q[v].y, q[v].z, q[v].w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const unsigned t = (words[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        if (t == 0u)
+          ++z;
+        else
+          atomicAdd(hist + (t >> 1), 1u << ((t & 1u) << 4));
+      }
+    }
+  }
+  z = __reduce_add_sync(kFull, z);
+  if (lane_id() == 0 && z) atomicAdd(hist, z);
+  __syncthreads();
+}
+
+// Sorted sizes skey[p] = token of sorted position p: starts of every token
+// value (ascending: exclusive prefix; descending: n - inclusive prefix), run
+// heads skey[start] = tok + 1 over a zeroed skey, then a "last non-zero"
+// fill-forward scan.  All threads.
+template <int W>
+__device__ __forceinline__ void fp_prep(const FusedArgs& a, long long b) {
+  NarrowSmem& S = shared_state();
+  const unsigned* hist = fp_hist_buf<W>();
+  unsigned short* skey = fp_skey<W>();
+  BatchState& T = fp_state<W>();
+  const int n = a.n, tid = threadIdx.x;
   const bool desc = a.order == DTB_DESCENDING;
-  unsigned* hist = reinterpret_cast<unsigned*>(S.kbi);
-  unsigned short* skey = S.idx16;
-  bool keep = false;
+  if (tid == 0) T.zc = static_cast<int>(hist[0] & 0xffffu);
+  for (int q = tid; q < kFusedSlots / 8; q += kFusedT)
+    reinterpret_cast<uint4*>(skey)[q] = make_uint4(0, 0, 0, 0);
+  constexpr int kWordsPer = kHistBins / 2 / kFusedT;  // 4 words = 8 bins per thread
+  static_assert(kWordsPer % 4 == 0 && kWordsPer >= 4, "scan layout");
+  int sum = 0;
+#pragma unroll
+  for (int q = 0; q < kWordsPer / 4; ++q) {
+    const uint4 v = reinterpret_cast<const uint4*>(hist + tid * kWordsPer)[q];
+    sum += static_cast<int>((v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) +
+                            (v.z & 0xffffu) + (v.z >> 16) + (v.w & 0xffffu) + (v.w >> 16));
+  }
+  int tot;
+  int base = block_excl_scan<kFusedT>(sum, S.tmp, &tot);  // also orders the zeroing
+  {
+    unsigned c[kWordsPer];  // re-read: nothing held across the scan
+#pragma unroll
+    for (int q = 0; q < kWordsPer / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4*>(hist + tid * kWordsPer)[q];
+      c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int q = 0; q < kWordsPer; ++q) {
+      const int lo = static_cast<int>(c[q] & 0xffffu), hi = static_cast<int>(c[q] >> 16);
+      const unsigned v0 = static_cast<unsigned>(tid * 2 * kWordsPer + 2 * q);
+      const int s0 = desc ? n - (base + lo) : base;
+      const int s1 = desc ? n - (base + lo + hi) : base + lo;
+      base += lo + hi;
+      if (lo) skey[s0] = static_cast<unsigned short>(v0 + 1);
+      if (hi) skey[s1] = static_cast<unsigned short>(v0 + 2);
+    }
+  }
+  __syncthreads();
+  constexpr int C = kFusedSlots / kFusedT;  // positions per thread (16 = 2 x 16 bytes)
+  static_assert(C % 8 == 0, "fill-forward chunks of 16 bytes");
+  const int p0 = tid * C;
+  unsigned last = 0u;
+#pragma unroll
+  for (int q = 0; q < C / 8; ++q) {
+    const uint4 v = reinterpret_cast<const uint4*>(skey + p0)[q];
+    const unsigned wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const unsigned e = (wd[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
+      if (e) last = e;
+    }
+  }
+  unsigned run;
+  block_last_nz(last, S.tmp, &run);
+#pragma unroll
+  for (int q = 0; q < C / 8; ++q) {
+    const uint4 v = reinterpret_cast<const uint4*>(skey + p0)[q];  // re-read: no registers held across the scan
+    unsigned wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const unsigned e = (wd[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
+      if (e) run = e;
+      const unsigned val = (run - 1u) & 0xffffu;
+      wd[h >> 1] = (h & 1) ? ((wd[h >> 1] & 0xffffu) | (val << 16)) : ((wd[h >> 1] & 0xffff0000u) | val);
+    }
+    reinterpret_cast<uint4*>(skey + p0)[q] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  }
+  __syncthreads();
+}
+
+// The equal-count greedy over slot W's sorted sizes (reference:
+// src/reorder.cpp:70-90): descending on warp W, ascending on threads
+// [0, 256) over named barrier 1.  The caller brackets it with __syncthreads.
+template <int W>
+__device__ __forceinline__ void fp_greedy(const FusedArgs& a, long long b) {
+  const unsigned short* skey = fp_skey<W>();
+  unsigned short* cells = fp_cells<W>();
+  BatchState& T = fp_state<W>();
+  const int n = a.n, m = a.m, tid = threadIdx.x, w = warp_id();
+  const bool desc = a.order == DTB_DESCENDING;
   const int cap = (n + m - 1) / m;
   const int capP = ((cap + 1) | 3) - 1;
-  if (a.intra) {
-    const int zc = static_cast<int>(hist[0] & 0xffffu);
-    // ---- 1. starts of every token value in the sorted order (ascending:
-    // exclusive prefix; descending: n - inclusive prefix) and run heads
-    // skey[start] = tok + 1 over a zeroed skey
-    for (int q = tid; q < kFusedSlots / 8; q += kFusedT)
-      reinterpret_cast<uint4*>(skey)[q] = make_uint4(0, 0, 0, 0);
-    constexpr int kScanT = kFusedT;                      // threads owning bins
-    constexpr int kWordsPer = kHistBins / 2 / kScanT;    // 4 words = 8 bins per thread
-    static_assert(kWordsPer % 4 == 0 && kWordsPer >= 4, "scan layout");
-    int sum = 0;
-    if (tid < kScanT) {
-#pragma unroll
-      for (int q = 0; q < kWordsPer / 4; ++q) {
-        const uint4 v = reinterpret_cast<const uint4*>(hist + tid * kWordsPer)[q];
-        sum += static_cast<int>((v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) +
-                                (v.z & 0xffffu) + (v.z >> 16) + (v.w & 0xffffu) + (v.w >> 16));
-      }
+  const int zc = T.zc;
+  const int z0 = desc ? n - zc : 0;
+  const int z1 = desc ? n : zc;
+  auto size_at = [&](int k) -> unsigned {
+    const unsigned t = skey[k];
+    return t + t;
+  };
+  auto emit = [&](int k, int g, int slot) { cells[g * capP + slot] = static_cast<unsigned short>(k); };
+  constexpr int kGT = 256;
+  unsigned long long* gprof = a.prof ? a.prof + b * kProfSlots + 6 : nullptr;
+  if (desc) {
+    // u32 keys (load << 8 | gid) while every load stays below 2^24
+    if (w == W) {
+      if (static_cast<long long>(cap) * 2 * (kHistBins - 1) < (1ll << 24))
+        greedy_warp<unsigned>(n, m, cap, z0, z1, size_at, emit, T.WG, T.G.gload, T.G.gcnt, gprof);
+      else
+        greedy_warp<unsigned long long>(n, m, cap, z0, z1, size_at, emit, T.WG, T.G.gload, T.G.gcnt,
+                                        gprof);
     }
-    int tot;
-    int base = block_excl_scan<kFusedT>(sum, S.tmp, &tot);  // also orders the zeroing
-    if (tid < kScanT) {
-      unsigned c[kWordsPer];  // re-read: nothing held across the scan
-#pragma unroll
-      for (int q = 0; q < kWordsPer / 4; ++q) {
-        const uint4 v = reinterpret_cast<const uint4*>(hist + tid * kWordsPer)[q];
-        c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
-      }
-#pragma unroll
-      for (int q = 0; q < kWordsPer; ++q) {
-        const int lo = static_cast<int>(c[q] & 0xffffu), hi = static_cast<int>(c[q] >> 16);
-        const unsigned v0 = static_cast<unsigned>(tid * 2 * kWordsPer + 2 * q);
-        const int s0 = desc ? n - (base + lo) : base;
-        const int s1 = desc ? n - (base + lo + hi) : base + lo;
-        base += lo + hi;
-        if (lo) skey[s0] = static_cast<unsigned short>(v0 + 1);
-        if (hi) skey[s1] = static_cast<unsigned short>(v0 + 2);
-        c[q] = static_cast<unsigned>(s0) | (static_cast<unsigned>(s1) << 16);
-      }
-#pragma unroll
-      for (int q = 0; q < kWordsPer / 4; ++q)
-        reinterpret_cast<uint4*>(hist + tid * kWordsPer)[q] =
-            make_uint4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
-    }
-    __syncthreads();
-    // ---- 2. fill forward: skey[p] = token of sorted position p
-    {
-      constexpr int C = kFusedSlots / kFusedT;  // positions per thread (16 = 2 x 16 bytes)
-      static_assert(C % 8 == 0, "fill-forward chunks of 16 bytes");
-      const int p0 = tid * C;
-      const bool mine = p0 < kFusedSlots;
-      unsigned last = 0u;
-      if (mine) {
-#pragma unroll
-        for (int q = 0; q < C / 8; ++q) {
-          const uint4 v = reinterpret_cast<const uint4*>(skey + p0)[q];
-          const unsigned wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const unsigned e = (wd[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
-            if (e) last = e;
-          }
-        }
-      }
-      unsigned run;
-      block_last_nz(last, S.tmp, &run);
-      if (mine) {
-#pragma unroll
-        for (int q = 0; q < C / 8; ++q) {
-          const uint4 v = reinterpret_cast<const uint4*>(skey + p0)[q];  // re-read: no registers held across the scan
-          unsigned wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const unsigned e = (wd[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
-            if (e) run = e;
-            const unsigned val = (run - 1u) & 0xffffu;
-            wd[h >> 1] = (h & 1) ? ((wd[h >> 1] & 0xffffu) | (val << 16)) : ((wd[h >> 1] & 0xffff0000u) | val);
-          }
-          reinterpret_cast<uint4*>(skey + p0)[q] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-        }
-      }
-      __syncthreads();
-    }
-    if (a.prof && tid == 0) a.prof[b * kProfSlots + 2] = globaltimer();
-    // ---- 3. greedy equal-count partition over the sorted sizes
-    const int z0 = desc ? n - zc : 0;
-    const int z1 = desc ? n : zc;
-    auto size_at = [&](int k) -> unsigned {
-      const unsigned t = skey[k];
-      return t + t;
-    };
-    auto emit = [&](int k, int g, int slot) {
-      S.out16[g * capP + slot] = static_cast<unsigned short>(k);
-    };
-    // ascending: the greedy runs on 8 warps over named barrier 1 (its full
-    // rounds are block-parallel; 8-warp barriers are much cheaper than
-    // 32-warp ones); descending (every round a general one): on one warp
-    constexpr int kGT = 256;
-    unsigned long long* gprof = a.prof ? a.prof + b * kProfSlots + 6 : nullptr;
-    if (desc) {
-      // u32 keys (load << 8 | gid) while every load stays below 2^24
-      if (w == 0) {
-        if (static_cast<long long>(cap) * 2 * (kHistBins - 1) < (1ll << 24))
-          greedy_warp<unsigned>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt, gprof);
-        else
-          greedy_warp<unsigned long long>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt,
-                                          gprof);
-      }
-    } else if (tid < kGT) {
-      greedy_fused<kGT, true, 1>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll, gprof);
-    }
-    __syncthreads();
-    if (a.prof && tid == 0) a.prof[b * kProfSlots + 3] = globaltimer();
-    // ---- 4. group offsets of the flat order, greedy block loads, decision
-    // (m <= 128 groups: one warp, 4 groups per lane, no block barriers)
-    if (w == 0) {
+  } else if (tid < kGT) {  // (ascending: slot A only)
+    greedy_fused<kGT, true, 1>(n, m, cap, z0, z1, size_at, emit, T.G, shared_state().tmp,
+                               shared_state().tmpll, gprof);
+  }
+}
+
+// Group offsets of the flat order, greedy block loads and the keep
+// decision (src/reorder.cpp:340-354, exact integer loads) on one warp; the
+// caller's __syncthreads publishes T.keep_flag.  Needs the slot's sorted
+// sizes (n % m != 0) and cells.
+template <int W>
+__device__ __forceinline__ void fp_decide(const FusedArgs& a) {
+  const unsigned short* skey = fp_skey<W>();
+  const unsigned short* cells = fp_cells<W>();
+  BatchState& T = fp_state<W>();
+  const int n = a.n, m = a.m, lane = lane_id(), w = warp_id();
+  const int pg = n / m;
+  const int cap = (n + m - 1) / m;
+  const int capP = ((cap + 1) | 3) - 1;
+  {
+    if (w == 0) {  // m <= 128 groups: 4 per lane, no block barriers
       int cnt[4], sum = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int g = 4 * lane + e;
-        cnt[e] = g < m ? S.G.gcnt[g] : 0;
+        cnt[e] = g < m ? T.G.gcnt[g] : 0;
         sum += cnt[e];
       }
       int incl = sum;
@@ -580,7 +666,7 @@ __device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSm
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int g = 4 * lane + e;
-        if (g < m) S.off[g] = base;
+        if (g < m) T.off[g] = base;
         base += cnt[e];
       }
       unsigned mg = 0u, mi = 0u;
@@ -589,76 +675,119 @@ __device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSm
         for (int e = 0; e < 4; ++e) {
           const int g = 4 * lane + e;
           if (g < m) {
-            const unsigned l = S.G.gload[g];
-            S.blk_greedy[g] = l;
+            const unsigned l = T.G.gload[g];
+            T.blk_greedy[g] = l;
             mg = max(mg, l);
-            mi = max(mi, S.blk_ident[g]);
+            mi = max(mi, T.blk_ident[g]);
           }
         }
       } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (4 * lane + e < m) S.blk_greedy[4 * lane + e] = 0u;
+          if (4 * lane + e < m) T.blk_greedy[4 * lane + e] = 0u;
         __syncwarp();
         for (int g = 0; g < m; ++g)
-          for (int slot = lane; slot < S.G.gcnt[g]; slot += 32) {
-            const int pos = S.off[g] + slot;
-            atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], size_at(S.out16[g * capP + slot]));
+          for (int slot = lane; slot < T.G.gcnt[g]; slot += 32) {
+            const int pos = T.off[g] + slot;
+            const unsigned t = skey[cells[g * capP + slot]];
+            atomicAdd(&T.blk_greedy[min(pos / pg, m - 1)], t + t);
           }
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int g = 4 * lane + e;
           if (g < m) {
-            mg = max(mg, S.blk_greedy[g]);
-            mi = max(mi, S.blk_ident[g]);
+            mg = max(mg, T.blk_greedy[g]);
+            mi = max(mi, T.blk_ident[g]);
           }
         }
       }
       mg = __reduce_max_sync(kFull, mg);
       mi = __reduce_max_sync(kFull, mi);
-      if (lane == 0) S.keep_flag = mg <= mi ? 1u : 0u;  // src/reorder.cpp:350-353 (exact integer loads)
+      if (lane == 0) T.keep_flag = mg <= mi ? 1u : 0u;
     }
-    __syncthreads();
-    keep = S.keep_flag != 0u;
   }
+}
+
+// The outputs after fp_decide (and a __syncthreads): loads, kept flag, and
+// for a kept batch its order — sorted here (the sort reuses kbi / idx16 and
+// the counters), or (defer_kept, cluster pair) handed to the peer that
+// sorted it.  All threads.
+template <int W>
+__device__ __forceinline__ void fp_output(const FusedArgs& a, long long b, bool defer_kept) {
+  NarrowSmem& S = shared_state();
+  BatchState& T = fp_state<W>();
+  const int n = a.n, m = a.m, tid = threadIdx.x;
+  const long long first = b * n;
+  const bool keep = a.intra && T.keep_flag != 0u;
   if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
   for (int g = tid; g < m; g += kFusedT)
-    write_outputs_common(a, b, g, S.blk_ident[g], keep ? S.blk_greedy[g] : S.blk_ident[g]);
+    write_outputs_common(a, b, g, T.blk_ident[g], keep ? T.blk_greedy[g] : T.blk_ident[g]);
   if (a.prof && tid == 0) a.prof[b * kProfSlots + 4] = globaltimer();
   if (!keep) {
     if (defer_kept && tid == 0)  // stop the peer's speculative sort
       *reinterpret_cast<volatile unsigned*>(cg::this_cluster().map_shared_rank(&S.sort_abort, 1)) =
           S.pair_epoch;
     if (a.state == nullptr) identity_order_out(a, first, n);  // else written by the cost pass
-  } else {
-    // ---- 5. kept: the permutation (here, or by the cluster peer)
-    if (defer_kept) {
-      // hand this CTA's cells, group offsets and counts to the cluster peer,
-      // which holds the sorted items (DSMEM stores: no round trips), and mark
-      // the batch there; the peer writes the kept order after the cluster sync
-      cg::cluster_group cl = cg::this_cluster();
-      uint4* dst = reinterpret_cast<uint4*>(cl.map_shared_rank(S.out16, 1));
-      const uint4* src = reinterpret_cast<const uint4*>(S.out16);
-      constexpr int kCellWords = static_cast<int>(sizeof(NarrowSmem::out16) / 16);
-      for (int q = tid; q < kCellWords; q += kFusedT) dst[q] = src[q];
-      int* doff = cl.map_shared_rank(S.off, 1);
-      int* dcnt = cl.map_shared_rank(S.G.gcnt, 1);
-      for (int g = tid; g < m; g += kFusedT) {
-        doff[g] = S.off[g];
-        dcnt[g] = S.G.gcnt[g];
-      }
-      if (tid == 0) *cl.map_shared_rank(&S.deferred, 1) = S.pair_epoch;
-    } else {
-      __syncthreads();
-      sort_batch_keys(a, b, S);
-      kept_output(a, b, S, batch_kv(S));
+  } else if (defer_kept) {  // (slot A)
+    // hand this CTA's cells, group offsets and counts to the cluster peer,
+    // which holds the sorted items (DSMEM stores: no round trips), and mark
+    // the batch there; the peer writes the kept order after the cluster sync
+    cg::cluster_group cl = cg::this_cluster();
+    uint4* dst = reinterpret_cast<uint4*>(cl.map_shared_rank(S.out16, 1));
+    const uint4* src = reinterpret_cast<const uint4*>(S.out16);
+    constexpr int kCellWords = static_cast<int>(sizeof(NarrowSmem::out16) / 16);
+    for (int q = tid; q < kCellWords; q += kFusedT) dst[q] = src[q];
+    int* doff = cl.map_shared_rank(S.A.off, 1);
+    int* dcnt = cl.map_shared_rank(S.A.G.gcnt, 1);
+    for (int g = tid; g < m; g += kFusedT) {
+      doff[g] = S.A.off[g];
+      dcnt[g] = S.A.G.gcnt[g];
     }
+    if (tid == 0) *cl.map_shared_rank(&S.deferred, 1) = S.pair_epoch;
+  } else {  // the permutation, here
+    __syncthreads();
+    sort_batch_keys(a, b, S);
+    kept_output<W>(a, b, batch_kv(S));
   }
   if (a.prof) {
     __syncthreads();
     if (tid == 0) a.prof[b * kProfSlots + 5] = globaltimer();
   }
+}
+
+// One batch on the histogram path (slot A).
+__device__ __noinline__ void fast_path(const FusedArgs& a, long long b, NarrowSmem&,
+                                      bool defer_kept) {
+  if (a.intra) {
+    fp_prep<0>(a, b);
+    if (a.prof && threadIdx.x == 0) a.prof[b * kProfSlots + 2] = globaltimer();
+    fp_greedy<0>(a, b);
+    __syncthreads();
+    if (a.prof && threadIdx.x == 0) a.prof[b * kProfSlots + 3] = globaltimer();
+    fp_decide<0>(a);
+    __syncthreads();
+  }
+  fp_output<0>(a, b, defer_kept);
+}
+
+// Two batches on the histogram path, descending order: their one-warp
+// greedies (all rounds general: ~95% of a batch's time) run side by side on
+// warps 0 and 1; everything else is block-wide, one batch after the other.
+__device__ __noinline__ void fast_path_two_desc(const FusedArgs& a, long long b0, long long b1) {
+  fp_hist<0>(a, b0);
+  fp_prep<0>(a, b0);
+  fp_hist<1>(a, b1);
+  fp_prep<1>(a, b1);
+  if (warp_id() == 0) fp_greedy<0>(a, b0);
+  else if (warp_id() == 1) fp_greedy<1>(a, b1);
+  __syncthreads();
+  fp_decide<0>(a);
+  fp_decide<1>(a);  // (warp 0 both: before A's sort reuses B's sorted sizes)
+  __syncthreads();
+  fp_output<0>(a, b0, false);
+  __syncthreads();
+  fp_output<1>(a, b1, false);
 }
 
 // Sort path of the 16-bit layout (token sums up to 0x7fff, or the separate
@@ -674,7 +803,7 @@ __device__ __noinline__ void narrow_sort_path(const FusedArgs& a, long long b, N
   const int pg = n / m;
   const bool desc = a.order == DTB_DESCENDING;
   __syncthreads();
-  for (int g = tid; g < m; g += kFusedT) S.blk_ident[g] = 0u;
+  for (int g = tid; g < m; g += kFusedT) S.A.blk_ident[g] = 0u;
   if (tid == 0) {
     S.s_and = ~0u;
     S.s_or = 0u;
@@ -719,10 +848,10 @@ __device__ __noinline__ void narrow_sort_path(const FusedArgs& a, long long b, N
           run += 2u * t;
         } else {
           const unsigned qd = a.div_pg.div(static_cast<unsigned>(i));
-          atomicAdd(&S.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2u * t);
+          atomicAdd(&S.A.blk_ident[min(qd, static_cast<unsigned>(m - 1))], 2u * t);
         }
       }
-      if (blk0 == blk7) atomicAdd(&S.blk_ident[blk0], run);
+      if (blk0 == blk7) atomicAdd(&S.A.blk_ident[blk0], run);
     }
   }
   // sort padding: key 0xffff has the largest digit in every pass
@@ -776,38 +905,38 @@ __device__ __noinline__ void narrow_sort_path(const FusedArgs& a, long long b, N
       // u32 keys (load << 8 | gid) while every load stays below 2^24
       if (w == 0) {
         if (static_cast<long long>(cap) * 2 * 0x7fff < (1ll << 24))
-          greedy_warp<unsigned>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt, gprof);
+          greedy_warp<unsigned>(n, m, cap, z0, z1, size_at, emit, S.A.WG, S.A.G.gload, S.A.G.gcnt, gprof);
         else
-          greedy_warp<unsigned long long>(n, m, cap, z0, z1, size_at, emit, S.WG, S.G.gload, S.G.gcnt,
+          greedy_warp<unsigned long long>(n, m, cap, z0, z1, size_at, emit, S.A.WG, S.A.G.gload, S.A.G.gcnt,
                                           gprof);
       }
     } else if (tid < kGT) {
-      greedy_fused<kGT, true, 1>(n, m, cap, z0, z1, size_at, emit, S.G, S.tmp, S.tmpll, gprof);
+      greedy_fused<kGT, true, 1>(n, m, cap, z0, z1, size_at, emit, S.A.G, S.tmp, S.tmpll, gprof);
     }
     __syncthreads();
     if (a.prof && tid == 0) a.prof[b * kProfSlots + 3] = globaltimer();
     // ---- group offsets of the flat order and the greedy block loads
-    int c = tid < m ? S.G.gcnt[tid] : 0, tot;
+    int c = tid < m ? S.A.G.gcnt[tid] : 0, tot;
     const int o = block_excl_scan<kFusedT>(c, S.tmp, &tot);
-    if (tid < m) S.off[tid] = o;
+    if (tid < m) S.A.off[tid] = o;
     if (n % m == 0) {
       // blocks are the groups (every group holds cap = n / m items)
-      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = S.G.gload[g];
+      for (int g = tid; g < m; g += kFusedT) S.A.blk_greedy[g] = S.A.G.gload[g];
     } else {
-      for (int g = tid; g < m; g += kFusedT) S.blk_greedy[g] = 0u;
+      for (int g = tid; g < m; g += kFusedT) S.A.blk_greedy[g] = 0u;
       __syncthreads();
       for (int g = w; g < m; g += kFusedT / 32) {
-        for (int slot = lane; slot < S.G.gcnt[g]; slot += 32) {
-          const int pos = S.off[g] + slot;
-          atomicAdd(&S.blk_greedy[min(pos / pg, m - 1)], size_at(S.out16[g * capP + slot]));
+        for (int slot = lane; slot < S.A.G.gcnt[g]; slot += 32) {
+          const int pos = S.A.off[g] + slot;
+          atomicAdd(&S.A.blk_greedy[min(pos / pg, m - 1)], size_at(S.out16[g * capP + slot]));
         }
       }
     }
     __syncthreads();
     unsigned mg = 0u, mi = 0u;
     for (int g = tid; g < m; g += kFusedT) {
-      mg = max(mg, S.blk_greedy[g]);
-      mi = max(mi, S.blk_ident[g]);
+      mg = max(mg, S.A.blk_greedy[g]);
+      mi = max(mi, S.A.blk_ident[g]);
     }
     mg = static_cast<unsigned>(block_max_ll<kFusedT>(mg, S.tmpll));
     mi = static_cast<unsigned>(block_max_ll<kFusedT>(mi, S.tmpll));
@@ -819,14 +948,14 @@ __device__ __noinline__ void narrow_sort_path(const FusedArgs& a, long long b, N
   }
   if (tid == 0 && a.kept != nullptr) a.kept[b] = keep ? 1 : 0;
   for (int g = tid; g < m; g += kFusedT)
-    write_outputs_common(a, b, g, S.blk_ident[g], keep ? S.blk_greedy[g] : S.blk_ident[g]);
+    write_outputs_common(a, b, g, S.A.blk_ident[g], keep ? S.A.blk_greedy[g] : S.A.blk_ident[g]);
   if (a.prof && tid == 0) a.prof[b * kProfSlots + 4] = globaltimer();
   // ---- outputs, coalesced: one warp per group, lanes over its slots — the
   // intra order and, when the greedy split is kept, its per-position tokens
   // (identity batches reuse the input-order tokens, see TokSrc)
   if (keep) {
     for (int g = w; g < m; g += kFusedT / 32) {
-      const int base = S.off[g], cnt = S.G.gcnt[g];
+      const int base = S.A.off[g], cnt = S.A.G.gcnt[g];
       for (int slot = lane; slot < cnt; slot += 32) {
         const unsigned idx = S.idx16[swz(S.out16[g * capP + slot])];
         const unsigned key = S.kbi[idx];
@@ -869,42 +998,7 @@ __device__ __forceinline__ void process_batch(const FusedArgs& a, long long b, N
   }
   // ---- histogram path: token histogram from the cost pass's u16 tokens;
   // identity block loads from the cost pass
-  unsigned* hist = reinterpret_cast<unsigned*>(S.kbi);
-  for (int q = tid; q < kHistBins / 8; q += kFusedT)
-    reinterpret_cast<uint4*>(hist)[q] = make_uint4(0, 0, 0, 0);
-  for (int g = tid; g < m; g += kFusedT) S.blk_ident[g] = a.blk_ident[b * m + g];
-  __syncthreads();
-  {
-    constexpr int V = 3;  // 128-bit loads in flight per thread and round
-    const uint4* src = reinterpret_cast<const uint4*>(a.tok16 + first);
-    const int nv = n >> 3;
-    unsigned z = 0u;
-    for (int v0 = 0; v0 * kFusedT < nv; v0 += V) {
-    uint4 q[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int idx = tid + (v0 + v) * kFusedT;
-      q[v] = idx < nv ? __ldg(src + idx) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int idx = tid + (v0 + v) * kFusedT;
-      if (idx >= nv) break;
-      const unsigned words[4] = {q[v].x, q[v].y, q[v].z, q[v].w};
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const unsigned t = (words[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-        if (t == 0u)
-          ++z;
-        else
-          atomicAdd(hist + (t >> 1), 1u << ((t & 1u) << 4));
-      }
-    }
-    }
-    z = __reduce_add_sync(kFull, z);
-    if (lane_id() == 0 && z) atomicAdd(hist, z);
-  }
-  __syncthreads();
+  fp_hist<0>(a, b);
   if (a.prof && tid == 0) a.prof[b * kProfSlots + 1] = globaltimer();
   fast_path(a, b, S, defer_kept);
 }
@@ -926,7 +1020,25 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   const unsigned count = a.list[0];
   const unsigned pairs = gridDim.x / 2;  // launched as clusters of two CTAs
   if (count > pairs) {  // many batches: every CTA takes its own
-    for (unsigned q = blockIdx.x; q < count; q += gridDim.x) {
+    const bool desc = a.order == DTB_DESCENDING && a.intra && a.m <= kNarrowMaxM &&
+                      a.n <= kFusedMaxN && (a.n & 7) == 0;
+    auto fast = [&](long long b) { return a.state[b] == kBatchFast; };
+    unsigned q = blockIdx.x;
+    if (desc) {  // two histogram-path batches at a time: their greedies side by side
+      for (; q + gridDim.x < count; q += 2 * gridDim.x) {
+        const long long b0 = a.list[1 + q], b1 = a.list[1 + q + gridDim.x];
+        if (fast(b0) && fast(b1)) {
+          if (a.prof && threadIdx.x == 0) a.prof[b0 * kProfSlots + 0] = globaltimer();
+          fast_path_two_desc(a, b0, b1);
+        } else {
+          process_batch(a, b0, S);
+          __syncthreads();
+          process_batch(a, b1, S);
+        }
+        __syncthreads();  // the shared state is reused by the next batches
+      }
+    }
+    for (; q < count; q += gridDim.x) {
       process_batch(a, a.list[1 + q], S);
       __syncthreads();  // the shared state is reused by the next batch
     }
@@ -956,7 +1068,7 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
     }
     cl.sync();  // rank 1: its sorted items and (kept) rank 0's cells are ready
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 58] = globaltimer();
-    if (rank == 1 && S.deferred == q + 1) kept_output(a, b, S, batch_kv(S));
+    if (rank == 1 && S.deferred == q + 1) kept_output<0>(a, b, batch_kv(S));
     cl.sync();  // rank 1's shared memory is free for the next batch's cells
     if (a.prof && rank == 1 && threadIdx.x == 0) a.prof[b * kProfSlots + 59] = globaltimer();
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 59] = globaltimer();
