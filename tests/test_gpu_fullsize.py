@@ -61,6 +61,20 @@ def test_c4_full_stream_intra(gpu, ora, c4_stream):
     _compare(ra, rb, "C4 intra, 1024 batches")
 
 
+@pytest.mark.parametrize("bs,dp,nb,fam", [(2048, 16, 301, "mixed"), (2056, 16, 240, "dense"),
+                                          (16384, 128, 160, "mixed")])
+def test_descending_many_batches(gpu, ora, bs, dp, nb, fam):
+    """More listed batches than CTA pairs: the partition kernel's
+    single-CTA mode, which in descending order runs two batches per CTA
+    with their one-warp greedies side by side (odd counts, n % m != 0)."""
+    ci, co = _desk(gpu, ora)
+    pl = H.plan((1, dp, 1), (1, dp, 2), (1, dp, 1), bs)
+    s = synth_stream(nb * bs, seed=4242 + bs, family=fam)
+    ra = gpu.reorder_stream(ci, pl, s, nb, inter=False, sort_order=DESCENDING)
+    rb = ora.reorder_stream(co, pl, s, nb, inter=False, sort_order=DESCENDING)
+    _compare(ra, rb, f"descending {nb} x {bs} {fam}")
+
+
 def test_c4_descending(gpu, ora, c4_stream):
     ci, co = _desk(gpu, ora)
     pl = H.plan((1, 128, 1), (1, 128, 2), (1, 128, 1), 16384)
