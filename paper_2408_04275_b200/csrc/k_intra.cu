@@ -598,39 +598,47 @@ __device__ __forceinline__ void fp_prep(const FusedArgs& a, long long b) {
 }
 
 // The equal-count greedy over slot W's sorted sizes (reference:
-// src/reorder.cpp:70-90): descending on warp W, ascending on threads
-// [0, 256) over named barrier 1.  The caller brackets it with __syncthreads.
-template <int W>
-__device__ __forceinline__ void fp_greedy(const FusedArgs& a, long long b) {
+// src/reorder.cpp:70-90): descending on warp W; ascending on all threads
+// (greedy_asc_block).  The caller brackets it with __syncthreads.
+// (each variant its own function: separate register allocation)
+template <int W, bool DESC>
+__device__ __noinline__ void fp_greedy_run(const FusedArgs& a, long long b) {
   const unsigned short* skey = fp_skey<W>();
   unsigned short* cells = fp_cells<W>();
   BatchState& T = fp_state<W>();
-  const int n = a.n, m = a.m, tid = threadIdx.x, w = warp_id();
-  const bool desc = a.order == DTB_DESCENDING;
+  const int n = a.n, m = a.m;
   const int cap = (n + m - 1) / m;
   const int capP = ((cap + 1) | 3) - 1;
   const int zc = T.zc;
-  const int z0 = desc ? n - zc : 0;
-  const int z1 = desc ? n : zc;
   auto size_at = [&](int k) -> unsigned {
     const unsigned t = skey[k];
     return t + t;
   };
   auto emit = [&](int k, int g, int slot) { cells[g * capP + slot] = static_cast<unsigned short>(k); };
-  constexpr int kGT = 256;
-  unsigned long long* gprof = a.prof ? a.prof + b * kProfSlots + 6 : nullptr;
-  if (desc) {
-    // u32 keys (load << 8 | gid) while every load stays below 2^24
-    if (w == W) {
-      if (static_cast<long long>(cap) * 2 * (kHistBins - 1) < (1ll << 24))
-        greedy_warp<unsigned>(n, m, cap, z0, z1, size_at, emit, T.WG, T.G.gload, T.G.gcnt, gprof);
-      else
-        greedy_warp<unsigned long long>(n, m, cap, z0, z1, size_at, emit, T.WG, T.G.gload, T.G.gcnt,
-                                        gprof);
-    }
-  } else if (tid < kGT) {  // (ascending: slot A only)
-    greedy_fused<kGT, true, 1>(n, m, cap, z0, z1, size_at, emit, T.G, shared_state().tmp,
-                               shared_state().tmpll, gprof);
+  // u32 keys (load << 8 | gid) while every load stays below 2^24
+  const bool k32 = static_cast<long long>(cap) * 2 * (kHistBins - 1) < (1ll << 24);
+  if constexpr (DESC) {  // warp W
+    unsigned long long* gprof = a.prof ? a.prof + b * kProfSlots + 6 : nullptr;
+    if (k32)
+      greedy_warp<unsigned>(n, m, cap, n - zc, n, size_at, emit, T.WG, T.G.gload, T.G.gcnt, gprof);
+    else
+      greedy_warp<unsigned long long>(n, m, cap, n - zc, n, size_at, emit, T.WG, T.G.gload,
+                                      T.G.gcnt, gprof);
+  } else {  // threads [0, 256), named barrier 1 (8-warp barriers: much cheaper than 32-warp ones)
+    constexpr int kGT = 256;
+    unsigned long long* gprof = a.prof ? a.prof + b * kProfSlots + 6 : nullptr;
+    if (threadIdx.x < kGT)
+      greedy_fused<kGT, true, 1>(n, m, cap, 0, zc, size_at, emit, T.G, shared_state().tmp,
+                                 shared_state().tmpll, gprof);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void fp_greedy(const FusedArgs& a, long long b) {
+  if (a.order == DTB_DESCENDING) {
+    if (warp_id() == W) fp_greedy_run<W, true>(a, b);
+  } else {
+    fp_greedy_run<W, false>(a, b);  // (slot A only)
   }
 }
 
@@ -779,8 +787,8 @@ __device__ __noinline__ void fast_path_two_desc(const FusedArgs& a, long long b0
   fp_prep<0>(a, b0);
   fp_hist<1>(a, b1);
   fp_prep<1>(a, b1);
-  if (warp_id() == 0) fp_greedy<0>(a, b0);
-  else if (warp_id() == 1) fp_greedy<1>(a, b1);
+  if (warp_id() == 0) fp_greedy_run<0, true>(a, b0);
+  else if (warp_id() == 1) fp_greedy_run<1, true>(a, b1);
   __syncthreads();
   fp_decide<0>(a);
   fp_decide<1>(a);  // (warp 0 both: before A's sort reuses B's sorted sizes)
