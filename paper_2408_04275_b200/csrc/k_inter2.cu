@@ -123,8 +123,14 @@ inter_tok_kernel(const __grid_constant__ InterArgs a) {
   auto F = [&](int i) -> double& { return colF[static_cast<size_t>(i) * T + t]; };
   auto G = [&](int i) -> double& { return colG[static_cast<size_t>(i) * T + t]; };
   auto K = [&](int i) -> double& { return colK[static_cast<size_t>(i) * T + t]; };
-  auto TK = [&](int i) -> unsigned short& { return colT[static_cast<size_t>(i) * T + t]; };
-  auto RET = [&](int i) -> unsigned char& { return colR[static_cast<size_t>(i) * T + t]; };
+  // u16 / u8 columns: the 32 lanes of a warp read 32 different rows, so each
+  // lane's element gets its own bank — lane j of warp w at column 2j + (w & 1)
+  // (u16) / 4j + (w & 3) (u8) of its 64- / 128-thread block (T % 128 == 0)
+  const bool swz_ok = (T & 127) == 0;
+  const int ct = swz_ok ? (t & ~63) + 2 * (t & 31) + ((t >> 5) & 1) : t;
+  const int cr = swz_ok ? (t & ~127) + 4 * (t & 31) + ((t >> 5) & 3) : t;
+  auto TK = [&](int i) -> unsigned short& { return colT[static_cast<size_t>(i) * T + ct]; };
+  auto RET = [&](int i) -> unsigned char& { return colR[static_cast<size_t>(i) * T + cr]; };
   auto BE = [&](int pos) -> double& { return colBE[static_cast<size_t>(pos % kBRing) * T + t]; };
   auto BG = [&](int pos) -> double& { return colBG[static_cast<size_t>(pos % kBRing) * T + t]; };
   auto Fv = [&](int i) -> double {
