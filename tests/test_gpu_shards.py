@@ -9,7 +9,9 @@
   dtb_reorder_stream_dev; the replica holds the ordering as u16.
 * With two or more GPUs visible: tools/peer_check.py under torchrun (two
   ranks, NCCL for the handle exchange only) — every rank's replica and outputs
-  bit-exact against a single-GPU reorder of the whole stream.
+  bit-exact against a single-GPU reorder of the whole stream, and the search
+  sharded over the two ranks, folded on the device, equal to
+  model_orchestration's winner.
 """
 import ctypes as C
 import json

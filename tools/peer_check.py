@@ -1,6 +1,8 @@
 """Multi-GPU check of dtb_reorder_stream_shard_dev (run under torchrun, one
 process per GPU): every rank reorders its batch range of ONE stream and the
-library exchanges the ordering over NVLink into every rank's replica.  Each
+library exchanges the ordering over NVLink into every rank's replica.  Also
+the search sharded over the ranks (dtb_orchestration_shard_dev), the winners
+all-gathered and folded by dtb_best_reduce_dev, against model_orchestration.  Each
 rank checks the whole replica against a single-GPU reorder of the whole
 stream (dtb_reorder_stream_dev on its own GPU) and its per-batch outputs at
 its own batch positions; then times the sharded step (CUDA events, max over
@@ -135,6 +137,34 @@ def main():
             pl.peer_group_close(group)
             dist.barrier()
             pl.peer_buffer_destroy(replica)
+    # the search sharded over the ranks (dtb_orchestration_shard_dev), the
+    # winners all-gathered and folded on the device (dtb_best_reduce_dev)
+    from paper_2408_04275_b200.api import PlanSpec, stats_to_c
+    m72, cl72, bk72 = H.mllm72b_model(), H.a800_cluster(1172), H.mllm72b_book()
+    st72 = stats_to_c(m72.seq_len, 2048.0, 2048.0)
+    cm72 = pl.cost_model(m72, cl72, bk72)
+    want = pl.model_orchestration(cm72, st72, 1920)
+    csz = C.sizeof(A.Candidate)
+    rec = torch.zeros(csz, dtype=torch.uint8, device="cuda")
+    evn = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sh0 = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    pl._check(lib.orchestration_shard_dev(pl.ctx, cm72.h, C.byref(st72), 1920, 1, rank, world,
+                                          C.c_void_p(rec.data_ptr()), C.c_void_p(evn.data_ptr()), sh0))
+    recs = torch.zeros(world * csz, dtype=torch.uint8, device="cuda")
+    evs = torch.zeros(world, dtype=torch.int64, device="cuda")
+    dist.all_gather_into_tensor(recs, rec)
+    dist.all_gather_into_tensor(evs, evn)
+    best = torch.zeros(csz, dtype=torch.uint8, device="cuda")
+    pl._check(lib.best_reduce_dev(pl.ctx, C.c_void_p(recs.data_ptr()), world, C.c_void_p(best.data_ptr()), sh0))
+    torch.cuda.synchronize()
+    c = A.Candidate.from_buffer_copy(best.cpu().numpy().tobytes())
+    ok_search = bool(c.feasible == 1 and PlanSpec.from_c(c.plan) == want["best"] and
+                     (c.times.t_warm, c.times.t_steady, c.times.t_iter) == want["times"] and
+                     int(evs.sum().item()) == want["candidates_evaluated"])
+    res = torch.tensor([1 if ok_search else 0], dtype=torch.int32, device="cuda")
+    dist.all_reduce(res, op=dist.ReduceOp.MIN)
+    results["search sharded"] = {"all_ranks_bit_exact": bool(res.item()),
+                                 "candidates": int(evs.sum().item())}
     if rank == 0:
         print(json.dumps({"world": world, "results": results}, indent=1), flush=True)
     dist.barrier()
