@@ -1375,7 +1375,7 @@ static dtb_status run_stream(dtb_context* ctx, const dtb_cost_model* cm, const d
     GroupSimArgs gr = ga;
     gr.t_iter = tb;
     gr.dp_sync = cm->model.dp_sync_seconds;
-    CU(launch_group_sims(gr, scr.p, s));
+    CU(launch_group_sims(gr, scr.p, s, true));  // programmatic launch after the cost table
   } else {
     CU(launch_group_sims(ga, scr.p, s));
     CU(launch_t_iter_reduce(n_batches, dp_me, tgrp.as<double>(), cm->model.dp_sync_seconds, tb, s));

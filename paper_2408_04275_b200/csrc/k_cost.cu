@@ -29,6 +29,7 @@
 
 #include "block_ops.cuh"
 #include "kernels.cuh"
+#include "pdl.cuh"
 #include "tma.cuh"
 
 namespace dtb {
@@ -270,6 +271,7 @@ __device__ __noinline__ void small_batch(const CostArgs& a, long long b, unsigne
 // state; batches the partition kernel must process are appended to `list`.
 __global__ void __launch_bounds__(kCostT) cost_finalize_kernel(const __grid_constant__ CostArgs a) {
   __shared__ long long red[kCostT / 32 + 1];
+  pdl_wait();  // the cost pass's statistics
   const int m = a.m, tid = threadIdx.x;
   const long long b = blockIdx.x;
   const unsigned* st = a.bstat + 4 * b;
@@ -598,7 +600,9 @@ cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream) {
   e = cudaFuncSetAttribute(cost_stream_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cost_stream_kernel<<<static_cast<unsigned>(grid), kCostT, 0, stream>>>(a);
-  cost_finalize_kernel<<<static_cast<unsigned>(a.n_batches), kCostT, 0, stream>>>(a);
+  e = launch_pdl(cost_finalize_kernel, dim3(static_cast<unsigned>(a.n_batches)), dim3(kCostT), 0,
+                 stream, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

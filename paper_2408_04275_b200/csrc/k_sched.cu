@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "pdl.cuh"
 #include "sched.cuh"
 
 #ifndef DTB_SIM_EXPERIMENT
@@ -867,6 +868,7 @@ __device__ __noinline__ void sim_group_direct(const GroupSimArgs* a, long long g
 template <int PE, int PB, int PG, bool BUSY>
 __global__ void __launch_bounds__(kSimT, 4)
 group_sims_tiled(const __grid_constant__ GroupSimArgs a) {
+  pdl_wait();  // tokens, flags, cost table of the preceding kernels
   const long long gid = blockIdx.x * static_cast<long long>(kSimT) + threadIdx.x;
   const bool live = gid < a.n_batches * a.groups && !sim_skipped(a, gid);
   if (live) {
@@ -1238,7 +1240,7 @@ bool group_sims_fuse_reduce(const GroupSimArgs& a) {
 }
 
 cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, bool pdl) {
   const long long total = a.n_batches * a.groups;
   if (total == 0) return cudaSuccess;
   const int T = 128;
@@ -1256,6 +1258,7 @@ cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
       // rows a stream touches, token sums <= seq_len, are ~260 KB)
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, DTB_SIM_CARVEOUT);
       const unsigned g = static_cast<unsigned>((total + kSimT - 1) / kSimT);
+      if (pdl) return launch_pdl(fn, dim3(g), dim3(kSimT), 0, stream, a);
       fn<<<g, kSimT, 0, stream>>>(a);
       return cudaGetLastError();
     }
@@ -1331,6 +1334,9 @@ cudaError_t launch_mb_tokens(const GroupSimArgs& a, int* out, cudaStream_t strea
 // Token-indexed cost table (see CostTable): thread per token sum s.
 __global__ void cost_table_kernel(DevCM cm, dtb_plan plan, int span, int size, double4* eg,
                                   double* key, DevErr* err) {
+  // the table reads only the cost model, but the kernels after it rely on
+  // everything before it being complete (PDL waits chain one kernel back)
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= size) return;
   UnitEval ue, ug;
@@ -1348,7 +1354,9 @@ __global__ void cost_table_kernel(DevCM cm, dtb_plan plan, int span, int size, d
 cudaError_t launch_cost_table(const DevCM& cm, const dtb_plan& plan, int span, int size,
                               double4* eg, double* key, DevErr* err, cudaStream_t stream) {
   if (size <= 0) return cudaSuccess;
-  cost_table_kernel<<<(size + 255) / 256, 256, 0, stream>>>(cm, plan, span, size, eg, key, err);
+  cudaError_t e = launch_pdl(cost_table_kernel, dim3((size + 255) / 256), dim3(256), 0, stream, cm,
+                             plan, span, size, eg, key, err);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

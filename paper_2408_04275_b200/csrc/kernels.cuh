@@ -267,7 +267,7 @@ __device__ __forceinline__ bool sim_skipped(const GroupSimArgs& a, long long gid
 }
 bool group_sims_fuse_reduce(const GroupSimArgs& a);
 cudaError_t launch_group_sims(const GroupSimArgs& a, void* scratch,
-                              cudaStream_t stream);
+                              cudaStream_t stream, bool pdl = false);
 size_t group_sims_scratch(const GroupSimArgs& a);
 
 // ------------------------------------------------- exhaustive orderings
