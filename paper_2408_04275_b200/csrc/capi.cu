@@ -1123,7 +1123,7 @@ static cudaError_t launch_sort_partition(FusedArgs& fa, long long n_batches, DBu
     if (e != cudaSuccess) return e;
     return launch_intra_fused(fa, n_batches, side);
   }
-  return launch_intra_fused(fa, n_batches, s);
+  return launch_intra_fused(fa, n_batches, s, true);
 }
 
 // Warning log of a stream call: the queries disaggregated_reorder makes per

@@ -26,6 +26,7 @@
 #include "greedy_fused.cuh"
 #include "greedy_warp.cuh"
 #include "kernels.cuh"
+#include "pdl.cuh"
 #include "tma.cuh"
 
 namespace dtb {
@@ -1017,6 +1018,7 @@ __global__ void __launch_bounds__(kFusedT, DTB_FUSED_MIN_BLOCKS)
 intra_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   NarrowSmem& S = *reinterpret_cast<NarrowSmem*>(smem_raw);
+  pdl_wait();  // the cost pass's list and batch states
   if (a.prof && threadIdx.x == 0) {  // debug: first CTA entry, last CTA exit
     atomicMin(a.prof + 62, globaltimer());
     atomicMax(a.prof + 63, 0ull);
@@ -1085,7 +1087,8 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
 }
 
 // ------------------------------------------------------------- host glue
-cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches, cudaStream_t stream) {
+cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches, cudaStream_t stream,
+                               bool pdl) {
   // the opt-in is per device: set it on every launch (cheap), so contexts on
   // several devices and several host threads need no shared state
   cudaError_t e = cudaFuncSetAttribute(intra_fused_kernel,
@@ -1103,13 +1106,17 @@ cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches, cudaStre
     cfg.blockDim = dim3(kFusedT);
     cfg.dynamicSmemBytes = kFusedSmem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic launch right behind the cost pass's finalize kernel (same
+    // stream, no event wait in between)
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, intra_fused_kernel, a);
   }
   intra_fused_kernel<<<static_cast<unsigned>(grid), kFusedT, kFusedSmem, stream>>>(a);

@@ -133,7 +133,7 @@ size_t fused_smem_bytes();
 int fused_max_n();
 int fused_max_m();
 cudaError_t launch_intra_fused(const FusedArgs& a, long long n_batches,
-                               cudaStream_t stream);
+                               cudaStream_t stream, bool pdl = false);
 
 size_t intra_generic_scratch(int n, int m);
 int intra_generic_max_m();
