@@ -304,6 +304,7 @@ __device__ void tile_pass_blocked(unsigned short* idx, const unsigned short* key
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const int dst = static_cast<int>((old[j] >> half) & 0xffffu);
+      DTB_CHECK(dst < T * ITEMS);
       idx[SWZ ? swz(dst) : dst] = static_cast<unsigned short>(v[j]);
     }
   }
@@ -369,6 +370,7 @@ __device__ void tile_pass_kv(unsigned* kv, const DigitFn& digit, unsigned* cntw,
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const int dst = static_cast<int>((old[j] >> half) & 0xffffu);
+      DTB_CHECK(dst < T * ITEMS);
       kv[SWZ ? swz(dst) : dst] = v[j];
     }
   }

@@ -5,12 +5,35 @@
 // (the library is compiled with -fmad=false; no fast-math).
 #pragma once
 
+#include <cstdio>
+
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "disttrain_b200.h"
 
 namespace dtb {
+
+// Debug bounds checks (the pool has no compute-sanitizer): built with
+// DTB_DEFINES=DTB_DEBUG_CHECKS, every DTB_CHECK traps the kernel when its
+// condition fails — the GPU suite run against that build then fails loudly
+// (tools/gpu_run_checks.sh).  Compiled out otherwise.
+#ifdef DTB_DEBUG_CHECKS
+#define DTB_CHECK(cond)                                                         \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      printf("DTB_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond,        \
+             __FILE__, __LINE__, static_cast<int>(blockIdx.x),                  \
+             static_cast<int>(threadIdx.x));                                    \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define DTB_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 
 constexpr int kFull = 0xffffffff;
 

@@ -120,6 +120,7 @@ __device__ void greedy_warp(int n, int m, int cap, int z0, int z1, const SizeFn&
           if (W.pre[mid] <= q) lo = mid;
           else hi = mid - 1;
         }
+        DTB_CHECK(lo >= 0 && lo < r);
         const int g = static_cast<int>(key[lo] & 0xffu);
         emit(k + q, g, W.cnt[g] + (q - W.pre[lo]));
       }

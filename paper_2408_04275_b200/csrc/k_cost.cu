@@ -453,10 +453,12 @@ __device__ __forceinline__ void cost_consume(const CostArgs& a, CostSmem& S, con
     const int* F = S.tk + L.abase - L.afl;
     for (int j0 = 4 * tid; j0 < qs; j0 += 4 * kCostT) {  // qs % 4 == 0 when STAGED
       const int4 o = *reinterpret_cast<const int4*>(io_s + j0);
+      DTB_CHECK(o.x - L.fl >= 0 && io_s[j0 + 4] - L.fl < L.abase);
       const int e0 = E[o.x], e1 = E[o.y], e2 = E[o.z], e3 = E[o.w], e4 = E[io_s[j0 + 4]];
       int v[4] = {e1 - e0, e2 - e1, e3 - e2, e4 - e3};
       if (audio) {
         const int4 p = *reinterpret_cast<const int4*>(ao_s + j0);
+        DTB_CHECK(p.x - L.afl >= 0 && L.abase + ao_s[j0 + 4] - L.afl < L.len);
         const int f0 = F[p.x], f1 = F[p.y], f2 = F[p.z], f3 = F[p.w], f4 = F[ao_s[j0 + 4]];
         v[0] += f1 - f0, v[1] += f2 - f1, v[2] += f3 - f2, v[3] += f4 - f3;
       }

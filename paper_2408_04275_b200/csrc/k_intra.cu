@@ -456,7 +456,10 @@ __device__ __noinline__ void kept_output(const FusedArgs& a, long long b, const 
   for (int g = w; g < m; g += kFusedT / 32) {
     const int base = T.off[g], cnt = T.G.gcnt[g];
     for (int slot = lane; slot < cnt; slot += 32) {
+      DTB_CHECK(g * capP + slot < kCells && base + slot < n);
+      DTB_CHECK(cells[g * capP + slot] < n);
       const unsigned item = kv[swz(cells[g * capP + slot])];
+      DTB_CHECK(static_cast<int>(item & 0xffffu) < n);
       a.order_out[first + base + slot] = static_cast<int>(item & 0xffffu);
       if (a.tok16_staged != nullptr) {
         const unsigned k = item >> 16;
@@ -509,6 +512,7 @@ __device__ __forceinline__ void fp_hist(const FusedArgs& a, long long b) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const unsigned t = (words[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        DTB_CHECK(t < static_cast<unsigned>(kHistBins));
         if (t == 0u)
           ++z;
         else
@@ -561,6 +565,8 @@ __device__ __forceinline__ void fp_prep(const FusedArgs& a, long long b) {
       const int s0 = desc ? n - (base + lo) : base;
       const int s1 = desc ? n - (base + lo + hi) : base + lo;
       base += lo + hi;
+      DTB_CHECK(!lo || (s0 >= 0 && s0 < n));
+      DTB_CHECK(!hi || (s1 >= 0 && s1 < n));
       if (lo) skey[s0] = static_cast<unsigned short>(v0 + 1);
       if (hi) skey[s1] = static_cast<unsigned short>(v0 + 2);
     }
@@ -615,7 +621,10 @@ __device__ __noinline__ void fp_greedy_run(const FusedArgs& a, long long b) {
     const unsigned t = skey[k];
     return t + t;
   };
-  auto emit = [&](int k, int g, int slot) { cells[g * capP + slot] = static_cast<unsigned short>(k); };
+  auto emit = [&](int k, int g, int slot) {
+    DTB_CHECK(g >= 0 && g < m && slot >= 0 && slot < cap && g * capP + slot < kCells && k >= 0 && k < n);
+    cells[g * capP + slot] = static_cast<unsigned short>(k);
+  };
   // u32 keys (load << 8 | gid) while every load stays below 2^24
   const bool k32 = static_cast<long long>(cap) * 2 * (kHistBins - 1) < (1ll << 24);
   if constexpr (DESC) {  // warp W
