@@ -43,6 +43,9 @@ namespace dtb {
 #ifndef DTB_COST_T
 #define DTB_COST_T 128
 #endif
+#ifndef DTB_COST_SCAN_L
+#define DTB_COST_SCAN_L 8
+#endif
 constexpr int kCostT = DTB_COST_T;          // threads per chunk CTA
 constexpr int kCostQ = DTB_COST_Q;          // samples per chunk
 constexpr int kCostOff = kCostQ + 4;        // offsets + the next boundary, padded
@@ -98,16 +101,17 @@ __device__ __forceinline__ ChunkLayout chunk_layout(int lo, int hi, int alo, int
 // four sums, a second pass scans with the carry-in.
 __device__ __forceinline__ bool chunk_prefix(int* tk, int len, int* tmp) {
   constexpr int W = kCostT / 32;
-  constexpr int L = 8;  // consecutive slots per lane and step (two 16-byte words)
+  constexpr int L = DTB_COST_SCAN_L;  // consecutive slots per lane and step (16-byte words)
   const int lane = lane_id(), w = warp_id();
   const int R = (len + W * 32 * L - 1) / (W * 32 * L) * (32 * L);  // slots per warp
   const int beg = w * R, end = min(beg + R, len);
   auto load = [&](int p, int* v) {
     if (p + L <= end) {
-      const int4 x0 = *reinterpret_cast<const int4*>(tk + p);
-      const int4 x1 = *reinterpret_cast<const int4*>(tk + p + 4);
-      v[0] = x0.x, v[1] = x0.y, v[2] = x0.z, v[3] = x0.w;
-      v[4] = x1.x, v[5] = x1.y, v[6] = x1.z, v[7] = x1.w;
+#pragma unroll
+      for (int q = 0; q < L / 4; ++q) {
+        const int4 x = *reinterpret_cast<const int4*>(tk + p + 4 * q);
+        v[4 * q] = x.x, v[4 * q + 1] = x.y, v[4 * q + 2] = x.z, v[4 * q + 3] = x.w;
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < L; ++k) v[k] = p + k < end ? tk[p + k] : 0;
@@ -155,7 +159,10 @@ __device__ __forceinline__ bool chunk_prefix(int* tk, int len, int* tmp) {
       const int e = carry + incl - v[L - 1];  // exclusive carry-in of the lane
       if (p + L <= end) {
         *reinterpret_cast<int4*>(tk + p) = make_int4(e, e + v[0], e + v[1], e + v[2]);
-        *reinterpret_cast<int4*>(tk + p + 4) = make_int4(e + v[3], e + v[4], e + v[5], e + v[6]);
+#pragma unroll
+        for (int q = 1; q < L / 4; ++q)
+          *reinterpret_cast<int4*>(tk + p + 4 * q) =
+              make_int4(e + v[4 * q - 1], e + v[4 * q], e + v[4 * q + 1], e + v[4 * q + 2]);
       } else {
         for (int k = 0; k < L && p + k < end; ++k) tk[p + k] = k ? e + v[k - 1] : e;
       }
@@ -336,11 +343,11 @@ struct ChunkPos {
   long long b, s0;
   int q0, qs;
 };
-__device__ __forceinline__ ChunkPos chunk_pos(const CostArgs& a, long long c) {
-  const int cpb = (a.n + kCostQ - 1) / kCostQ;
+__device__ __forceinline__ ChunkPos chunk_pos(const CostArgs& a, unsigned c) {
+  const unsigned b = a.div_cpb.div(c);  // grid < 2^31 chunks
   ChunkPos P;
-  P.b = c / cpb;
-  P.q0 = static_cast<int>(c - P.b * cpb) * kCostQ;
+  P.b = b;
+  P.q0 = static_cast<int>(c - b * a.div_cpb.d) * kCostQ;
   P.qs = min(kCostQ, a.n - P.q0);
   P.s0 = P.b * a.n + P.q0;
   return P;
@@ -451,6 +458,10 @@ __device__ __forceinline__ void cost_consume(const CostArgs& a, CostSmem& S, con
     // batch's loads are recomputed by the partition kernel)
     const int* E = S.tk - L.fl;
     const int* F = S.tk + L.abase - L.afl;
+    // every lane in range (qs % 4 == 0): a sample's clamp, the chunk's wide /
+    // big flags and zero count from one running max and one compare per sample
+    const bool al8 = (reinterpret_cast<uintptr_t>(tok_out) & 7u) == 0;
+    unsigned mx = 0u;
     for (int j0 = 4 * tid; j0 < qs; j0 += 4 * kCostT) {  // qs % 4 == 0 when STAGED
       const int4 o = *reinterpret_cast<const int4*>(io_s + j0);
       DTB_CHECK(o.x - L.fl >= 0 && io_s[j0 + 4] - L.fl < L.abase);
@@ -464,9 +475,21 @@ __device__ __forceinline__ void cost_consume(const CostArgs& a, CostSmem& S, con
       }
       unsigned t4[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) t4[k] = static_cast<unsigned>(v[k]);  // in [0, 0x7fff * len]
-      store4(j0, t4);
+      for (int k = 0; k < 4; ++k) {
+        const unsigned t = static_cast<unsigned>(v[k]);  // in [0, 0x7fff * len]
+        mx = max(mx, t);
+        zeros += t == 0u;
+        t4[k] = min(t, 0x7fffu);
+      }
+      if (al8) {
+        *reinterpret_cast<uint2*>(tok_out + j0) = make_uint2(t4[0] | (t4[1] << 16), t4[2] | (t4[3] << 16));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) tok_out[j0 + k] = static_cast<unsigned short>(t4[k]);
+      }
     }
+    wide = mx > 0x7fffu;
+    big = mx >= 8192u;  // a clamped token (0x7fff) is big too
     auto span = [&](int lo, int hi) {  // tokens of local samples [lo, hi)
       int t = E[io_s[hi]] - E[io_s[lo]];
       if (audio) t += F[ao_s[hi]] - F[ao_s[lo]];
@@ -601,7 +624,9 @@ cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream) {
   // kernel's shared-memory opt-in)
   e = cudaFuncSetAttribute(cost_stream_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
-  cost_stream_kernel<<<static_cast<unsigned>(grid), kCostT, 0, stream>>>(a);
+  CostArgs k = a;
+  k.div_cpb = FastDiv::make(static_cast<unsigned>(cpb));
+  cost_stream_kernel<<<static_cast<unsigned>(grid), kCostT, 0, stream>>>(k);
   e = launch_pdl(cost_finalize_kernel, dim3(static_cast<unsigned>(a.n_batches)), dim3(kCostT), 0,
                  stream, a);
   if (e != cudaSuccess) return e;

@@ -81,6 +81,7 @@ struct CostArgs {
   double* load_after;
   unsigned char* kept;     // [n_batches] or null
   FastDiv div_pg;
+  FastDiv div_cpb;         // chunks per batch (set by launch_cost_stream)
   DevErr* err;             // a negative or >= 2^31 token sum (E_COST_RANGE)
 };
 size_t cost_scratch_bytes(long long n_batches, int m);  // blk_ident, bstat, list, state
