@@ -1660,7 +1660,11 @@ dtb_status dtb_reorder_stream(dtb_context* ctx, const dtb_cost_model* cm, const 
   CU(cudaEventRecord(ready, s));  // allocations + error reset are ordered first
   CU(cudaStreamWaitEvent(ctx->copy_in, ready, 0));
   CU(cudaStreamWaitEvent(ctx->copy_out, ready, 0));
-  const long long chunk = std::max<long long>(16, (n_batches + 7) / 8);
+#ifndef DTB_E2E_CHUNKS
+#define DTB_E2E_CHUNKS 8
+#endif
+  const long long chunk =
+      std::max<long long>(16, (n_batches + DTB_E2E_CHUNKS - 1) / DTB_E2E_CHUNKS);
   const long long n_chunks = n_batches > 0 ? (n_batches + chunk - 1) / chunk : 0;
   std::vector<cudaEvent_t> in_done(n_chunks), run_done(n_chunks);
   dtb_status st = DTB_OK;

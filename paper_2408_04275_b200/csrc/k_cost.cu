@@ -7,8 +7,8 @@
 // chunk of a batch is done — the keep decision of disaggregated_reorder
 // (src/reorder.cpp:340-354) whenever an averaging bound already settles it.
 //
-// One CTA of 128 threads per chunk of 1024 consecutive samples; ~25 KB of
-// shared memory, so eight CTAs share an SM and the pass streams at HBM rate.
+// One CTA of 128 threads per chunk of 1024 consecutive samples; ~20 KB of
+// shared memory, so eleven CTAs share an SM.
 // A chunk's CSR offsets and the CONTIGUOUS token spans its samples own
 // ([io[c0], io[c0 + 1024]) — a batch's tokens are one span of the CSR) are
 // brought in by bulk asynchronous copies (TMA, cp.async.bulk, completed on an
@@ -38,7 +38,7 @@ namespace dtb {
 #define DTB_COST_Q 1024
 #endif
 #ifndef DTB_COST_MINB
-#define DTB_COST_MINB 10
+#define DTB_COST_MINB 11
 #endif
 #ifndef DTB_COST_T
 #define DTB_COST_T 128
@@ -49,7 +49,10 @@ namespace dtb {
 constexpr int kCostT = DTB_COST_T;          // threads per chunk CTA
 constexpr int kCostQ = DTB_COST_Q;          // samples per chunk
 constexpr int kCostOff = kCostQ + 4;        // offsets + the next boundary, padded
-constexpr int kCostTok = 3 * kCostQ;        // token slots (image + audio + spares; ~2.1 per sample used)
+#ifndef DTB_COST_TOKQ
+#define DTB_COST_TOKQ 11
+#endif
+constexpr int kCostTok = DTB_COST_TOKQ * kCostQ / 4;  // token slots (image + audio + spares; ~2.1 per sample used)
 constexpr int kCostPer = kCostQ / kCostT;   // samples per thread
 
 struct CostSmem {
@@ -616,7 +619,10 @@ cudaError_t launch_cost_stream(const CostArgs& a, cudaStream_t stream) {
   // blk_ident, bstat and the list count are contiguous and zeroed here
   cudaError_t e = cudaMemsetAsync(a.blk_ident, 0, 4ull * (a.n_batches * (a.m + 4) + 1), stream);
   if (e != cudaSuccess) return e;
-  // all of the unified L1 / shared memory as shared: ten 21 KB chunk CTAs per SM
+  // all of the unified L1 / shared memory as shared: eleven 20.6 KB chunk CTAs
+  // per SM (token slots for 2.75 subsequences per sample: the mixed stream's
+  // chunks peak at 2.30, the dense stream's at 2.60; a chunk that does not fit
+  // sums its samples from global memory; ten 21.6 KB CTAs: 77.7 vs 76.3 µs)
   // (a persistent double-buffered variant — 5 CTAs of two stages per SM,
   // copies of chunk i + 1 in flight while chunk i computes — measured
   // slower: 95 µs at 128 threads, 101-105 µs at 256, vs 80 µs)
