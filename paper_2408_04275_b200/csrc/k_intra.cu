@@ -453,6 +453,10 @@ __device__ __noinline__ void kept_output(const FusedArgs& a, long long b, const 
   const bool desc = a.order == DTB_DESCENDING;
   const int cap = (n + m - 1) / m;
   const int capP = ((cap + 1) | 3) - 1;
+  // the output pointers in registers: stores through them cannot then force
+  // reloads of the (generic-addressed) kernel parameters every iteration
+  int* __restrict__ order_out = a.order_out + first;
+  unsigned short* __restrict__ tok_out = a.tok16_staged != nullptr ? a.tok16_staged + first : nullptr;
   for (int g = w; g < m; g += kFusedT / 32) {
     const int base = T.off[g], cnt = T.G.gcnt[g];
     for (int slot = lane; slot < cnt; slot += 32) {
@@ -460,10 +464,10 @@ __device__ __noinline__ void kept_output(const FusedArgs& a, long long b, const 
       DTB_CHECK(cells[g * capP + slot] < n);
       const unsigned item = kv[swz(cells[g * capP + slot])];
       DTB_CHECK(static_cast<int>(item & 0xffffu) < n);
-      a.order_out[first + base + slot] = static_cast<int>(item & 0xffffu);
-      if (a.tok16_staged != nullptr) {
+      order_out[base + slot] = static_cast<int>(item & 0xffffu);
+      if (tok_out != nullptr) {
         const unsigned k = item >> 16;
-        a.tok16_staged[first + base + slot] = static_cast<unsigned short>(desc ? 0x7fffu - k : k);
+        tok_out[base + slot] = static_cast<unsigned short>(desc ? 0x7fffu - k : k);
       }
     }
   }
@@ -1087,7 +1091,14 @@ intra_fused_kernel(const __grid_constant__ FusedArgs a) {
     }
     cl.sync();  // rank 1: its sorted items and (kept) rank 0's cells are ready
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 58] = globaltimer();
-    if (rank == 1 && S.deferred == q + 1) kept_output<0>(a, b, batch_kv(S));
+    if (rank == 1 && S.deferred == q + 1) {
+      if (a.prof && threadIdx.x == 0) a.prof[b * kProfSlots + 61] = globaltimer();
+      kept_output<0>(a, b, batch_kv(S));
+      if (a.prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) a.prof[b * kProfSlots + 60] = globaltimer();
+      }
+    }
     cl.sync();  // rank 1's shared memory is free for the next batch's cells
     if (a.prof && rank == 1 && threadIdx.x == 0) a.prof[b * kProfSlots + 59] = globaltimer();
     if (a.prof && rank == 0 && threadIdx.x == 0) a.prof[b * kProfSlots + 59] = globaltimer();

@@ -98,6 +98,11 @@ def main():
               f"first cluster sync {np.median(rel(58)):.1f} / {rel(58).max():.1f}; "
               f"second {np.median(rel(59)):.1f} / {rel(59).max():.1f} (from batch start)")
         kp = pi[:, 0] > 0
+        gap = rel(59) - rel(58)
+        for i in np.argsort(-gap)[:4]:  # the kept batches: rank 1 writes the order in between
+            print(f"    batch row {i}: first sync {rel(58)[i]:.1f}, second {rel(59)[i]:.1f}, "
+                  f"gap {gap[i]:.1f} us, outputs end {rel(5)[i]:.1f}"
+                  + (f", kept order written {rel(61)[i]:.1f} -> {rel(60)[i]:.1f}" if p[i, 60] > 0 else ""))
     ks = p[:, 56:61] * 0
     okk = ks[:, 0] > 0
     if okk.any():
